@@ -1,0 +1,296 @@
+"""Pins of the CPU oracle (oracle/fpck.py) against things other than itself.
+
+- hand-derived golden images (tests/golden/*.hex, written before the oracle);
+- published FNV-1a-64 test vectors;
+- closed forms fixed by the model definitions (16 B/param with GPT-3 shapes,
+  PAPER.md P:191-192) and the paper's Table 2 checkpoint sizes;
+- brute-force partition invariants;
+- an independent decoder round trip and library byte views.
+"""
+import hashlib
+import os
+import random
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import fpck
+from workloads import config_specs, gpt3_param_count, make_state
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def tbytes(t: torch.Tensor) -> bytes:
+    """Raw bytes of a tensor via torch/numpy library views (no method code)."""
+    return t.detach().contiguous().reshape(-1).view(torch.uint8).numpy().tobytes()
+
+
+def load_golden(name):
+    size = None
+    img = None
+    unknown = set()
+    extents = {}
+    with open(os.path.join(GOLDEN, name)) as f:
+        for line in f:
+            line = line.split("#", 1)[0].strip()
+            if not line:
+                continue
+            parts = line.split()
+            if parts[0] == "size":
+                size = int(parts[1])
+                img = bytearray(size)
+            elif parts[0] == "extents":
+                r, io, fo, n = int(parts[1]), *(int(x, 16) for x in parts[2:5])
+                extents.setdefault(r, []).append((io, fo, n))
+            else:
+                off = int(parts[0], 16)
+                for i, b in enumerate(parts[1:]):
+                    if b == "??":
+                        unknown.add(off + i)
+                    else:
+                        img[off + i] = int(b, 16)
+    return bytes(img), unknown, extents
+
+
+def u8(data):
+    return np.frombuffer(bytes(data), dtype=np.uint8)
+
+
+# ---------------------------------------------------------------------------
+def test_fnv1a64_published_vectors():
+    # FNV-1a 64-bit reference vectors (Fowler/Noll/Vo test suite).
+    assert fpck.fnv1a64(b"") == 0xCBF29CE484222325
+    assert fpck.fnv1a64(b"a") == 0xAF63DC4C8601EC8C
+    assert fpck.fnv1a64(b"foobar") == 0x85944171F73967E8
+
+
+def _check_golden(img, gold, unknown):
+    assert len(img) == len(gold)
+    diff = [i for i in range(len(img)) if i not in unknown and img[i] != gold[i]]
+    assert diff == [], f"first mismatches at {diff[:8]}"
+
+
+def test_golden_single_tensor():
+    gold, unknown, _ = load_golden("w_f32x2.hex")
+    w = torch.tensor([1.0, -2.0], dtype=torch.float32)
+    t = fpck.OTensor("w", "f32", "other", -1, (2,), tbytes(w))
+    lay = fpck.Layout([t], k=1)
+    img = lay.image()
+    _check_golden(img, gold, unknown)
+    # digest slot = FNV-1a-64 over (128-B entry table || names pool "w")
+    dg = int.from_bytes(img[48:56], "little")
+    assert dg == fpck.fnv1a64(img[64:192] + b"w")
+
+
+def test_golden_local_regions_k2():
+    gold, unknown, ext = load_golden("local_k2.hex")
+    a = fpck.OTensor("a", "u8", "other", -1, (3,), bytes([1, 2, 3]))
+    b = fpck.OTensor("b", "i32", "other", 0, (1,),
+                     tbytes(torch.tensor([0x11223344], dtype=torch.int32)))
+    lay = fpck.Layout([a], [[b], []], k=2)
+    img = lay.image()
+    _check_golden(img, gold, unknown)
+    assert int.from_bytes(img[48:56], "little") == fpck.fnv1a64(img[0x40:0xC0] + b"a")
+    assert int.from_bytes(img[0x2030:0x2038], "little") == \
+        fpck.fnv1a64(img[0x2040:0x20C0] + b"b")
+    got = fpck.shard_extents(lay)
+    assert {r: got[r] for r in range(2)} == {r: ext[r] for r in range(2)}
+    # shards concatenate back into the image
+    s0, s1 = fpck.shard_bytes(lay, 0), fpck.shard_bytes(lay, 1)
+    assert s0 == img[0:0x1000] + img[0x2000:0x4000]
+    assert s1 == img[0x1000:0x2000] + img[0x4000:0x5000]
+
+
+# ---------------------------------------------------------------------------
+# closed forms fixed by the models and Table 2
+# ---------------------------------------------------------------------------
+def _zeros(n):
+    return lambda off, m: b"\x00" * m
+
+
+def _layout_of(specs, k=1, by_rank=None):
+    rep = [fpck.OTensor(s.name, s.dtype, s.section, s.owner, s.shape, _zeros(s.nbytes))
+           for s in specs if s.owner < 0]
+    local = None
+    if by_rank is not None:
+        local = [[fpck.OTensor(s.name, s.dtype, s.section, s.owner, s.shape,
+                               _zeros(s.nbytes)) for s in sp if s.owner >= 0]
+                 for sp in by_rank]
+    return fpck.Layout(rep, local, k=k)
+
+
+def test_param_counts_match_model_definitions():
+    # GPT-3 XL (1.3B) in the Megatron layout, vocab padded to 50304
+    assert gpt3_param_count(2048, 24) == 1_315_819_520
+    assert abs(gpt3_param_count(4096, 32) / 6.7e9 - 1) < 0.01
+    assert abs(gpt3_param_count(5120, 40) / 13e9 - 1) < 0.02
+
+
+@pytest.mark.parametrize("d,L,table_gb", [(1536, 24, 10), (2048, 24, 17),
+                                          (2560, 32, 35), (4096, 32, 88),
+                                          (5140, 40, 173)])
+def test_14x_rule_vs_paper_table2(d, L, table_gb):
+    # "checkpoint size ... roughly 14X of the parameter count";
+    # Table 2 sizes match 14*P in GiB (reading R2); 13B with GPT-3's d=5140.
+    P = gpt3_param_count(d, L)
+    est = P * fpck.state_bytes_per_param("adam14") / 2**30
+    assert abs(est / table_gb - 1) < 0.035, (est, table_gb)
+
+
+def test_image_size_c1_closed_form():
+    lay = _layout_of(config_specs("c1_tiny"))
+    # 8 payloads padded to 4 KiB = 67,112,960 B, plus one header page
+    assert lay.image_bytes == 67_117_056
+    assert lay.header_bytes == 4096
+
+
+@pytest.mark.parametrize("cfg,d,L", [("c2_gpt3_1.3b", 2048, 24),
+                                     ("c3_gpt3_6.7b", 4096, 32)])
+def test_image_size_gpt3_is_16_bytes_per_param(cfg, d, L):
+    specs = config_specs(cfg)
+    lay = _layout_of(specs)
+    P = gpt3_param_count(d, L)
+    # GPT-3 shapes: every payload is a 4 KiB multiple -> zero padding, so the
+    # data region is exactly 16 B/param (adam16; BASELINE.json north_star).
+    assert lay.image_bytes - lay.header_bytes == 16 * P
+    assert lay.header_bytes % 4096 == 0
+    n = len(specs)
+    assert n == 5 * (12 * L + 4)
+    names = sum(len(s.name.encode()) for s in specs)
+    assert 64 + 128 * n + names <= lay.header_bytes < 64 + 128 * n + names + 4096
+
+
+def test_adam14_profile_drops_grads():
+    specs = config_specs("c2_gpt3_1.3b", profile="adam14")
+    lay = _layout_of(specs)
+    assert lay.image_bytes - lay.header_bytes == 14 * 1_315_819_520
+
+
+def test_zero_partitioned_c4_sizes():
+    k = 8
+    by_rank = [config_specs("c4_gpt3_13b_zero", r, k) for r in range(k)]
+    lay = _layout_of([], k=k, by_rank=by_rank)
+    P = gpt3_param_count(5120, 40)
+    data = sum(n for _, n in lay.regions) - sum(
+        fpck.header_len(len(sp), 0, sum(len(s.name.encode()) for s in sp), 4096)
+        for sp in by_rank)
+    # dim-0 shards of GPT-3 tensors: rows of 5120 fp32/bf16 are page multiples
+    # except the 1-D tensors, whose 640-element shards are padded.
+    assert data >= 16 * P
+    assert len(lay.regions) == k
+
+
+# ---------------------------------------------------------------------------
+# partition: brute force over all small cases
+# ---------------------------------------------------------------------------
+def test_partition_brute_force():
+    for Q in range(0, 65):
+        for k in range(1, 9):
+            parts = fpck.partition_units(Q, k)
+            assert len(parts) == k
+            cover = []
+            for s, n in parts:
+                cover.extend(range(s, s + n))
+            assert cover == list(range(Q))              # tiles [0,Q) exactly once
+            sizes = [n for _, n in parts]
+            assert max(sizes) - min(sizes) <= 1          # balance within 1 unit
+            assert sizes == sorted(sizes, reverse=True)  # extra units to low ranks
+            assert parts == fpck.partition_units(Q, k)   # deterministic
+
+
+def _rand_state(rng, n_rep, n_local, k):
+    dts = ["f32", "bf16", "u8", "i64", "f16"]
+    rep, local = [], [[] for _ in range(k)]
+    for i in range(n_rep):
+        dt = rng.choice(dts)
+        shape = tuple(rng.randint(0, 5000) for _ in range(rng.randint(0, 2)))
+        n = int(np.prod(shape)) if shape else 1
+        data = bytes(rng.getrandbits(8) for _ in range(n * fpck.ITEMSIZE[dt]))
+        rep.append(fpck.OTensor(f"r{i}", dt, rng.choice(list(fpck.SECTION_CODE)), -1,
+                                shape, data))
+    for j in range(n_local):
+        r = rng.randrange(k)
+        n = rng.randint(0, 9000)
+        local[r].append(fpck.OTensor(f"l{j}", "u8", "other", r, (n,),
+                                     bytes(rng.getrandbits(8) for _ in range(n))))
+    return rep, local
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_extents_tile_image_and_decode_roundtrip(seed, tmp_path):
+    rng = random.Random(seed)
+    k = rng.randint(1, 8)
+    rep, local = _rand_state(rng, rng.randint(0, 6), rng.randint(0, 5), k)
+    align = rng.choice([512, 4096])
+    lay = fpck.Layout(rep, local, k=k, align=align)
+    img = lay.image()
+    assert len(img) == lay.image_bytes and lay.image_bytes % align == 0
+    # every byte of the image in exactly one extent; file offsets contiguous
+    seen = np.zeros(lay.image_bytes, dtype=np.int32)
+    for ext in fpck.shard_extents(lay):
+        fo = 0
+        for io, f, n in ext:
+            assert f == fo and io % align == 0 and n % align == 0
+            seen[io:io + n] += 1
+            fo += n
+    assert (seen == 1).all()
+    # independent decoder recovers every tensor bit for bit (load(save(x)) == x)
+    dec = fpck.decode(img)
+    assert [(t["name"], t["data"], t["shape"], t["dtype"]) for t in dec["replicated"]] == \
+        [(t.name, t.read(0, t.nbytes), t.shape, t.dtype) for t in rep]
+    for r in range(k):
+        got = dec["local"].get(r, [])
+        assert [(t["name"], t["data"], t["owner"]) for t in got] == \
+            [(t.name, t.read(0, t.nbytes), r) for t in local[r]]
+    # oracle save -> files -> assemble == image; sha per shard matches
+    shas = fpck.save(lay, str(tmp_path))
+    paths = [str(tmp_path / fpck.shard_name(r, k)) for r in range(k)]
+    assert fpck.assemble(paths, fpck.shard_extents(lay), lay.image_bytes) == img
+    for r in range(k):
+        with open(paths[r], "rb") as f:
+            assert hashlib.sha256(f.read()).hexdigest() == shas[r]
+
+
+def test_payloads_are_library_byte_views_and_padding_is_zero():
+    specs = config_specs("c1_tiny")
+    state = make_state(specs, "cpu")
+    ts = [fpck.OTensor(s.name, s.dtype, s.section, s.owner, s.shape, tbytes(t))
+          for s, t in state]
+    lay = fpck.Layout(ts)
+    img = u8(lay.image())
+    dec = fpck.decode(img.tobytes())
+    for (s, t), d in zip(state, dec["replicated"]):
+        assert d["data"] == t.contiguous().reshape(-1).view(torch.uint8).numpy().tobytes()
+        assert d["shape"] == tuple(t.shape)
+    # bytes between payloads are zero: total nonzero-capable bytes = header + data
+    mask = np.zeros(len(img), dtype=bool)
+    mask[:lay.header_bytes] = True
+    for off, t in zip(lay.rep_offsets, ts):
+        mask[off:off + t.nbytes] = True
+    assert not img[~mask].any()
+
+
+def test_determinism_two_builds_identical():
+    specs = config_specs("gpt3_small")
+    st = make_state(specs, "cpu")
+    shas = []
+    for _ in range(2):
+        ts = [fpck.OTensor(s.name, s.dtype, s.section, s.owner, s.shape, tbytes(t))
+              for s, t in st]
+        lay = fpck.Layout(ts, k=3)
+        shas.append([fpck.shard_sha256(lay, r) for r in range(3)])
+    assert shas[0] == shas[1]
+
+
+def test_corruption_detected_by_decoder():
+    w = fpck.OTensor("w", "f32", "other", -1, (2,), b"\x00" * 8)
+    img = bytearray(fpck.Layout([w]).image())
+    img[100] ^= 1           # inside the entry table -> digest mismatch
+    with pytest.raises(ValueError):
+        fpck.decode(bytes(img))
+
+
+def test_required_bandwidth_eq1():
+    # Eq. 1: 107 GB over a 4.28 s fwd+bwd window needs 25 GB/s
+    assert fpck.required_bandwidth(107e9, 2.14, 2.14) == pytest.approx(25e9, rel=1e-3)
