@@ -1,0 +1,206 @@
+/*
+ * fastpersist.h — C-ABI of the B200-native FastPersist checkpoint-write path.
+ *
+ * The calls follow the paper's problem statement (PAPER.md, arXiv 2406.13768):
+ *   - the checkpoint is written after the optimizer and overlapped with the
+ *     next iteration's forward/backward, "blocks before optimizer to receive
+ *     confirmation of the completion of the previous checkpoint" (§4.3,
+ *     P:511-515)                                       -> fp_ckpt_begin / fp_ckpt_wait
+ *   - each DP rank writes only its portion of the (replicated) checkpoint,
+ *     partitioned at setup, byte-balanced after serialization (§4.2,
+ *     P:483-503)                                        -> dp_rank / dp_size
+ *   - "Loading parallel checkpoints ... loads its checkpoint partition"
+ *     (§4.2)                                     -> fp_ckpt_load
+ *   - NVMe-optimised async I/O, DMA-able page-locked double buffering, aligned
+ *     writes (§4.1)                          -> fp_config
+ * The on-disk image is FPCK v2.
+ *
+ * Conventions
+ *   - Every int-returning call returns 0 on success or a NEGATIVE error:
+ *     -errno (EINVAL, ENOMEM, EBUSY, EIO, ENOSPC, ENOENT, ...) or an FP_E* code.
+ *   - No call throws; no call aborts the process on bad input.
+ *   - Pointers passed in are borrowed; nothing is freed by the library
+ *     except what it allocated itself (ctx, pinned ring, device slab).
+ *   - No torch types: plain pointers, sizes and an opaque cudaStream_t.
+ */
+#ifndef FASTPERSIST_H
+#define FASTPERSIST_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FP_ABI_VERSION 1
+
+/* ---- error codes beyond -errno ----------------------------------------- */
+#define FP_EMISMATCH (-1001) /* layout differs across ranks, or load target != file */
+#define FP_ECORRUPT  (-1002) /* manifest / header / extent inconsistent on load     */
+#define FP_ECUDA     (-1003) /* a CUDA runtime call failed                           */
+#define FP_ENODEV    (-1004) /* device tensors given but no CUDA device in this ctx  */
+#define FP_ECOMM     (-1005) /* a comm callback returned an error                    */
+
+/* ---- tensor metadata ("data type, data size, originating device") - */
+enum fp_dtype { FP_F32 = 1, FP_BF16 = 2, FP_F16 = 3, FP_F64 = 4, FP_I64 = 5,
+                FP_I32 = 6, FP_U8 = 7 };
+enum fp_section { FP_SEC_PARAM = 0, FP_SEC_GRAD = 1, FP_SEC_MASTER = 2,
+                  FP_SEC_EXP_AVG = 3, FP_SEC_EXP_AVG_SQ = 4, FP_SEC_OTHER = 5 };
+
+#define FP_TENSOR_HOST 1u   /* data is a host pointer (host-resident state).     */
+
+typedef struct fp_tensor {
+  const void *data;   /* device pointer (or host pointer with FP_TENSOR_HOST);
+                         contiguous bytes [data, data+nbytes). Borrowed: must stay
+                         alive and UNMODIFIED from fp_ckpt_begin until
+                         fp_ckpt_wait returns (the optimizer fence).
+                         Any alignment is accepted; 16-B alignment takes the
+                         vector/TMA fast path.                                  */
+  uint64_t nbytes;    /* = numel * itemsize(dtype), else -EINVAL                 */
+  const char *name;   /* UTF-8, NUL-terminated, 1..65535 bytes                    */
+  int64_t shape[8];   /* first ndim entries used                                 */
+  int32_t owner;      /* -1: replicated on all DP ranks (byte-range sharded,
+                         P:485); r >= 0: rank r's own partition (ZeRO shard /
+                         local experts), written whole by rank r; must equal
+                         the caller's dp_rank                                    */
+  uint8_t dtype;      /* enum fp_dtype   */
+  uint8_t section;    /* enum fp_section */
+  uint8_t ndim;       /* 0..8            */
+  uint8_t flags;      /* FP_TENSOR_*     */
+} fp_tensor;
+
+/* ---- collectives supplied by the caller (torch.distributed NCCL group) -----
+ * Called ONLY on the caller's thread, inside fp_ckpt_begin (first call for a
+ * new tensor signature: all-gather of per-rank sizes + layout digest)
+ * and fp_ckpt_wait (status all-reduce = completion barrier). Return 0 or <0. */
+typedef struct fp_comm {
+  void *ctx;
+  /* send: n_per_rank values; recv: dp_size * n_per_rank values, rank-major   */
+  int (*allgather_u64)(void *ctx, const uint64_t *send, uint64_t *recv,
+                       uint64_t n_per_rank);
+  /* in-place MIN over ranks                                                  */
+  int (*allreduce_min_i32)(void *ctx, int32_t *inout);
+} fp_comm;
+
+/* ---- configuration ------------------------------------------------------ */
+enum fp_io_engine { FP_IO_URING = 0,    /* io_uring, O_DIRECT, registered bufs */
+                    FP_IO_PWRITE = 1,   /* pwrite thread pool, O_DIRECT         */
+                    FP_IO_BUFFERED = 2  /* pwrite through the page cache        */ };
+enum fp_pack_impl { FP_PACK_V4 = 0,     /* LSU 16-B vector gather               */
+                    FP_PACK_BULK = 1    /* cp.async.bulk (TMA engine) via smem   */ };
+
+#define FP_CFG_NO_FSYNC 1u     /* skip fdatasync (benchmark ablation only)       */
+
+typedef struct fp_config {
+  uint32_t ring_slots;   /* pinned host slots; 2 = the paper's double buffer
+                            (P:473); default 4                                   */
+  uint32_t io_depth;     /* max in-flight I/O requests per rank; default 64      */
+  uint64_t slot_bytes;   /* bytes per slot = one chunk; multiple of alignment;
+                            default 64 MiB                                       */
+  uint32_t sqe_bytes;    /* bytes per write request; default 1 MiB               */
+  uint32_t alignment;    /* power of two >= 512; default 4096           */
+  uint32_t io_engine;    /* enum fp_io_engine; default FP_IO_URING              */
+  uint32_t pack_impl;    /* enum fp_pack_impl; default FP_PACK_V4               */
+  uint32_t pack_ctas;    /* 0 = whole GPU (burst); else CTA cap (background)    */
+  uint32_t flags;        /* FP_CFG_*                                             */
+  const char *dirs;      /* nullable: comma-separated roots; rank r's shard goes
+                            under dirs[r % n]; the manifest under dirs[0].
+                            NULL: `path` is used as given.                       */
+} fp_config;
+
+/* ---- per-checkpoint statistics ------------------------------------------ */
+typedef struct fp_stats {
+  uint64_t image_bytes;    /* whole FPCK image (all ranks)                       */
+  uint64_t header_bytes;   /* GHDR bytes                                          */
+  uint64_t shard_bytes;    /* bytes this rank wrote                               */
+  uint64_t chunks;         /* ring chunks this rank staged                        */
+  uint64_t io_requests;    /* write requests submitted                            */
+  uint64_t pack_launches;  /* pack kernel launches                                */
+  uint64_t pack_bytes;     /* slab bytes produced by those launches               */
+  double   pack_ms;        /* sum of CUDA-event durations of the pack launches    */
+  double   d2h_ms;         /* sum of CUDA-event durations of the D2H copies       */
+  double   t_total;        /* s, begin -> wait return (incl. barrier + commit)    */
+  double   t_helper;       /* s, helper start -> local durability                 */
+  double   t_fsync;        /* s, fdatasync                                        */
+  double   t_barrier;      /* s, status all-reduce in wait                        */
+  double   t_commit;       /* s, manifest write + rename + dir fsync (rank 0)     */
+  double   t_io_stall;     /* s, helper time blocked waiting for I/O completions  */
+  uint32_t max_inflight;   /* peak in-flight I/O requests                         */
+  uint32_t fallback;       /* 1 if O_DIRECT was unavailable -> buffered I/O       */
+  int32_t  engine;         /* enum fp_io_engine actually used                     */
+  int32_t  status;         /* final status of this checkpoint                     */
+  int64_t  err_offset;     /* file offset of the first failed request, or -1      */
+} fp_stats;
+
+typedef struct fp_ctx fp_ctx;
+
+/* Fill *cfg with the defaults above (env overrides: FP_RING_SLOTS,
+ * FP_SLOT_BYTES, FP_SQE_BYTES, FP_QD, FP_IO_ENGINE=uring|pwrite|buffered,
+ * FP_PACK=v4|bulk, FP_PACK_CTAS, FP_ALIGN). Returns 0.                        */
+int fp_config_default(fp_config *cfg);
+
+/* Create a context bound to CUDA device `cuda_device` (-1: host tensors only).
+ * Allocates the pinned ring (slots*slot_bytes, page-locked and registered with
+ * the I/O engine), one device slab of slot_bytes, a low-priority CUDA stream and
+ * the helper thread. `comm` may be NULL only if every call uses dp_size == 1.
+ * *out receives the context. Errors: -EINVAL (bad config), -ENOMEM, FP_ECUDA. */
+int fp_ckpt_init(const fp_config *cfg, int cuda_device, const fp_comm *comm,
+                 fp_ctx **out);
+
+/* Start checkpoint `path` (a directory; created if missing) of the tensor list
+ * t[0..n) — caller order is image order (P:479 order preserved). Returns after
+ * enqueueing (microseconds when the tensor signature is unchanged); the first
+ * pack kernel waits on an event recorded on `producer_stream` (cudaStream_t;
+ * NULL = legacy default stream), so it sees the optimizer's writes.
+ * On a new signature this call runs the layout + partition setup, including
+ * one comm->allgather_u64 (collective: all ranks must call begin together).
+ * Rank r writes `<path>/shard-<r>-of-<dp_size>.fpck`.
+ * Errors: -EINVAL (bad tensor, owner != dp_rank, dp_rank >= dp_size, mixed
+ * host/device tensors), -EBUSY (a checkpoint is outstanding: at most one,
+ * S:361), FP_EMISMATCH (replicated layouts differ across ranks), FP_ENODEV,
+ * FP_ECOMM, -ENOMEM.                                                          */
+int fp_ckpt_begin(fp_ctx *ctx, const fp_tensor *t, size_t n, const char *path,
+                  int dp_rank, int dp_size, void *producer_stream);
+
+/* Block until the outstanding checkpoint is durable everywhere: this rank's
+ * shard is fdatasync'd, the status all-reduce (barrier) has completed, and
+ * rank 0 has committed manifest.json (tmp + rename + dir fsync). Collective
+ * when dp_size > 1. Returns 0 if nothing is outstanding. On any rank's failure
+ * every rank returns that (most negative) error and no manifest is committed.
+ * `out` (nullable) receives the statistics.                                    */
+int fp_ckpt_wait(fp_ctx *ctx, fp_stats *out);
+
+/* Restore tensors t[0..n) (same names/dtypes/shapes/order as saved, each
+ * rank passing its own local tensors) from checkpoint `path` written with
+ * the same dp_size. Reads the manifest, validates every header against the
+ * target list, O_DIRECT-reads the needed extents through the pinned ring and
+ * scatters them into t[i].data with the unpack kernel on `stream`. Synchronous.
+ * Errors: -ENOENT (missing manifest or shard, named on stderr), FP_ECORRUPT,
+ * FP_EMISMATCH, -EIO, -EBUSY (a save is outstanding).                         */
+int fp_ckpt_load(fp_ctx *ctx, const fp_tensor *t, size_t n, const char *path,
+                 int dp_rank, int dp_size, void *stream);
+
+/* Image facts of the last planned checkpoint of this ctx: image/header bytes and
+ * this rank's extents as (image_offset, file_offset, length) triples.
+ * *n_ext receives the extent count; at most max_ext are written. -ENOENT if
+ * nothing was planned yet.                                                    */
+int fp_ckpt_plan_info(fp_ctx *ctx, uint64_t *image_bytes, uint64_t *header_bytes,
+                      uint64_t *extents, uint32_t max_ext, uint32_t *n_ext);
+
+/* Release everything (waits for an outstanding checkpoint first).            */
+void fp_ckpt_destroy(fp_ctx *ctx);
+
+/* Human-readable text for a return code (static storage).                    */
+const char *fp_strerror(int err);
+
+/* Storage roofline tool (the built-in substitute for fio): write
+ * `bytes` of host data to `<dir>/fp_iobench.<tag>` with the configured engine
+ * (O_DIRECT, io_depth x sqe_bytes), fdatasync, unlink; *gbps = bytes / time.  */
+int fp_io_bench(const char *dir, uint64_t bytes, const fp_config *cfg, int tag,
+                double *gbps);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASTPERSIST_H */

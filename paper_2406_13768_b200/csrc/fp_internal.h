@@ -1,0 +1,140 @@
+// Internal declarations of libfastpersist (not part of the C-ABI).
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "fastpersist.h"
+
+namespace fp {
+
+// ---------------------------------------------------------------------------
+// FPCK v2 layout constants
+// ---------------------------------------------------------------------------
+constexpr uint32_t kVersion = 2;
+constexpr uint64_t kFixedHdr = 64;
+constexpr uint64_t kEntry = 128;
+constexpr uint64_t kRegion = 16;
+constexpr uint32_t kFlagHasLocal = 1;
+constexpr uint32_t kFlagLocal = 2;
+
+inline uint64_t round_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+int dtype_size(uint8_t dtype);  // 0 if unknown
+uint64_t fnv1a64(const uint8_t* p, size_t n, uint64_t h = 0xCBF29CE484222325ull);
+
+struct TensorRef {
+  uint64_t ptr;      // device or host address
+  uint64_t nbytes;
+  std::string name;
+  int64_t shape[8];
+  int32_t owner;
+  uint8_t dtype, section, ndim, flags;
+};
+
+// Validate + copy the caller's tensor table. Returns 0 or -EINVAL.
+int import_tensors(const fp_tensor* t, size_t n, int dp_rank, std::vector<TensorRef>* rep,
+                   std::vector<TensorRef>* loc, bool* host);
+
+// One header (GHDR or LREG): encoded bytes + payload offsets.
+struct Header {
+  std::vector<uint8_t> bytes;
+  uint64_t digest = 0;
+};
+uint64_t header_len(uint64_t n_tensors, uint64_t n_regions, uint64_t names_bytes, uint64_t align);
+void encode_header(const std::vector<TensorRef>& ts, const std::vector<uint64_t>& offs,
+                   const std::vector<std::pair<uint64_t, uint64_t>>& regions, uint32_t align,
+                   uint64_t total_bytes, int64_t owner, uint32_t flags, Header* out);
+
+struct Extent {
+  uint64_t image_off, file_off, len;
+};
+
+// A contiguous run of image bytes with a single source.
+struct Piece {
+  uint64_t image_off;
+  uint64_t len;
+  uint64_t src;  // address (device or host); 0 = zero fill
+};
+
+// Everything rank `rank` needs to write (or read) its shard.
+struct Plan {
+  uint32_t align = 4096;
+  int rank = 0, k = 1;
+  uint64_t header_bytes = 0, rep_bytes = 0, image_bytes = 0, digest = 0;
+  std::vector<std::pair<uint64_t, uint64_t>> regions;  // (offset, bytes) per rank or empty
+  Header ghdr, lhdr;
+  std::vector<uint64_t> rep_off, loc_off;
+  std::vector<Extent> extents;  // this rank, image order
+  uint64_t shard_bytes = 0;
+  // sources of this rank's image bytes, sorted by image_off (header sources
+  // point at hdr_base + offset: device copy of ghdr||lhdr, or the host copy)
+  std::vector<Piece> pieces;
+};
+
+// Layout pass 1 (local): replicated header + offsets, and what this rank
+// contributes to the all-gather: {local_region_bytes, n_local, digest}.
+struct LocalFacts {
+  uint64_t region_bytes, n_local, digest, rep_bytes;
+};
+void plan_local_facts(const std::vector<TensorRef>& rep, const std::vector<TensorRef>& loc,
+                      uint32_t align, LocalFacts* out);
+// Layout pass 2: needs all ranks' facts (k entries). Returns 0 / FP_EMISMATCH.
+int plan_build(const std::vector<TensorRef>& rep, const std::vector<TensorRef>& loc,
+               uint32_t align, int rank, int k, const std::vector<LocalFacts>& all, Plan* out);
+// Rebase header pieces onto hdr_base (ghdr at +0, lhdr at +ghdr.size());
+// hdr_base == 0 turns header pieces into skip (zero) items, as load needs.
+void plan_pieces(Plan* p, const std::vector<TensorRef>& rep, const std::vector<TensorRef>& loc,
+                 uint64_t hdr_base);
+
+// Work items of the pack/unpack kernels: one tile of <= kTile bytes.
+constexpr uint32_t kTile = 32768;
+struct Item {
+  uint64_t src;  // gather source (0 = zero fill); for unpack: scatter destination
+  uint32_t dst;  // byte offset inside the slab
+  uint32_t len;  // <= kTile
+};
+static_assert(sizeof(Item) == 16, "Item must be 16 bytes");
+
+// Items for every chunk of the shard file (chunk = slot_bytes of file bytes).
+// item_lo has n_chunks+1 entries.
+void plan_items(const Plan& p, uint64_t slot_bytes, std::vector<Item>* items,
+                std::vector<uint32_t>* item_lo);
+
+// ---------------------------------------------------------------------------
+// I/O engines
+// ---------------------------------------------------------------------------
+struct IoDone {
+  uint64_t user;
+  int32_t res;
+};
+
+class IoEngine {
+ public:
+  virtual ~IoEngine() {}
+  virtual int kind() const = 0;
+  // Optional fixed-buffer registration (io_uring). 0 or -errno (non-fatal).
+  virtual int register_buffers(void* base, uint64_t slot_bytes, uint32_t slots) { return -1; }
+  // Queue one request (buf_index >= 0: registered slot). 0 or -errno.
+  virtual int queue(bool write, int fd, void* buf, uint32_t len, uint64_t off, int buf_index,
+                    uint64_t user) = 0;
+  virtual int submit() = 0;                                 // push queued requests
+  virtual int reap(IoDone* out, int max, int min_wait) = 0;  // >= 0 count or -errno
+  virtual int fdatasync(int fd) = 0;
+  virtual uint32_t capacity() const = 0;
+};
+
+IoEngine* make_uring(uint32_t depth, int* err);
+IoEngine* make_pwrite(uint32_t threads, bool direct);
+
+// ---------------------------------------------------------------------------
+// kernels (pack.cu)
+// ---------------------------------------------------------------------------
+int pack_launch(int impl, const Item* d_items, uint32_t n_items, uint8_t* d_slab, int ctas,
+                void* stream);
+int unpack_launch(const Item* d_items, uint32_t n_items, const uint8_t* d_slab, int ctas,
+                  void* stream);
+int pack_default_ctas(int impl, int device);
+
+}  // namespace fp

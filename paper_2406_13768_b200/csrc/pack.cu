@@ -1,0 +1,264 @@
+// Pack / unpack kernels for sm_100a.
+//
+// The pack kernel gathers one chunk of this rank's shard — fragments of many
+// device tensors (bf16 params/grads, fp32 master/m/v), header pages and zero
+// padding — into a contiguous, alignment-padded device slab that the copy
+// engine then moves to a pinned host ring slot (§4.1: GPU ->
+// page-locked CPU memory -> NVMe, double buffered; the paper moved each
+// serialized tensor separately, §5.1). Work arrives as a flat list
+// of <= 32 KiB items {src, slab offset, len} precomputed on the host at setup
+// (the partition is fixed before the first iteration), so the kernels
+// do no searching: they are pure HBM streams (1 B read + 1 B written per image
+// byte).
+//
+//  fp_pack_v4   : LSU path. 16-B vector loads (ld.global.nc.L1::no_allocate)
+//                 and stores, 8 loads in flight per thread, co-aligned
+//                 head/body/tail handling; byte path for mutually misaligned
+//                 pointers (odd storage offsets).
+//  fp_pack_bulk : TMA-engine path. One elected thread per CTA streams items
+//                 through a 6-stage shared-memory ring with
+//                 cp.async.bulk (G2S, mbarrier complete_tx) and
+//                 cp.async.bulk (S2G, bulk_group); the other warps handle
+//                 zero fill, vector tails and misaligned items with the LSU.
+//  fp_unpack_v4 : load path, slab -> tensors (zero items skipped).
+#include <cuda_runtime.h>
+
+#include <cerrno>
+#include <cstdint>
+
+#include "fp_internal.h"
+
+namespace fp {
+namespace {
+
+constexpr int kV4Threads = 256;
+constexpr int kV4Unroll = 8;  // 256 thr x 8 x 16 B = 32 KiB = kTile per pass
+
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_v4(uint4* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+// Copy `len` bytes src -> dst with `nthr` threads (index t). src == nullptr
+// means zero fill. Vector body when src and dst share the same 16-B phase.
+__device__ __forceinline__ void copy_bytes(uint8_t* __restrict__ dst,
+                                           const uint8_t* __restrict__ src, uint32_t len,
+                                           int t, int nthr) {
+  const uint32_t phase = (uint32_t)((uintptr_t)dst & 15);
+  const bool coaligned = !src || (((uintptr_t)src & 15) == phase);
+  if (!coaligned) {
+    for (uint32_t i = t; i < len; i += nthr) dst[i] = src[i];
+    return;
+  }
+  uint32_t head = (16 - phase) & 15;
+  if (head > len) head = len;
+  if ((uint32_t)t < head) dst[t] = src ? src[t] : 0;
+  const uint32_t n16 = (len - head) >> 4;
+  uint4* d16 = reinterpret_cast<uint4*>(dst + head);
+  if (src) {
+    const uint4* s16 = reinterpret_cast<const uint4*>(src + head);
+    for (uint32_t base = 0; base < n16; base += (uint32_t)nthr * kV4Unroll) {
+      uint4 v[kV4Unroll];
+#pragma unroll
+      for (int u = 0; u < kV4Unroll; ++u) {
+        const uint32_t j = base + (uint32_t)u * nthr + t;
+        if (j < n16) v[u] = ld_stream(s16 + j);
+      }
+#pragma unroll
+      for (int u = 0; u < kV4Unroll; ++u) {
+        const uint32_t j = base + (uint32_t)u * nthr + t;
+        if (j < n16) st_v4(d16 + j, v[u]);
+      }
+    }
+  } else {
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    for (uint32_t j = t; j < n16; j += nthr) st_v4(d16 + j, z);
+  }
+  const uint32_t done = head + (n16 << 4);
+  const uint32_t tail = len - done;
+  if ((uint32_t)t < tail) dst[done + t] = src ? src[done + t] : 0;
+}
+
+__global__ void __launch_bounds__(kV4Threads) fp_pack_v4(const Item* __restrict__ items,
+                                                         uint32_t n, uint8_t* __restrict__ slab) {
+  for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const Item it = items[i];
+    copy_bytes(slab + it.dst, reinterpret_cast<const uint8_t*>(it.src), it.len, threadIdx.x,
+               kV4Threads);
+  }
+}
+
+__global__ void __launch_bounds__(kV4Threads) fp_unpack_v4(const Item* __restrict__ items,
+                                                           uint32_t n,
+                                                           const uint8_t* __restrict__ slab) {
+  for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const Item it = items[i];
+    if (!it.src) continue;  // padding: nothing to restore
+    copy_bytes(reinterpret_cast<uint8_t*>(it.src), slab + it.dst, it.len, threadIdx.x,
+               kV4Threads);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// bulk-async (TMA engine) variant
+// ---------------------------------------------------------------------------
+constexpr int kBulkStages = 6;
+constexpr int kBulkThreads = 128;
+constexpr uint32_t kBulkStageBytes = kTile;  // one item per stage
+constexpr size_t kBulkSmem = (size_t)kBulkStages * kBulkStageBytes + kBulkStages * 16;
+
+__device__ __forceinline__ bool bulk_ok(const Item& it) {
+  return it.src && !(it.src & 15) && !(it.dst & 15) && it.len >= 16;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__global__ void __launch_bounds__(kBulkThreads, 1)
+    fp_pack_bulk(const Item* __restrict__ items, uint32_t n, uint8_t* __restrict__ slab) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + (size_t)kBulkStages * kBulkStageBytes);
+  uint32_t* st_dst = reinterpret_cast<uint32_t*>(mbar + kBulkStages);
+  uint32_t* st_len = st_dst + kBulkStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // contiguous item range of this CTA
+  const uint32_t lo = (uint32_t)(((uint64_t)n * blockIdx.x) / gridDim.x);
+  const uint32_t hi = (uint32_t)(((uint64_t)n * (blockIdx.x + 1)) / gridDim.x);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kBulkStages; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // warp 0 walks the items 32 at a time (one coalesced descriptor load per
+    // lane); lane 0 alone issues the bulk copies.
+    uint32_t issued = 0, stored = 0;
+    auto store_one = [&]() {
+      const uint32_t s = stored % kBulkStages;
+      const uint32_t parity = (stored / kBulkStages) & 1;
+      const uint32_t bar = smem_u32(&mbar[s]);
+      asm volatile(
+          "{\n"
+          ".reg .pred p;\n"
+          "WAIT_%=:\n"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+          "@!p bra WAIT_%=;\n"
+          "}\n" ::"r"(bar),
+          "r"(parity)
+          : "memory");
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                       slab + st_dst[s]),
+                   "r"(smem_u32(smem + (size_t)s * kBulkStageBytes)), "r"(st_len[s])
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      ++stored;
+    };
+    for (uint32_t b = lo; b < hi; b += 32) {
+      Item mine = {0, 0, 0};
+      if (b + lane < hi) mine = items[b + lane];
+      uint32_t mask = __ballot_sync(0xffffffffu, b + lane < hi && bulk_ok(mine));
+      while (mask) {
+        const int j = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const uint64_t src = __shfl_sync(0xffffffffu, mine.src, j);
+        const uint32_t dst = __shfl_sync(0xffffffffu, mine.dst, j);
+        const uint32_t len = __shfl_sync(0xffffffffu, mine.len, j);
+        if (lane == 0) {
+          // keep <= kBulkStages-1 loads in flight: one stage of slack lets
+          // the most recent store still be reading shared memory
+          while (issued - stored >= (uint32_t)kBulkStages - 1) store_one();
+          const uint32_t s = issued % kBulkStages;
+          if (issued >= (uint32_t)kBulkStages)
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          const uint32_t bytes = len & ~15u;
+          st_dst[s] = dst;
+          st_len[s] = bytes;
+          const uint32_t bar = smem_u32(&mbar[s]);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                       "r"(bytes)
+                       : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
+              "%2, [%3];" ::"r"(smem_u32(smem + (size_t)s * kBulkStageBytes)),
+              "l"(src), "r"(bytes), "r"(bar)
+              : "memory");
+          ++issued;
+        }
+      }
+    }
+    if (lane == 0) {
+      while (stored < issued) store_one();
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+  } else {
+    // LSU warps: zero fill, misaligned items, and the <16 B vector tails
+    const int t = threadIdx.x - 32, nthr = kBulkThreads - 32;
+    for (uint32_t i = lo; i < hi; ++i) {
+      const Item it = items[i];
+      if (bulk_ok(it)) {
+        const uint32_t body = it.len & ~15u;
+        if (body < it.len && t < (int)(it.len - body))
+          slab[it.dst + body + t] = reinterpret_cast<const uint8_t*>(it.src)[body + t];
+      } else {
+        copy_bytes(slab + it.dst, reinterpret_cast<const uint8_t*>(it.src), it.len, t, nthr);
+      }
+    }
+  }
+}
+
+int sm_count(int device) {
+  int d = device;
+  if (d < 0 && cudaGetDevice(&d) != cudaSuccess) return 148;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || n <= 0)
+    return 148;
+  return n;
+}
+
+}  // namespace
+
+int pack_default_ctas(int impl, int device) {
+  const int sms = sm_count(device);
+  return impl == FP_PACK_BULK ? sms : sms * 4;
+}
+
+int pack_launch(int impl, const Item* d_items, uint32_t n_items, uint8_t* d_slab, int ctas,
+                void* stream) {
+  if (!n_items) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int grid = (int)((uint32_t)ctas < n_items ? (uint32_t)ctas : n_items);
+  if (impl == FP_PACK_BULK) {
+    static bool attr_set = false;
+    if (!attr_set) {
+      if (cudaFuncSetAttribute(fp_pack_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kBulkSmem) != cudaSuccess)
+        return FP_ECUDA;
+      attr_set = true;
+    }
+    fp_pack_bulk<<<grid, kBulkThreads, kBulkSmem, st>>>(d_items, n_items, d_slab);
+  } else {
+    fp_pack_v4<<<grid, kV4Threads, 0, st>>>(d_items, n_items, d_slab);
+  }
+  return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
+}
+
+int unpack_launch(const Item* d_items, uint32_t n_items, const uint8_t* d_slab, int ctas,
+                  void* stream) {
+  if (!n_items) return 0;
+  const int grid = (int)((uint32_t)ctas < n_items ? (uint32_t)ctas : n_items);
+  fp_unpack_v4<<<grid, kV4Threads, 0, (cudaStream_t)stream>>>(d_items, n_items, d_slab);
+  return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
+}
+
+}  // namespace fp

