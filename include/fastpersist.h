@@ -91,6 +91,8 @@ enum fp_pack_impl { FP_PACK_V4 = 0,     /* LSU 16-B vector gather               
                     FP_PACK_BULK = 1    /* cp.async.bulk (TMA engine) via smem   */ };
 
 #define FP_CFG_NO_FSYNC 1u     /* skip fdatasync (benchmark ablation only)       */
+#define FP_CFG_PRIO_LOW 2u     /* pack/D2H stream at the least priority (default:
+                                  greatest)                    */
 
 typedef struct fp_config {
   uint32_t ring_slots;   /* pinned host slots; 2 = the paper's double buffer
@@ -107,6 +109,10 @@ typedef struct fp_config {
   const char *dirs;      /* nullable: comma-separated roots; rank r's shard goes
                             under dirs[r % n]; the manifest under dirs[0].
                             NULL: `path` is used as given.                       */
+  uint64_t pack_bytes;   /* bytes gathered per pack-kernel launch (device slab
+                            size); rounded up to a multiple of slot_bytes, so one
+                            launch feeds pack_bytes/slot_bytes ring slots; 0 =
+                            slot_bytes; default 256 MiB, max 2 GiB             */
 } fp_config;
 
 /* ---- per-checkpoint statistics ------------------------------------------ */
@@ -137,12 +143,12 @@ typedef struct fp_ctx fp_ctx;
 
 /* Fill *cfg with the defaults above (env overrides: FP_RING_SLOTS,
  * FP_SLOT_BYTES, FP_SQE_BYTES, FP_QD, FP_IO_ENGINE=uring|pwrite|buffered,
- * FP_PACK=v4|bulk, FP_PACK_CTAS, FP_ALIGN). Returns 0.                        */
+ * FP_PACK=v4|bulk, FP_PACK_CTAS, FP_ALIGN, FP_PACK_BYTES). Returns 0.         */
 int fp_config_default(fp_config *cfg);
 
 /* Create a context bound to CUDA device `cuda_device` (-1: host tensors only).
  * Allocates the pinned ring (slots*slot_bytes, page-locked and registered with
- * the I/O engine), one device slab of slot_bytes, a low-priority CUDA stream and
+ * the I/O engine), one device slab of pack_bytes, a CUDA stream and
  * the helper thread. `comm` may be NULL only if every call uses dp_size == 1.
  * *out receives the context. Errors: -EINVAL (bad config), -ENOMEM, FP_ECUDA. */
 int fp_ckpt_init(const fp_config *cfg, int cuda_device, const fp_comm *comm,
@@ -194,9 +200,12 @@ void fp_ckpt_destroy(fp_ctx *ctx);
 /* Human-readable text for a return code (static storage).                    */
 const char *fp_strerror(int err);
 
-/* Storage roofline tool (the built-in substitute for fio): write
- * `bytes` of host data to `<dir>/fp_iobench.<tag>` with the configured engine
- * (O_DIRECT, io_depth x sqe_bytes), fdatasync, unlink; *gbps = bytes / time.  */
+/* Storage roofline tool (the built-in substitute for fio): with the
+ * configured engine (O_DIRECT, io_depth x sqe_bytes from a registered pinned
+ * ring) write `bytes` of non-compressible host data to `<dir>/fp_iobench.<tag>`
+ * and fdatasync (untimed pass: allocates every block), then overwrite the same
+ * file sequentially and fdatasync again (timed pass), unlink.
+ * *gbps = bytes / (timed pass seconds) / 1e9.                                 */
 int fp_io_bench(const char *dir, uint64_t bytes, const fp_config *cfg, int tag,
                 double *gbps);
 

@@ -98,9 +98,11 @@ struct Item {
 static_assert(sizeof(Item) == 16, "Item must be 16 bytes");
 
 // Items for every chunk of the shard file (chunk = slot_bytes of file bytes).
-// item_lo has n_chunks+1 entries.
-void plan_items(const Plan& p, uint64_t slot_bytes, std::vector<Item>* items,
-                std::vector<uint32_t>* item_lo);
+// item_lo has n_chunks+1 entries. Item.dst is relative to the start of the
+// chunk's pack group (group = group_bytes/slot_bytes consecutive chunks that
+// one pack launch gathers into one device slab).
+void plan_items(const Plan& p, uint64_t slot_bytes, uint64_t group_bytes,
+                std::vector<Item>* items, std::vector<uint32_t>* item_lo);
 
 // ---------------------------------------------------------------------------
 // I/O engines

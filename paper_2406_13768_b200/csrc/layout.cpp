@@ -266,8 +266,9 @@ void plan_pieces(Plan* p, const std::vector<TensorRef>& rep, const std::vector<T
   }
 }
 
-void plan_items(const Plan& p, uint64_t slot_bytes, std::vector<Item>* items,
-                std::vector<uint32_t>* item_lo) {
+void plan_items(const Plan& p, uint64_t slot_bytes, uint64_t group_bytes,
+                std::vector<Item>* items, std::vector<uint32_t>* item_lo) {
+  const uint64_t per_group = group_bytes / slot_bytes;
   items->clear();
   item_lo->clear();
   const uint64_t n_chunks = (p.shard_bytes + slot_bytes - 1) / slot_bytes;
@@ -286,7 +287,8 @@ void plan_items(const Plan& p, uint64_t slot_bytes, std::vector<Item>* items,
       }
       const uint64_t cend = (chunk + 1) * slot_bytes;
       const uint64_t n = std::min<uint64_t>({left, (uint64_t)kTile, cend - fo});
-      items->push_back({src, (uint32_t)(fo - chunk * slot_bytes), (uint32_t)n});
+      const uint64_t gbase = chunk / per_group * per_group * slot_bytes;
+      items->push_back({src, (uint32_t)(fo - gbase), (uint32_t)n});
       fo += n;
       left -= n;
       if (src) src += n;

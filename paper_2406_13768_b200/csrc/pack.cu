@@ -89,10 +89,20 @@ __device__ __forceinline__ void copy_bytes(uint8_t* __restrict__ dst,
 
 __global__ void __launch_bounds__(kV4Threads) fp_pack_v4(const Item* __restrict__ items,
                                                          uint32_t n, uint8_t* __restrict__ slab) {
-  for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
-    const Item it = items[i];
+  // the next item's descriptor is loaded before the current item's data, so
+  // its latency hides behind the copy instead of opening a bubble per item
+  uint32_t i = blockIdx.x;
+  if (i >= n) return;
+  Item it = items[i];
+  for (;;) {
+    const uint32_t nx = i + gridDim.x;
+    Item nit = {0, 0, 0};
+    if (nx < n) nit = items[nx];
     copy_bytes(slab + it.dst, reinterpret_cast<const uint8_t*>(it.src), it.len, threadIdx.x,
                kV4Threads);
+    if (nx >= n) break;
+    i = nx;
+    it = nit;
   }
 }
 

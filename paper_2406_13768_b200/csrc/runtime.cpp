@@ -215,7 +215,8 @@ struct fp_ctx {
   uint8_t* d_slab = nullptr;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_producer = nullptr;
-  std::vector<cudaEvent_t> ev_p0, ev_p1, ev_d2h;
+  std::vector<cudaEvent_t> ev_p0, ev_p1, ev_d0, ev_d2h;
+  std::vector<uint8_t> has_pack;  // per ring slot: its chunk led a pack launch
   IoEngine* io = nullptr;
   int pack_ctas = 0;
   // plan cache
@@ -317,6 +318,11 @@ int fp_ctx::save_shard() {
     return 0;
   };
 
+  // one pack launch gathers a group of G consecutive chunks into the device
+  // slab (pack_bytes = G * slot_bytes); each chunk is then copied to its own
+  // ring slot as that slot frees up (stream order keeps the next group's pack
+  // behind the previous group's copies)
+  const uint64_t G = host ? 1 : std::max<uint64_t>(1, cfg.pack_bytes / S);
   auto stage = [&](uint64_t c) -> int {
     const uint32_t s = (uint32_t)(c % R);
     const uint64_t len = std::min<uint64_t>(S, plan.shard_bytes - c * S);
@@ -332,16 +338,23 @@ int fp_ctx::save_shard() {
       st.pack_bytes += len;
       return 0;
     }
-    if (c == 0) CK(cudaStreamWaitEvent(stream, ev_producer, 0));
-    CK(cudaEventRecord(ev_p0[s], stream));
-    int r = pack_launch(cfg.pack_impl, d_items + item_lo[c], item_lo[c + 1] - item_lo[c],
-                        d_slab, pack_ctas, stream);
-    if (r) return r;
-    CK(cudaEventRecord(ev_p1[s], stream));
-    CK(cudaMemcpyAsync(slot, d_slab, len, cudaMemcpyDeviceToHost, stream));
+    const uint64_t g0 = c / G * G;
+    has_pack[s] = 0;
+    if (c == g0) {
+      const uint64_t c1 = std::min<uint64_t>(g0 + G, C);
+      if (c == 0) CK(cudaStreamWaitEvent(stream, ev_producer, 0));
+      CK(cudaEventRecord(ev_p0[s], stream));
+      int r = pack_launch(cfg.pack_impl, d_items + item_lo[c], item_lo[c1] - item_lo[c], d_slab,
+                          pack_ctas, stream);
+      if (r) return r;
+      CK(cudaEventRecord(ev_p1[s], stream));
+      has_pack[s] = 1;
+      ++st.pack_launches;
+      st.pack_bytes += std::min<uint64_t>(c1 * S, plan.shard_bytes) - c * S;
+    }
+    CK(cudaEventRecord(ev_d0[s], stream));
+    CK(cudaMemcpyAsync(slot, d_slab + (c - g0) * S, len, cudaMemcpyDeviceToHost, stream));
     CK(cudaEventRecord(ev_d2h[s], stream));
-    ++st.pack_launches;
-    st.pack_bytes += len;
     return 0;
   };
 
@@ -351,8 +364,9 @@ int fp_ctx::save_shard() {
     if (!host) {
       CK(cudaEventSynchronize(ev_d2h[s]));
       float a = 0, b = 0;
-      if (cudaEventElapsedTime(&a, ev_p0[s], ev_p1[s]) == cudaSuccess) st.pack_ms += a;
-      if (cudaEventElapsedTime(&b, ev_p1[s], ev_d2h[s]) == cudaSuccess) st.d2h_ms += b;
+      if (has_pack[s] && cudaEventElapsedTime(&a, ev_p0[s], ev_p1[s]) == cudaSuccess)
+        st.pack_ms += a;
+      if (cudaEventElapsedTime(&b, ev_d0[s], ev_d2h[s]) == cudaSuccess) st.d2h_ms += b;
     }
     uint8_t* slot = ring + (size_t)s * S;
     for (uint64_t off = 0; off < len; off += SQ) {
@@ -598,7 +612,8 @@ static int build_items(fp_ctx* c, bool for_save) {
                         : c->host ? (uint64_t)(uintptr_t)c->h_hdr.data()
                                   : (uint64_t)(uintptr_t)c->d_hdr;
   plan_pieces(&c->plan, c->rep, c->loc, base);
-  plan_items(c->plan, c->cfg.slot_bytes, &c->items, &c->item_lo);
+  plan_items(c->plan, c->cfg.slot_bytes, c->host ? c->cfg.slot_bytes : c->cfg.pack_bytes,
+             &c->items, &c->item_lo);
   if (!c->host && c->dev >= 0 && !c->items.empty()) {
     const size_t need = c->items.size() * sizeof(Item);
     if (c->d_items_cap < need) {
@@ -638,6 +653,9 @@ int fp_config_default(fp_config* cfg) {
   cfg->sqe_bytes = (uint32_t)env_u64("FP_SQE_BYTES", 1u << 20);
   cfg->alignment = (uint32_t)env_u64("FP_ALIGN", 4096);
   cfg->pack_ctas = (uint32_t)env_u64("FP_PACK_CTAS", 0);
+  cfg->pack_bytes = env_u64("FP_PACK_BYTES", 256ull << 20);
+  const char* pr = getenv("FP_PACK_PRIO");
+  if (pr && !strcmp(pr, "low")) cfg->flags |= FP_CFG_PRIO_LOW;
   const char* e = getenv("FP_IO_ENGINE");
   cfg->io_engine = !e ? FP_IO_URING
                    : !strcmp(e, "pwrite") ? FP_IO_PWRITE
@@ -657,6 +675,7 @@ static int check_cfg(const fp_config& c) {
   if (!c.sqe_bytes || c.sqe_bytes % A || c.sqe_bytes > (1u << 30)) return -EINVAL;
   if (c.sqe_bytes / 512 >= (1u << 24)) return -EINVAL;
   if (c.io_engine > FP_IO_BUFFERED || c.pack_impl > FP_PACK_BULK) return -EINVAL;
+  if (c.pack_bytes > (2ull << 30)) return -EINVAL;
   return 0;
 }
 
@@ -691,6 +710,10 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
     fp_config_default(&cfg);
   int r = check_cfg(cfg);
   if (r) return r;
+  // the device slab holds a whole number of ring chunks
+  if (!cfg.pack_bytes || cfg.pack_bytes < cfg.slot_bytes) cfg.pack_bytes = cfg.slot_bytes;
+  cfg.pack_bytes = round_up(cfg.pack_bytes, cfg.slot_bytes);
+  if (cfg.pack_bytes > (2ull << 30)) return -EINVAL;
   fp_ctx* c = new fp_ctx();
   c->cfg = cfg;
   if (cfg.dirs && *cfg.dirs) {
@@ -727,19 +750,27 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
     if (cudaHostRegister(c->ring, c->ring_bytes, cudaHostRegisterPortable) != cudaSuccess)
       return fail(FP_ECUDA);
     c->ring_cuda_registered = true;
-    if (cudaMalloc(&c->d_slab, cfg.slot_bytes) != cudaSuccess) return fail(-ENOMEM);
+    if (cudaMalloc(&c->d_slab, cfg.pack_bytes) != cudaSuccess) return fail(-ENOMEM);
+    // The pack is short (a 256 MiB group is ~85 us of HBM time) and is what
+    // feeds the ring: by default it runs at the GREATEST priority so its CTAs
+    // are dispatched in the gaps of a saturating compute stream instead of
+    // starving behind it; FP_CFG_PRIO_LOW selects the least priority.
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    if (cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, least) != cudaSuccess)
+    const int prio = (cfg.flags & FP_CFG_PRIO_LOW) ? least : greatest;
+    if (cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio) != cudaSuccess)
       return fail(FP_ECUDA);
     if (cudaEventCreateWithFlags(&c->ev_producer, cudaEventDisableTiming) != cudaSuccess)
       return fail(FP_ECUDA);
     c->ev_p0.resize(cfg.ring_slots);
     c->ev_p1.resize(cfg.ring_slots);
+    c->ev_d0.resize(cfg.ring_slots);
     c->ev_d2h.resize(cfg.ring_slots);
+    c->has_pack.assign(cfg.ring_slots, 0);
     for (uint32_t s = 0; s < cfg.ring_slots; ++s) {
       if (cudaEventCreate(&c->ev_p0[s]) != cudaSuccess ||
           cudaEventCreate(&c->ev_p1[s]) != cudaSuccess ||
+          cudaEventCreate(&c->ev_d0[s]) != cudaSuccess ||
           cudaEventCreateWithFlags(&c->ev_d2h[s], cudaEventBlockingSync) != cudaSuccess)
         return fail(FP_ECUDA);
     }
@@ -983,7 +1014,7 @@ int fp_ckpt_load(fp_ctx* c, const fp_tensor* t, size_t n, const char* path, int 
   plan_pieces(&lp, c->rep, c->loc, 0);  // header pieces -> skip items
   std::vector<Item> items;
   std::vector<uint32_t> lo;
-  plan_items(lp, c->cfg.slot_bytes, &items, &lo);
+  plan_items(lp, c->cfg.slot_bytes, c->cfg.slot_bytes, &items, &lo);
   Item* d_items = nullptr;
   if (!c->host && !items.empty()) {
     if (cudaMalloc(&d_items, items.size() * sizeof(Item)) != cudaSuccess ||
@@ -1094,7 +1125,7 @@ void fp_ckpt_destroy(fp_ctx* c) {
   }
   if (c->dev >= 0) {
     if (c->stream) cudaStreamSynchronize(c->stream);
-    for (auto* v : {&c->ev_p0, &c->ev_p1, &c->ev_d2h})
+    for (auto* v : {&c->ev_p0, &c->ev_p1, &c->ev_d0, &c->ev_d2h})
       for (cudaEvent_t e : *v)
         if (e) cudaEventDestroy(e);
     if (c->ev_producer) cudaEventDestroy(c->ev_producer);
@@ -1154,34 +1185,43 @@ int fp_io_bench(const char* dir, uint64_t bytes, const fp_config* cfg_in, int ta
     return r;
   }
   fallocate(fd, 0, 0, (off_t)bytes);
-  const double t0 = now_s();
-  uint64_t off = 0;
-  uint32_t inflight = 0;
+  // Pass 1 (untimed) allocates and writes every block; pass 2 (timed) is a
+  // sequential O_DIRECT overwrite of the same file, which is what a
+  // checkpoint generation rewriting its shard in place does (the bench
+  // rotates two generations), so the roofline and the checkpoint see the
+  // device in the same state.
   IoDone done[64];
   int status = 0;
   const uint64_t span = ring_bytes;
-  while ((off < bytes || inflight) && !status) {
-    while (off < bytes && inflight < io->capacity()) {
-      const uint32_t n = (uint32_t)std::min<uint64_t>(cfg.sqe_bytes, bytes - off);
-      const uint64_t ro = off % span;
-      const uint32_t slot = (uint32_t)(ro / cfg.slot_bytes);
-      const uint32_t nn = (uint32_t)std::min<uint64_t>(n, cfg.slot_bytes - ro % cfg.slot_bytes);
-      if (io->queue(true, fd, ring + ro, nn, off, (int)slot, nn)) break;
-      ++inflight;
-      off += nn;
+  auto pass = [&]() {
+    uint64_t off = 0;
+    uint32_t inflight = 0;
+    while ((off < bytes || inflight) && !status) {
+      while (off < bytes && inflight < io->capacity()) {
+        const uint32_t n = (uint32_t)std::min<uint64_t>(cfg.sqe_bytes, bytes - off);
+        const uint64_t ro = off % span;
+        const uint32_t slot = (uint32_t)(ro / cfg.slot_bytes);
+        const uint32_t nn = (uint32_t)std::min<uint64_t>(n, cfg.slot_bytes - ro % cfg.slot_bytes);
+        if (io->queue(true, fd, ring + ro, nn, off, (int)slot, nn)) break;
+        ++inflight;
+        off += nn;
+      }
+      io->submit();
+      int k2 = io->reap(done, 64, 1);
+      if (k2 < 0) {
+        status = k2;
+        break;
+      }
+      for (int i = 0; i < k2; ++i)
+        if (done[i].res != (int32_t)done[i].user && !status)
+          status = done[i].res < 0 ? done[i].res : -EIO;
+      inflight -= (uint32_t)k2;
     }
-    io->submit();
-    int k2 = io->reap(done, 64, 1);
-    if (k2 < 0) {
-      status = k2;
-      break;
-    }
-    for (int i = 0; i < k2; ++i)
-      if (done[i].res != (int32_t)done[i].user && !status)
-        status = done[i].res < 0 ? done[i].res : -EIO;
-    inflight -= (uint32_t)k2;
-  }
-  if (!status && !(cfg.flags & FP_CFG_NO_FSYNC)) status = io->fdatasync(fd);
+    if (!status && !(cfg.flags & FP_CFG_NO_FSYNC)) status = io->fdatasync(fd);
+  };
+  pass();
+  const double t0 = now_s();
+  if (!status) pass();
   const double dt = now_s() - t0;
   close(fd);
   unlink(f.c_str());

@@ -29,6 +29,7 @@ LIB_PATH = os.path.join(_PKG, "libfastpersist.so")
 FP_EMISMATCH, FP_ECORRUPT, FP_ECUDA, FP_ENODEV, FP_ECOMM = -1001, -1002, -1003, -1004, -1005
 FP_TENSOR_HOST = 1
 FP_CFG_NO_FSYNC = 1
+FP_CFG_PRIO_LOW = 2
 IO_ENGINES = {"uring": 0, "pwrite": 1, "buffered": 2}
 PACK_IMPLS = {"v4": 0, "bulk": 1}
 SECTIONS = {"param": 0, "grad": 1, "master": 2, "exp_avg": 3, "exp_avg_sq": 4, "other": 5}
@@ -55,7 +56,7 @@ class fp_config(C.Structure):
     _fields_ = [("ring_slots", C.c_uint32), ("io_depth", C.c_uint32), ("slot_bytes", C.c_uint64),
                 ("sqe_bytes", C.c_uint32), ("alignment", C.c_uint32), ("io_engine", C.c_uint32),
                 ("pack_impl", C.c_uint32), ("pack_ctas", C.c_uint32), ("flags", C.c_uint32),
-                ("dirs", C.c_char_p)]
+                ("dirs", C.c_char_p), ("pack_bytes", C.c_uint64)]
 
 
 class fp_stats(C.Structure):
@@ -146,6 +147,8 @@ def make_config(**kw) -> fp_config:
             k, v = "pack_impl", PACK_IMPLS[v] if isinstance(v, str) else v
         elif k == "no_fsync":
             k, v = "flags", cfg.flags | (FP_CFG_NO_FSYNC if v else 0)
+        elif k == "prio":
+            k, v = "flags", (cfg.flags & ~FP_CFG_PRIO_LOW) | (FP_CFG_PRIO_LOW if v == "low" else 0)
         elif k == "dirs":
             v = (",".join(v) if isinstance(v, (list, tuple)) else v).encode()
         setattr(cfg, k, v)

@@ -41,10 +41,38 @@ def _check_rank_files(tmp, lay, k):
 def test_c1_tiny_parity(tmp_path, pack, slot_bytes):
     st = _state("c1_tiny")
     lay = oracle_layout([st], 1)
-    with fp.Checkpointer(DEV, pack=pack, slot_bytes=slot_bytes, ring_slots=4) as ck:
+    with fp.Checkpointer(DEV, pack=pack, slot_bytes=slot_bytes, ring_slots=4,
+                         pack_bytes=slot_bytes) as ck:
         s = ck.save(entries(st), str(tmp_path))
     assert s["pack_launches"] == s["chunks"] > 0
     assert s["pack_bytes"] == lay.image_bytes and s["pack_ms"] > 0
+    _check_rank_files(str(tmp_path), lay, 1)
+
+
+@pytest.mark.parametrize("pack", ["v4", "bulk"])
+@pytest.mark.parametrize("slot_bytes,pack_bytes,slots", [(1 << 20, 3 << 20, 2), (4096, 5 * 4096, 3),
+                                                         (8 << 20, 64 << 20, 4),
+                                                         (2 << 20, 2 << 20, 1)])
+def test_pack_groups_parity(tmp_path, pack, slot_bytes, pack_bytes, slots):
+    """One pack launch gathers pack_bytes (several ring chunks, ragged last
+    group) into the device slab; every chunk is copied to its own ring slot."""
+    st = _state("c1_tiny")
+    lay = oracle_layout([st], 1)
+    with fp.Checkpointer(DEV, pack=pack, slot_bytes=slot_bytes, pack_bytes=pack_bytes,
+                         ring_slots=slots) as ck:
+        s = ck.save(entries(st), str(tmp_path))
+    groups = -(-lay.image_bytes // pack_bytes)
+    assert s["pack_launches"] == groups and s["chunks"] == -(-lay.image_bytes // slot_bytes)
+    assert s["pack_bytes"] == lay.image_bytes
+    _check_rank_files(str(tmp_path), lay, 1)
+
+
+@pytest.mark.parametrize("prio", ["high", "low"])
+def test_stream_priority_parity(tmp_path, prio):
+    st = _state("gpt3_odd")
+    lay = oracle_layout([st], 1)
+    with fp.Checkpointer(DEV, prio=prio, slot_bytes=1 << 20) as ck:
+        ck.save(entries(st), str(tmp_path))
     _check_rank_files(str(tmp_path), lay, 1)
 
 
