@@ -39,6 +39,9 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 CFG = "c2_gpt3_1.3b"
+# test hook: all ranks on cuda:0 over gloo (exercises the N>1 code path on a
+# 1-GPU box; NCCL refuses two ranks on one device). Never used for numbers.
+SHARE_GPU = os.environ.get("FP_BENCH_SHARE_GPU") == "1"
 METRIC = "checkpoint persist GB/s and latency at 1/2/4/8 B200; % iter overhead per-iter ckpt"
 SEQ, GBS_1P3B = 2048, 512          # PAPER.md Table tb:gpt-setup: 1.3B, GBS 512
 
@@ -63,10 +66,14 @@ def out_root():
     return os.path.join(base, "bench_ckpt")
 
 
+def _coll_dev(dev):
+    return dev if dist.get_backend() == "nccl" else torch.device("cpu")
+
+
 def allreduce_max(x, dev):
     if not dist.is_initialized():
         return x
-    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=_coll_dev(dev))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -74,7 +81,7 @@ def allreduce_max(x, dev):
 def allreduce_sum(x, dev):
     if not dist.is_initialized():
         return x
-    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=_coll_dev(dev))
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
@@ -325,9 +332,12 @@ def synthetic_overhead(a, ck, ents, state, dev, rank, world, root, shard_gb):
 def our_arm(a):
     ws, rank, lr = env_dist()
     if ws > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
+        if SHARE_GPU:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
     world = ws
-    dev = torch.device("cuda", lr)
+    dev = torch.device("cuda", 0 if SHARE_GPU else lr)
     torch.cuda.set_device(dev)
 
     import paper_2406_13768_b200 as fp
@@ -347,7 +357,8 @@ def our_arm(a):
     barrier()
 
     cfg = dict(pack=a.pack, slot_bytes=a.slot_mib << 20, ring_slots=a.ring_slots,
-               io_depth=a.qd, sqe_bytes=a.sqe_kib << 10)
+               io_depth=a.qd, sqe_bytes=a.sqe_kib << 10, pack_bytes=a.pack_mib << 20,
+               prio=a.prio)
     peaks, peak_src = measured_peaks()
 
     # ---- rooflines measured in the same run --------------------------------
@@ -407,9 +418,20 @@ def our_arm(a):
     # ---- e2e: public API with the state sourced from pinned HOST memory ------
     e2e = None
     if not a.no_e2e:
-        host = [torch.empty_like(t, device="cpu").pin_memory() for _, t in state]
-        for h, (_, t) in zip(host, state):
+        # this rank sources its share of the state from pinned host memory:
+        # tensors are dealt to ranks by the position of their middle byte in
+        # the state (rank r takes [r/N, (r+1)/N)), so across ranks every state
+        # byte crosses PCIe H2D exactly once per step and each rank pins ~1/N
+        mine, cum = [], 0
+        for _, t in state:
+            nb = t.numel() * t.element_size()
+            if int((cum + nb / 2) * world // state_bytes) == rank:
+                mine.append(t)
+            cum += nb
+        host = [torch.empty_like(t, device="cpu").pin_memory() for t in mine]
+        for h, t in zip(host, mine):
             h.copy_(t)
+        my_h2d = sum(t.numel() * t.element_size() for t in mine)
         torch.cuda.synchronize(dev)
         ke = max(1, min(a.steps, a.e2e_steps))
         barrier()
@@ -417,7 +439,7 @@ def our_arm(a):
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for i in range(ke):
-            for h, (_, t) in zip(host, state):
+            for h, t in zip(host, mine):
                 t.copy_(h, non_blocking=True)          # H2D of this step's inputs
             ck.begin(ents, os.path.join(root, f"gen{i % 2}"), stream=stream)
             st = ck.wait()                             # result: durable status (host)
@@ -426,7 +448,7 @@ def our_arm(a):
         barrier()
         e_el = allreduce_max(f0.elapsed_time(f1) / 1e3, dev)
         e2e = {"value": round(st["image_bytes"] * ke / e_el / 1e9, 4), "unit": "GB/s",
-               "h2d_bytes_per_step": int(allreduce_sum(state_bytes, dev)),
+               "h2d_bytes_per_step": int(allreduce_sum(my_h2d, dev)),
                "d2h_bytes_per_step": int(st["image_bytes"]), "steps": ke,
                "note": "timed: H2D of the whole state from pinned host memory, then "
                        "begin/wait through the Python API (D2H of the image via the ring)"}
@@ -449,11 +471,25 @@ def our_arm(a):
         croot = os.path.join(out_root(), "oracle")
         os.makedirs(croot, exist_ok=True)
         cg, ct, cimg = run_oracle_steps(sample, 1, croot)
+        # the paper's baseline: torch.save of the same tensors (host
+        # state dict) + fsync, as context for "speedup vs torch.save"
+        tsd = {s.name: t for s, t in sample}
+        fpath = os.path.join(croot, "torch_save.pt")
+        t0 = time.perf_counter()
+        with open(fpath, "wb") as f:
+            torch.save(tsd, f)
+            f.flush()
+            os.fsync(f.fileno())
+        ts_dt = time.perf_counter() - t0
+        ts_bytes = os.path.getsize(fpath)
         shutil.rmtree(croot, ignore_errors=True)
         cpu = {"value": round(cg, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
                "sample": f"first {len(sample)} tensors of {CFG} ({cimg} image bytes), "
                          "host-resident, buffered write()+fsync, 1 step",
-               "host_cores_available": cpu_cores()}
+               "host_cores_available": cpu_cores(),
+               "torch_save_gbs": round(ts_bytes / ts_dt / 1e9, 4),
+               "torch_save_note": "context only: torch.save(state dict of the same sample) "
+                                  "+ fsync on the same file system (PAPER.md P:259 baseline)"}
 
     if rank == 0:
         hbm = float(peaks["hbm_gbs"])
@@ -467,12 +503,14 @@ def our_arm(a):
             "config": {"workload": CFG, "dp": world, "image_bytes": image_bytes,
                        "shard_bytes_rank0": shard_bytes, "profile": "adam16",
                        "pack": a.pack, "ring": f"{a.ring_slots}x{a.slot_mib}MiB",
+                       "pack_launch_mib": a.pack_mib, "pack_stream_prio": a.prio,
                        "sqe_kib": a.sqe_kib, "qd": a.qd, "engine": stats[-1]["engine"],
                        "l2": "inputs (21 GB of state) larger than L2; no flush needed",
                        "dir": root},
             "latency_s": {"median": round(statistics.median(lat_max), 4),
                           "min": round(min(lat_max), 4), "max": round(max(lat_max), 4)},
-            "roofline": {"bound": "hbm", "kernel": "fp_pack_v4" if a.pack == "v4" else "fp_pack_bulk",
+            "roofline": {"bound": "hbm", "kernel": {"v4": "fp_pack_v4", "bulk": "fp_pack_bulk",
+                                    "host": "fp_pack_v4 (to mapped host)", "ce": None}[a.pack],
                          "achieved": round(pack_gbs, 1), "peak": hbm, "unit": "GB/s",
                          "frac": round(pack_gbs / hbm, 4), "traffic": a.traffic,
                          "peak_source": peak_src, "launch_avg_ms": round(launch_avg_ms, 5),
@@ -504,7 +542,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--pack", default="v4", choices=["v4", "bulk"])
+    ap.add_argument("--pack", default="v4", choices=["v4", "bulk", "host", "ce"])
+    ap.add_argument("--pack-mib", type=int, default=256)
+    ap.add_argument("--prio", default="high", choices=["high", "low"])
     ap.add_argument("--slot-mib", type=int, default=64)
     ap.add_argument("--ring-slots", type=int, default=4)
     ap.add_argument("--qd", type=int, default=64)

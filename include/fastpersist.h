@@ -86,9 +86,20 @@ typedef struct fp_comm {
 /* ---- configuration ------------------------------------------------------ */
 enum fp_io_engine { FP_IO_URING = 0,    /* io_uring, O_DIRECT, registered bufs */
                     FP_IO_PWRITE = 1,   /* pwrite thread pool, O_DIRECT         */
-                    FP_IO_BUFFERED = 2  /* pwrite through the page cache        */ };
-enum fp_pack_impl { FP_PACK_V4 = 0,     /* LSU 16-B vector gather               */
-                    FP_PACK_BULK = 1    /* cp.async.bulk (TMA engine) via smem   */ };
+                    FP_IO_BUFFERED = 2, /* pwrite through the page cache        */
+                    FP_IO_NULL = 3      /* ablation: requests complete at once,
+                                           nothing is written (measures the
+                                           pack + D2H + ring ceiling)           */ };
+enum fp_pack_impl { FP_PACK_V4 = 0,     /* LSU 16-B vector gather -> device slab,
+                                           then copy engine -> pinned ring       */
+                    FP_PACK_BULK = 1,   /* cp.async.bulk (TMA engine) via smem
+                                           -> device slab, then copy engine      */
+                    FP_PACK_HOST = 2,   /* fused: the v4 kernel stores straight
+                                           into the mapped pinned ring slot
+                                           (zero-copy D2H over PCIe, no slab)    */
+                    FP_PACK_CE = 3      /* ablation, no kernel: one copy-engine
+                                           cudaMemcpyAsync per contiguous run of
+                                           a chunk, tensors -> pinned ring       */ };
 
 #define FP_CFG_NO_FSYNC 1u     /* skip fdatasync (benchmark ablation only)       */
 #define FP_CFG_PRIO_LOW 2u     /* pack/D2H stream at the least priority (default:
@@ -142,8 +153,8 @@ typedef struct fp_stats {
 typedef struct fp_ctx fp_ctx;
 
 /* Fill *cfg with the defaults above (env overrides: FP_RING_SLOTS,
- * FP_SLOT_BYTES, FP_SQE_BYTES, FP_QD, FP_IO_ENGINE=uring|pwrite|buffered,
- * FP_PACK=v4|bulk, FP_PACK_CTAS, FP_ALIGN, FP_PACK_BYTES). Returns 0.         */
+ * FP_SLOT_BYTES, FP_SQE_BYTES, FP_QD, FP_IO_ENGINE=uring|pwrite|buffered|null,
+ * FP_PACK=v4|bulk|host|ce, FP_PACK_PRIO=low, FP_PACK_CTAS, FP_ALIGN, FP_PACK_BYTES). Returns 0.         */
 int fp_config_default(fp_config *cfg);
 
 /* Create a context bound to CUDA device `cuda_device` (-1: host tensors only).

@@ -129,6 +129,7 @@ class IoEngine {
 
 IoEngine* make_uring(uint32_t depth, int* err);
 IoEngine* make_pwrite(uint32_t threads, bool direct);
+IoEngine* make_null(uint32_t depth);
 
 // ---------------------------------------------------------------------------
 // kernels (pack.cu)

@@ -294,4 +294,35 @@ class PwritePool final : public IoEngine {
 
 IoEngine* make_pwrite(uint32_t threads, bool direct) { return new PwritePool(threads, direct); }
 
+// ---------------------------------------------------------------------------
+// null sink (ablation): every request completes immediately with its full
+// length; nothing reaches storage. Used to measure the GPU side of the path.
+// ---------------------------------------------------------------------------
+class NullSink final : public IoEngine {
+ public:
+  explicit NullSink(uint32_t depth) : depth_(depth) {}
+  int kind() const override { return FP_IO_NULL; }
+  uint32_t capacity() const override { return depth_; }
+  int queue(bool, int, void*, uint32_t len, uint64_t, int, uint64_t user) override {
+    done_.push_back({user, (int32_t)len});
+    return 0;
+  }
+  int submit() override { return 0; }
+  int reap(IoDone* out, int max, int) override {
+    int got = 0;
+    while (!done_.empty() && got < max) {
+      out[got++] = done_.front();
+      done_.pop_front();
+    }
+    return got;
+  }
+  int fdatasync(int) override { return 0; }
+
+ private:
+  uint32_t depth_;
+  std::deque<IoDone> done_;
+};
+
+IoEngine* make_null(uint32_t depth) { return new NullSink(depth); }
+
 }  // namespace fp

@@ -210,6 +210,7 @@ struct fp_ctx {
   bool has_comm = false;
   // resources
   uint8_t* ring = nullptr;
+  uint8_t* d_ring = nullptr;  // device alias of the mapped ring (FP_PACK_HOST)
   size_t ring_bytes = 0;
   bool ring_cuda_registered = false;
   uint8_t* d_slab = nullptr;
@@ -227,6 +228,8 @@ struct fp_ctx {
   bool host = false;
   std::vector<Item> items;
   std::vector<uint32_t> item_lo;
+  std::vector<Item> runs;          // FP_PACK_CE: items merged into contiguous runs
+  std::vector<uint32_t> run_lo;
   Item* d_items = nullptr;
   size_t d_items_cap = 0;
   uint8_t* d_hdr = nullptr;
@@ -266,8 +269,9 @@ int fp_ctx::save_shard() {
     std::string m = join_path(manifest_dir, "manifest.json");
     if (unlink(m.c_str()) && errno != ENOENT) return -errno;
   }
-  const std::string file = join_path(shard_dir, shard_file(rank, k));
-  const bool want_direct = cfg.io_engine != FP_IO_BUFFERED;
+  const std::string file = cfg.io_engine == FP_IO_NULL ? std::string("/dev/null")
+                                                        : join_path(shard_dir, shard_file(rank, k));
+  const bool want_direct = cfg.io_engine != FP_IO_BUFFERED && cfg.io_engine != FP_IO_NULL;
   int fd = open(file.c_str(), O_WRONLY | O_CREAT | (want_direct ? O_DIRECT : 0), 0644);
   if (fd < 0 && want_direct && errno == EINVAL) {
     fd = open(file.c_str(), O_WRONLY | O_CREAT, 0644);  // no O_DIRECT here (e.g. old tmpfs)
@@ -275,7 +279,8 @@ int fp_ctx::save_shard() {
   }
   if (fd < 0) return -errno;
   struct stat sb;
-  if (fstat(fd, &sb) == 0 && (uint64_t)sb.st_size != plan.shard_bytes) {
+  if (cfg.io_engine != FP_IO_NULL && fstat(fd, &sb) == 0 &&
+      (uint64_t)sb.st_size != plan.shard_bytes) {
     if (ftruncate(fd, (off_t)plan.shard_bytes)) {
       err = -errno;
       close(fd);
@@ -322,7 +327,8 @@ int fp_ctx::save_shard() {
   // slab (pack_bytes = G * slot_bytes); each chunk is then copied to its own
   // ring slot as that slot frees up (stream order keeps the next group's pack
   // behind the previous group's copies)
-  const uint64_t G = host ? 1 : std::max<uint64_t>(1, cfg.pack_bytes / S);
+  const bool slabless = cfg.pack_impl == FP_PACK_HOST || cfg.pack_impl == FP_PACK_CE;
+  const uint64_t G = host || slabless ? 1 : std::max<uint64_t>(1, cfg.pack_bytes / S);
   auto stage = [&](uint64_t c) -> int {
     const uint32_t s = (uint32_t)(c % R);
     const uint64_t len = std::min<uint64_t>(S, plan.shard_bytes - c * S);
@@ -338,8 +344,39 @@ int fp_ctx::save_shard() {
       st.pack_bytes += len;
       return 0;
     }
-    const uint64_t g0 = c / G * G;
     has_pack[s] = 0;
+    if (cfg.pack_impl == FP_PACK_HOST) {
+      // fused pack -> mapped pinned slot: the kernel's stores cross PCIe
+      if (c == 0) CK(cudaStreamWaitEvent(stream, ev_producer, 0));
+      CK(cudaEventRecord(ev_p0[s], stream));
+      int r = pack_launch(FP_PACK_V4, d_items + item_lo[c], item_lo[c + 1] - item_lo[c],
+                          d_ring + (size_t)s * S, pack_ctas, stream);
+      if (r) return r;
+      CK(cudaEventRecord(ev_p1[s], stream));
+      CK(cudaEventRecord(ev_d0[s], stream));
+      CK(cudaEventRecord(ev_d2h[s], stream));
+      has_pack[s] = 1;
+      ++st.pack_launches;
+      st.pack_bytes += len;
+      return 0;
+    }
+    if (cfg.pack_impl == FP_PACK_CE) {
+      // ablation: copy-engine gather, one cudaMemcpyAsync per contiguous run
+      if (c == 0) CK(cudaStreamWaitEvent(stream, ev_producer, 0));
+      CK(cudaEventRecord(ev_d0[s], stream));
+      for (uint32_t i = run_lo[c]; i < run_lo[c + 1]; ++i) {
+        const Item& it = runs[i];
+        if (it.src)
+          CK(cudaMemcpyAsync(slot + it.dst, (const void*)(uintptr_t)it.src, it.len,
+                             cudaMemcpyDeviceToHost, stream));
+        else
+          memset(slot + it.dst, 0, it.len);  // slot is free: no copy in flight
+      }
+      CK(cudaEventRecord(ev_d2h[s], stream));
+      st.pack_bytes += len;
+      return 0;
+    }
+    const uint64_t g0 = c / G * G;
     if (c == g0) {
       const uint64_t c1 = std::min<uint64_t>(g0 + G, C);
       if (c == 0) CK(cudaStreamWaitEvent(stream, ev_producer, 0));
@@ -612,8 +649,31 @@ static int build_items(fp_ctx* c, bool for_save) {
                         : c->host ? (uint64_t)(uintptr_t)c->h_hdr.data()
                                   : (uint64_t)(uintptr_t)c->d_hdr;
   plan_pieces(&c->plan, c->rep, c->loc, base);
-  plan_items(c->plan, c->cfg.slot_bytes, c->host ? c->cfg.slot_bytes : c->cfg.pack_bytes,
-             &c->items, &c->item_lo);
+  const bool slabless = c->cfg.pack_impl == FP_PACK_HOST || c->cfg.pack_impl == FP_PACK_CE;
+  plan_items(c->plan, c->cfg.slot_bytes,
+             c->host || slabless ? c->cfg.slot_bytes : c->cfg.pack_bytes, &c->items,
+             &c->item_lo);
+  if (c->cfg.pack_impl == FP_PACK_CE && !c->host) {
+    // merge consecutive items of a chunk that continue the same source run
+    c->runs.clear();
+    c->run_lo.assign(1, 0);
+    for (size_t ch = 0; ch + 1 < c->item_lo.size(); ++ch) {
+      for (uint32_t i = c->item_lo[ch]; i < c->item_lo[ch + 1]; ++i) {
+        const Item& it = c->items[i];
+        if (c->runs.size() > c->run_lo.back()) {
+          Item& b = c->runs.back();
+          const bool contig = b.dst + b.len == it.dst && ((!b.src && !it.src) ||
+                                                           (b.src && it.src && b.src + b.len == it.src));
+          if (contig) {
+            b.len += it.len;
+            continue;
+          }
+        }
+        c->runs.push_back(it);
+      }
+      c->run_lo.push_back((uint32_t)c->runs.size());
+    }
+  }
   if (!c->host && c->dev >= 0 && !c->items.empty()) {
     const size_t need = c->items.size() * sizeof(Item);
     if (c->d_items_cap < need) {
@@ -660,9 +720,14 @@ int fp_config_default(fp_config* cfg) {
   cfg->io_engine = !e ? FP_IO_URING
                    : !strcmp(e, "pwrite") ? FP_IO_PWRITE
                    : !strcmp(e, "buffered") ? FP_IO_BUFFERED
+                   : !strcmp(e, "null")     ? FP_IO_NULL
                                              : FP_IO_URING;
   const char* pk = getenv("FP_PACK");
-  cfg->pack_impl = pk && !strcmp(pk, "bulk") ? FP_PACK_BULK : FP_PACK_V4;
+  cfg->pack_impl = !pk                   ? FP_PACK_V4
+                   : !strcmp(pk, "bulk") ? FP_PACK_BULK
+                   : !strcmp(pk, "host") ? FP_PACK_HOST
+                   : !strcmp(pk, "ce")   ? FP_PACK_CE
+                                         : FP_PACK_V4;
   cfg->dirs = getenv("FP_CKPT_DIRS");
   return 0;
 }
@@ -674,13 +739,18 @@ static int check_cfg(const fp_config& c) {
   if (!c.slot_bytes || c.slot_bytes % A || c.slot_bytes > (1ull << 31)) return -EINVAL;
   if (!c.sqe_bytes || c.sqe_bytes % A || c.sqe_bytes > (1u << 30)) return -EINVAL;
   if (c.sqe_bytes / 512 >= (1u << 24)) return -EINVAL;
-  if (c.io_engine > FP_IO_BUFFERED || c.pack_impl > FP_PACK_BULK) return -EINVAL;
+  if (c.io_engine > FP_IO_NULL || c.pack_impl > FP_PACK_CE) return -EINVAL;
   if (c.pack_bytes > (2ull << 30)) return -EINVAL;
   return 0;
 }
 
 static IoEngine* open_engine(const fp_config& cfg, int* kind_used) {
   IoEngine* io = nullptr;
+  if (cfg.io_engine == FP_IO_NULL) {
+    io = make_null(cfg.io_depth);
+    *kind_used = io->kind();
+    return io;
+  }
   if (cfg.io_engine == FP_IO_URING) {
     int err = 0;
     io = make_uring(cfg.io_depth, &err);
@@ -747,9 +817,12 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
   };
   if (cuda_device >= 0) {
     if (cudaSetDevice(cuda_device) != cudaSuccess) return fail(FP_ENODEV);
-    if (cudaHostRegister(c->ring, c->ring_bytes, cudaHostRegisterPortable) != cudaSuccess)
+    if (cudaHostRegister(c->ring, c->ring_bytes,
+                         cudaHostRegisterPortable | cudaHostRegisterMapped) != cudaSuccess)
       return fail(FP_ECUDA);
     c->ring_cuda_registered = true;
+    if (cudaHostGetDevicePointer((void**)&c->d_ring, c->ring, 0) != cudaSuccess)
+      return fail(FP_ECUDA);
     if (cudaMalloc(&c->d_slab, cfg.pack_bytes) != cudaSuccess) return fail(-ENOMEM);
     // The pack is short (a 256 MiB group is ~85 us of HBM time) and is what
     // feeds the ring: by default it runs at the GREATEST priority so its CTAs
@@ -774,7 +847,10 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
           cudaEventCreateWithFlags(&c->ev_d2h[s], cudaEventBlockingSync) != cudaSuccess)
         return fail(FP_ECUDA);
     }
-    c->pack_ctas = cfg.pack_ctas ? (int)cfg.pack_ctas : pack_default_ctas(cfg.pack_impl, cuda_device);
+    c->pack_ctas = cfg.pack_ctas ? (int)cfg.pack_ctas
+                                 : pack_default_ctas(cfg.pack_impl == FP_PACK_BULK ? FP_PACK_BULK
+                                                                                   : FP_PACK_V4,
+                                                     cuda_device);
   }
   c->th = std::thread([c] { c->helper(); });
   *out = c;
@@ -827,7 +903,7 @@ int fp_ckpt_wait(fp_ctx* c, fp_stats* out) {
       status = s;
     c->st.t_barrier = now_s() - tb;
   }
-  if (status == 0 && c->rank == 0) {
+  if (status == 0 && c->rank == 0 && c->cfg.io_engine != FP_IO_NULL) {  // null sink: no commit
     const double tc = now_s();
     status = c->write_manifest();
     c->st.t_commit = now_s() - tc;
@@ -881,6 +957,7 @@ int fp_ckpt_load(fp_ctx* c, const fp_tensor* t, size_t n, const char* path, int 
   if (!c || (!t && n) || !path || dp_size < 1 || dp_rank < 0 || dp_rank >= dp_size)
     return -EINVAL;
   if (dp_size > 1 && !c->has_comm) return -EINVAL;
+  if (c->cfg.io_engine == FP_IO_NULL) return -EINVAL;  // nothing was ever written
   {
     std::lock_guard<std::mutex> g(c->mu);
     if (c->state != fp_ctx::IDLE) return -EBUSY;

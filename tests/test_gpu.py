@@ -36,7 +36,7 @@ def _check_rank_files(tmp, lay, k):
         assert file_sha(os.path.join(tmp, fpck.shard_name(r, k))) == fpck.shard_sha256(lay, r), r
 
 
-@pytest.mark.parametrize("pack", ["v4", "bulk"])
+@pytest.mark.parametrize("pack", ["v4", "bulk", "host", "ce"])
 @pytest.mark.parametrize("slot_bytes", [4096, 1 << 20, 3 << 20, 64 << 20])
 def test_c1_tiny_parity(tmp_path, pack, slot_bytes):
     st = _state("c1_tiny")
@@ -44,8 +44,11 @@ def test_c1_tiny_parity(tmp_path, pack, slot_bytes):
     with fp.Checkpointer(DEV, pack=pack, slot_bytes=slot_bytes, ring_slots=4,
                          pack_bytes=slot_bytes) as ck:
         s = ck.save(entries(st), str(tmp_path))
-    assert s["pack_launches"] == s["chunks"] > 0
-    assert s["pack_bytes"] == lay.image_bytes and s["pack_ms"] > 0
+    if pack == "ce":     # ablation: no kernel at all, copy engine only
+        assert s["pack_launches"] == 0 and s["d2h_ms"] > 0
+    else:
+        assert s["pack_launches"] == s["chunks"] > 0 and s["pack_ms"] > 0
+    assert s["pack_bytes"] == lay.image_bytes
     _check_rank_files(str(tmp_path), lay, 1)
 
 
@@ -76,7 +79,7 @@ def test_stream_priority_parity(tmp_path, prio):
     _check_rank_files(str(tmp_path), lay, 1)
 
 
-@pytest.mark.parametrize("pack", ["v4", "bulk"])
+@pytest.mark.parametrize("pack", ["v4", "bulk", "host", "ce"])
 @pytest.mark.parametrize("cfg", ["gpt3_small", "gpt3_odd", "zero_small", "moe_small"])
 def test_structured_states_parity(tmp_path, cfg, pack):
     st = _state(cfg)
@@ -86,7 +89,7 @@ def test_structured_states_parity(tmp_path, cfg, pack):
     _check_rank_files(str(tmp_path), lay, 1)
 
 
-@pytest.mark.parametrize("pack", ["v4", "bulk"])
+@pytest.mark.parametrize("pack", ["v4", "bulk", "host", "ce"])
 def test_misaligned_and_degenerate_tensors(tmp_path, pack):
     """Odd storage offsets (byte path), empty tensors, scalars, 1-byte tails."""
     base = torch.randint(0, 256, (1 << 20,), dtype=torch.uint8, device=DEV)

@@ -213,3 +213,17 @@ def test_io_bench_runs(tmp_path):
     g = fp.io_bench(str(tmp_path), 8 << 20, slot_bytes=1 << 20, ring_slots=2)
     assert g > 0
     assert not os.listdir(tmp_path)
+
+
+def test_null_sink_engine_runs_the_pipeline_but_commits_nothing(tmp_path):
+    """FP_IO_NULL (ablation): the ring + submission path runs, nothing is
+    written, no manifest is committed, and load refuses it."""
+    st = _state("gpt3_small")
+    with fp.Checkpointer(None, slot_bytes=1 << 20, io_engine="null") as ck:
+        s = ck.save(entries(st), str(tmp_path))
+        assert s["engine"] == 3 and s["io_requests"] > 0 and s["shard_bytes"] > 0
+        assert not os.path.exists(tmp_path / "manifest.json")
+        assert not os.path.exists(tmp_path / "shard-0-of-1.fpck")
+        with pytest.raises(FastPersistError) as ei:
+            ck.load(entries(st), str(tmp_path))
+        assert ei.value.code == -22
