@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define FP_ABI_VERSION 1
+#define FP_ABI_VERSION 2
 
 /* ---- error codes beyond -errno ----------------------------------------- */
 #define FP_EMISMATCH (-1001) /* layout differs across ranks, or load target != file */
@@ -81,6 +81,15 @@ typedef struct fp_comm {
                        uint64_t n_per_rank);
   /* in-place MIN over ranks                                                  */
   int (*allreduce_min_i32)(void *ctx, int32_t *inout);
+  /* optional (NULL if unsupported; needed only by fp_ckpt_load_parallel with
+   * dp_size > 1): all-gather of `bytes` bytes per rank, rank-major:
+   * recv[r*bytes, (r+1)*bytes) = rank r's send. on_device = 1: send/recv are
+   * device pointers and the exchange must be ordered on `stream`
+   * (cudaStream_t) — after work already enqueued there, before work enqueued
+   * after the call returns (NCCL all-gather over NVLink on the B200 box);
+   * on_device = 0: host pointers, complete on return.                         */
+  int (*allgather_bytes)(void *ctx, const void *send, void *recv, uint64_t bytes,
+                         int on_device, void *stream);
 } fp_comm;
 
 /* ---- configuration ------------------------------------------------------ */
@@ -197,6 +206,22 @@ int fp_ckpt_wait(fp_ctx *ctx, fp_stats *out);
  * FP_EMISMATCH, -EIO, -EBUSY (a save is outstanding).                         */
 int fp_ckpt_load(fp_ctx *ctx, const fp_tensor *t, size_t n, const char *path,
                  int dp_rank, int dp_size, void *stream);
+
+/* Parallel restore, the paper's two-step load (§4.2: each rank "(i)
+ * loads its checkpoint partition, if any, into GPU memory, and (ii) performs
+ * an allgather"): rank r reads ONLY its own shard file, in slot_bytes chunks
+ * (O_DIRECT through the pinned ring, then H2D); every chunk of the replicated
+ * partitions is exchanged with one comm->allgather_bytes call (bytes =
+ * slot_bytes per rank; ranks whose partition is shorter send padding) and the
+ * unpack kernel scatters the gathered bytes into t[i] on `stream`; the rank's
+ * own local region comes from its own shard. GHDR / LHDR bytes are checked
+ * against the target list after the exchange. Collective: every rank of the
+ * DP group calls it together; a failure on any rank is returned on all ranks
+ * (status all-reduce before the first exchange and at the end). Synchronous.
+ * Errors: those of fp_ckpt_load, plus -ENOSYS when dp_size > 1 and
+ * comm->allgather_bytes is NULL.                                              */
+int fp_ckpt_load_parallel(fp_ctx *ctx, const fp_tensor *t, size_t n, const char *path,
+                          int dp_rank, int dp_size, void *stream);
 
 /* Image facts of the last planned checkpoint of this ctx: image/header bytes and
  * this rank's extents as (image_offset, file_offset, length) triples.

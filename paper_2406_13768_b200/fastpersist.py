@@ -46,10 +46,29 @@ class fp_tensor(C.Structure):
 AGFN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                    C.c_uint64)
 ARFN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_int32))
+ABFN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p)
 
 
 class fp_comm(C.Structure):
-    _fields_ = [("ctx", C.c_void_p), ("allgather_u64", AGFN), ("allreduce_min_i32", ARFN)]
+    _fields_ = [("ctx", C.c_void_p), ("allgather_u64", AGFN), ("allreduce_min_i32", ARFN),
+                ("allgather_bytes", ABFN)]
+
+
+class _DevBuf:
+    """Zero-copy torch view of raw device bytes (CUDA array interface)."""
+
+    def __init__(self, ptr, nbytes):
+        self.__cuda_array_interface__ = {"shape": (int(nbytes),), "typestr": "|u1",
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None}
+
+
+def dev_bytes(ptr, nbytes, device):
+    return torch.as_tensor(_DevBuf(ptr, nbytes), device=device)
+
+
+def host_bytes(ptr, nbytes):
+    return torch.frombuffer((C.c_uint8 * int(nbytes)).from_address(int(ptr)), dtype=torch.uint8)
 
 
 class fp_config(C.Structure):
@@ -72,7 +91,7 @@ class fp_stats(C.Structure):
 
 
 EXPORTS = ("fp_config_default", "fp_ckpt_init", "fp_ckpt_begin", "fp_ckpt_wait",
-           "fp_ckpt_load", "fp_ckpt_plan_info", "fp_ckpt_destroy", "fp_strerror",
+           "fp_ckpt_load", "fp_ckpt_load_parallel", "fp_ckpt_plan_info", "fp_ckpt_destroy", "fp_strerror",
            "fp_io_bench")
 
 _lib = None
@@ -95,6 +114,8 @@ def lib():
     L.fp_ckpt_wait.argtypes = [C.c_void_p, C.POINTER(fp_stats)]
     L.fp_ckpt_load.argtypes = [C.c_void_p, C.POINTER(fp_tensor), C.c_size_t, C.c_char_p,
                                C.c_int, C.c_int, C.c_void_p]
+    L.fp_ckpt_load_parallel.argtypes = [C.c_void_p, C.POINTER(fp_tensor), C.c_size_t,
+                                        C.c_char_p, C.c_int, C.c_int, C.c_void_p]
     L.fp_ckpt_plan_info.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                     C.POINTER(C.c_uint64), C.c_uint32, C.POINTER(C.c_uint32)]
     L.fp_ckpt_destroy.argtypes = [C.c_void_p]
@@ -165,7 +186,17 @@ class _CallbackComm:
         self.world = obj.world
         self.ag = AGFN(self._allgather)
         self.ar = ARFN(self._allreduce)
-        self.struct = fp_comm(None, self.ag, self.ar)
+        self.ab = ABFN(self._allgather_bytes)
+        self.struct = fp_comm(None, self.ag, self.ar,
+                              self.ab if hasattr(obj, "allgather_bytes") else ABFN())
+
+    def _allgather_bytes(self, _ctx, send, recv, n, on_device, stream):
+        try:
+            self.obj.allgather_bytes(send, recv, n, bool(on_device), stream)
+            return 0
+        except Exception as e:  # noqa: BLE001
+            print(f"fastpersist: allgather_bytes failed: {e}")
+            return -1
 
     def _allgather(self, _ctx, send, recv, n):
         try:
@@ -196,9 +227,34 @@ class _Comm:
         be = dist.get_backend(group)
         self.dev = device if be == "nccl" else torch.device("cpu")
         self.world = dist.get_world_size(group)
+        self.device = device
         self.ag = AGFN(self._allgather)
         self.ar = ARFN(self._allreduce)
-        self.struct = fp_comm(None, self.ag, self.ar)
+        self.ab = ABFN(self._allgather_bytes)
+        self.struct = fp_comm(None, self.ag, self.ar, self.ab)
+
+    def _allgather_bytes(self, _ctx, send, recv, n, on_device, stream):
+        """Parallel-load exchange: NCCL all-gather of device bytes
+        ordered on the library's stream; host bytes over the group's backend."""
+        try:
+            if on_device:
+                s = dev_bytes(send, n, self.device)
+                r = dev_bytes(recv, n * self.world, self.device)
+                with torch.cuda.stream(torch.cuda.ExternalStream(stream, device=self.device)):
+                    if self.dev.type == "cuda":
+                        self.dist.all_gather_into_tensor(r, s, group=self.group)
+                    else:                    # non-NCCL group: stage through host memory
+                        hs = s.cpu()
+                        hr = torch.empty(n * self.world, dtype=torch.uint8)
+                        self.dist.all_gather_into_tensor(hr, hs, group=self.group)
+                        r.copy_(hr)
+            else:
+                s, r = host_bytes(send, n), host_bytes(recv, n * self.world)
+                self.dist.all_gather_into_tensor(r, s, group=self.group)
+            return 0
+        except Exception as e:  # noqa: BLE001
+            print(f"fastpersist: allgather_bytes failed: {e}")
+            return -1
 
     def _allgather(self, _ctx, send, recv, n):
         try:
@@ -312,6 +368,13 @@ class Checkpointer:
         arr, n, keep = self._table(tensors)
         _check(lib().fp_ckpt_load(self.h, arr, n, os.fsencode(path), self.rank, self.world,
                                   _stream_handle(stream, self.device)), "fp_ckpt_load")
+
+    def load_parallel(self, tensors, path, stream=None):
+        """The paper's two-step load: own shard + all-gather + unpack."""
+        arr, n, keep = self._table(tensors)
+        _check(lib().fp_ckpt_load_parallel(self.h, arr, n, os.fsencode(path), self.rank,
+                                           self.world, _stream_handle(stream, self.device)),
+               "fp_ckpt_load_parallel")
 
     def plan_info(self):
         ib, hb, ne = C.c_uint64(), C.c_uint64(), C.c_uint32()

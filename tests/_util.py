@@ -90,6 +90,27 @@ class ThreadComm:
         self.sh.bar.wait()
         return out
 
+    def allgather_bytes(self, send, recv, n, on_device, stream):
+        """recv[r*n:(r+1)*n] = rank r's send (host memmove, or device copies
+        ordered after each rank's stream work)."""
+        import ctypes
+        if on_device:
+            from paper_2406_13768_b200.fastpersist import dev_bytes
+            st = torch.cuda.ExternalStream(stream)
+            st.synchronize()                       # our send is complete
+        self.sh.slots[self.rank] = send
+        self.sh.bar.wait()
+        for r in range(self.world):
+            if on_device:
+                dst = dev_bytes(recv + r * n, n, torch.device("cuda", 0))
+                with torch.cuda.stream(st):
+                    dst.copy_(dev_bytes(self.sh.slots[r], n, torch.device("cuda", 0)))
+            else:
+                ctypes.memmove(recv + r * n, self.sh.slots[r], n)
+        if on_device:
+            st.synchronize()                       # peers may reuse their send
+        self.sh.bar.wait()
+
 
 def run_threads(fns):
     """Run callables concurrently; re-raise the first exception."""

@@ -47,7 +47,10 @@ def _worker(rank, world, port, cfg, out_dir, mode, q):
                 q.put((rank, "err", e.code))
                 return
             dst = [(s, torch.zeros_like(t)) for s, t in st]
-            ck.load(entries(dst), out_dir)
+            if mode == "parallel":                # own shard + gloo all-gather
+                ck.load_parallel(entries(dst), out_dir)
+            else:
+                ck.load(entries(dst), out_dir)
             same = all(torch.equal(a.reshape(-1).view(torch.uint8), b.reshape(-1).view(torch.uint8))
                        for (_, a), (_, b) in zip(st, dst))
             q.put((rank, "ok", (stats["image_bytes"], stats["shard_bytes"], same)))
@@ -74,10 +77,11 @@ def _run(cfg, world, out_dir, mode="ok"):
     return res
 
 
-@pytest.mark.parametrize("cfg", ["gpt3_odd", "moe_small"])
-def test_gloo_world2_shards_match_oracle(tmp_path, cfg):
+@pytest.mark.parametrize("cfg,mode", [("gpt3_odd", "ok"), ("moe_small", "ok"),
+                                      ("moe_small", "parallel"), ("c1_tiny", "parallel")])
+def test_gloo_world2_shards_match_oracle(tmp_path, cfg, mode):
     world = 2
-    res = _run(cfg, world, str(tmp_path))
+    res = _run(cfg, world, str(tmp_path), mode)
     states = [make_state(config_specs(cfg, r, world), "cpu") for r in range(world)]
     lay = oracle_layout(states, world)
     ext = fpck.shard_extents(lay)

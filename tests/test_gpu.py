@@ -196,3 +196,28 @@ def test_c2_gpt3_1p3b_full_size_parity(tmp_path):
             f.seek(pg * 4096)
             assert f.read(4096) == lay.read(pg * 4096, 4096), pg
     assert file_sha(path) == fpck.shard_sha256(lay, 0)
+
+
+@pytest.mark.parametrize("cfg,k", [("gpt3_small", 4), ("moe_small", 2), ("c1_tiny", 3),
+                                   ("gpt3_odd", 1)])
+def test_load_parallel_device(tmp_path, cfg, k):
+    """P:503 two-step load on device: own shard -> H2D -> all-gather (ordered
+    on the library stream) -> unpack kernel scatter."""
+    states = [_state(cfg, r, k) for r in range(k)]
+    comms = ThreadComm.group(k)
+    cks = [fp.Checkpointer(DEV, comm=comms[r], slot_bytes=1 << 20) for r in range(k)]
+    try:
+        run_threads([lambda r=r: cks[r].save(entries(states[r]), str(tmp_path))
+                     for r in range(k)])
+        dst = [[(s, torch.full_like(t, 9) if t.is_floating_point() else torch.zeros_like(t))
+                for s, t in states[r]] for r in range(k)]
+        streams = [torch.cuda.Stream(DEV) for _ in range(k)]
+        run_threads([lambda r=r: cks[r].load_parallel(entries(dst[r]), str(tmp_path),
+                                                      stream=streams[r]) for r in range(k)])
+        torch.cuda.synchronize()
+        for r in range(k):
+            for (_, a), (_, b) in zip(states[r], dst[r]):
+                assert torch.equal(a.reshape(-1).view(torch.uint8), b.reshape(-1).view(torch.uint8))
+    finally:
+        for c in cks:
+            c.close()

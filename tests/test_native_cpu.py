@@ -227,3 +227,62 @@ def test_null_sink_engine_runs_the_pipeline_but_commits_nothing(tmp_path):
         with pytest.raises(FastPersistError) as ei:
             ck.load(entries(st), str(tmp_path))
         assert ei.value.code == -22
+
+
+@pytest.mark.parametrize("cfg,k", [("gpt3_odd", 3), ("moe_small", 4), ("c1_tiny", 2),
+                                   ("zero_small", 2), ("gpt3_small", 1)])
+def test_load_parallel_own_shard_plus_allgather(tmp_path, cfg, k):
+    """P:503 two-step load: each rank reads only its own shard, the replicated
+    partitions are all-gathered, local regions come from the own shard."""
+    states = [_state(cfg, r, k) for r in range(k)]
+    comms = ThreadComm.group(k)
+    cks = [fp.Checkpointer(None, comm=comms[r], slot_bytes=1 << 20) for r in range(k)]
+    try:
+        run_threads([lambda r=r: cks[r].save(entries(states[r]), str(tmp_path))
+                     for r in range(k)])
+        dst = [[(s, torch.zeros_like(t)) for s, t in states[r]] for r in range(k)]
+        run_threads([lambda r=r: cks[r].load_parallel(entries(dst[r]), str(tmp_path))
+                     for r in range(k)])
+        for r in range(k):
+            for (_, a), (_, b) in zip(states[r], dst[r]):
+                assert torch.equal(a.reshape(-1).view(torch.uint8), b.reshape(-1).view(torch.uint8))
+    finally:
+        for c in cks:
+            c.close()
+
+
+def test_load_parallel_errors_surface_on_every_rank(tmp_path):
+    k = 3
+    states = [_state("gpt3_odd", r, k) for r in range(k)]
+    comms = ThreadComm.group(k)
+    cks = [fp.Checkpointer(None, comm=comms[r], slot_bytes=1 << 20) for r in range(k)]
+
+    def load_all():
+        codes = [None] * k
+
+        def go(r):
+            try:
+                cks[r].load_parallel(entries(states[r]), str(tmp_path))
+                codes[r] = 0
+            except FastPersistError as e:
+                codes[r] = e.code
+        run_threads([lambda r=r: go(r) for r in range(k)])
+        return codes
+    try:
+        run_threads([lambda r=r: cks[r].save(entries(states[r]), str(tmp_path))
+                     for r in range(k)])
+        assert load_all() == [0, 0, 0]
+        # a flipped GHDR byte in rank 0's shard: every rank sees the gathered header
+        path = tmp_path / fpck.shard_name(0, k)
+        with open(path, "r+b") as f:
+            f.seek(70)
+            b = f.read(1)
+            f.seek(70)
+            f.write(bytes([b[0] ^ 0x5A]))
+        assert load_all() == [FP_ECORRUPT] * k
+        # rank 2's shard missing: every rank fails with ENOENT
+        os.unlink(tmp_path / fpck.shard_name(2, k))
+        assert load_all() == [-2] * k
+    finally:
+        for c in cks:
+            c.close()
