@@ -5,7 +5,7 @@
 
 Metric (BASELINE.json): "checkpoint persist GB/s and latency at 1/2/4/8 B200;
 % iter overhead per-iter ckpt". Workload: BASELINE.json configs[1], GPT-3 1.3B
-dense mixed-precision Adam state (adam16, 21,053,321,216-byte FPCK v2 image),
+dense mixed-precision Adam state (adam16, 21,053,362,176-byte FPCK v2 image),
 DP = N ranks, each persisting its page-balanced byte range (§4.2
 P:483-503) through the pinned ring with O_DIRECT io_uring writes (§4.1
 P:460-479). One step = one checkpoint: fp_ckpt_begin -> fp_ckpt_wait
@@ -237,7 +237,7 @@ def reference_arm(a):
     gbs, times, img = run_oracle_steps(sample, a.steps, root)
     shutil.rmtree(root, ignore_errors=True)
     sample_txt = (f"first {len(sample)} tensors of {CFG} in image order "
-                  f"({img} image bytes, {img / 21053321216:.3%} of the full image), "
+                  f"({img} image bytes, {img / 21053362176:.3%} of the full image), "
                   "host-resident, buffered write() + fsync, 1 rank")
     line = {"metric": METRIC,
             "value": round(gbs, 4), "unit": "GB/s", "impl": "reference",

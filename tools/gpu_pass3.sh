@@ -1,0 +1,14 @@
+#!/bin/bash
+# pass 3: parity of the new variants + parallel load, ablations, N=2 bench code path.
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+timeout 900 python -m pytest tests -m "gpu and not slow" -x -q > gpurun_out/pytest_gpu3.log 2>&1
+echo "pytest exit $?" >> gpurun_out/pytest_gpu3.log
+timeout 900 python tools/ablate.py --what pack > gpurun_out/ablate_pack.log 2>&1
+timeout 600 python tools/ablate.py --what buffer > gpurun_out/ablate_buffer.log 2>&1
+timeout 900 python tools/ablate.py --what prio --t-fb 4 --iters 3 > gpurun_out/ablate_prio.log 2>&1
+FP_BENCH_SHARE_GPU=1 timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+   --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 3 --warmup 3 \
+   --no-overhead --e2e-steps 1 > gpurun_out/bench_share2.json 2> gpurun_out/bench_share2.err
+echo "share2 exit $?" >> gpurun_out/bench_share2.err
+tail -3 gpurun_out/pytest_gpu3.log; cat gpurun_out/ablate_*.log | tail -40; cat gpurun_out/bench_share2.json; tail -5 gpurun_out/bench_share2.err
