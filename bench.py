@@ -516,8 +516,9 @@ def our_arm(a):
                          "peak_source": peak_src, "launch_avg_ms": round(launch_avg_ms, 5),
                          "bytes_per_launch": int(2 * pk_bytes / max(1, pk_launches))},
             "nvme": {"measured_gbs": round(nvme_gbs, 3), "frac": round(gbs / nvme_gbs, 4),
-                     "how": f"built-in O_DIRECT io_uring seq write (fio absent), {world} "
-                            f"concurrent writers x {nv_bytes} B, same dir, same run"},
+                     "how": f"built-in fp_io_bench (fio absent): O_DIRECT io_uring seq "
+                            f"overwrite, {a.qd} x {a.sqe_kib} KiB in flight, best of 2 timed passes, "
+                            f"{world} concurrent writers x {nv_bytes} B, same dir, same run"},
             "pcie_d2h": {"measured_gbs": round(d2h_gbs, 2), "frac": round(gbs / d2h_gbs, 4),
                          "ring_d2h_gbs": round(pk_bytes / (d2h_ms / 1e3) / 1e9, 2)
                          if d2h_ms > 0 else None},
@@ -549,7 +550,7 @@ def main():
     ap.add_argument("--ring-slots", type=int, default=4)
     ap.add_argument("--qd", type=int, default=64)
     ap.add_argument("--sqe-kib", type=int, default=1024)
-    ap.add_argument("--nvme-bytes", type=float, default=8e9)
+    ap.add_argument("--nvme-bytes", type=float, default=16e9)
     ap.add_argument("--oracle-bytes", type=float, default=1.5e9)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--overhead-iters", type=int, default=4)

@@ -111,6 +111,7 @@ enum fp_pack_impl { FP_PACK_V4 = 0,     /* LSU 16-B vector gather -> device slab
                                            a chunk, tensors -> pinned ring       */ };
 
 #define FP_CFG_NO_FSYNC 1u     /* skip fdatasync (benchmark ablation only)       */
+#define FP_CFG_NO_CRC   4u     /* skip the per-shard CRC-32          */
 #define FP_CFG_PRIO_LOW 2u     /* pack/D2H stream at the least priority (default:
                                   greatest)                    */
 
@@ -157,6 +158,10 @@ typedef struct fp_stats {
   int32_t  engine;         /* enum fp_io_engine actually used                     */
   int32_t  status;         /* final status of this checkpoint                     */
   int64_t  err_offset;     /* file offset of the first failed request, or -1      */
+  uint32_t shard_crc32;    /* CRC-32 (IEEE, = zlib.crc32) of this rank's shard
+                              file; computed on the GPU from the packed slab
+                              (host tensors: on the CPU); also in the manifest  */
+  uint32_t crc_valid;      /* 1 if shard_crc32 was computed                       */
 } fp_stats;
 
 typedef struct fp_ctx fp_ctx;
@@ -240,8 +245,9 @@ const char *fp_strerror(int err);
  * configured engine (O_DIRECT, io_depth x sqe_bytes from a registered pinned
  * ring) write `bytes` of non-compressible host data to `<dir>/fp_iobench.<tag>`
  * and fdatasync (untimed pass: allocates every block), then overwrite the same
- * file sequentially and fdatasync again (timed pass), unlink.
- * *gbps = bytes / (timed pass seconds) / 1e9.                                 */
+ * file sequentially and fdatasync again, twice (timed passes), unlink.
+ * *gbps = bytes / (faster timed pass seconds) / 1e9 — a roofline is the best
+ * the device did, not its average.                                            */
 int fp_io_bench(const char *dir, uint64_t bytes, const fp_config *cfg, int tag,
                 double *gbps);
 

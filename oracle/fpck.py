@@ -29,6 +29,7 @@ import hashlib
 import json
 import os
 import struct
+import zlib
 
 # ---------------------------------------------------------------------------
 # Constants of the FPCK v2 layout. Restated here, not imported.
@@ -292,6 +293,16 @@ def shard_sha256(layout, r):
     for b in iter_shard(layout, r):
         h.update(b)
     return h.hexdigest()
+
+
+def shard_crc32(layout, r):
+    """CRC-32 (IEEE 802.3 / zlib) of shard r's bytes — the integrity record the
+    manifest carries per shard (SPEC.md S:157 checksums in the
+    manifest). zlib.crc32 is the library routine; no custom arithmetic."""
+    c = 0
+    for b in iter_shard(layout, r):
+        c = zlib.crc32(b, c)
+    return c
 
 
 def save(layout, dirpath, ranks=None):

@@ -19,7 +19,7 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libfastpersist.so")
 BUILD = os.path.join(ROOT, "build")
 
-SOURCES = ["layout.cpp", "io.cpp", "runtime.cpp", "pack.cu"]
+SOURCES = ["layout.cpp", "io.cpp", "crc32.cpp", "runtime.cpp", "pack.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

@@ -139,5 +139,19 @@ int pack_launch(int impl, const Item* d_items, uint32_t n_items, uint8_t* d_slab
 int unpack_launch(const Item* d_items, uint32_t n_items, const uint8_t* d_slab, int ctas,
                   void* stream);
 int pack_default_ctas(int impl, int device);
+// raw CRC-32 of d_buf[0, bytes) per chunk_bytes chunk -> d_chunk_crc[]
+// (bytes, chunk_bytes: multiples of 4096; d_page_crc: bytes/4096 entries)
+int crc_launch(const uint8_t* d_buf, uint64_t bytes, uint64_t chunk_bytes, const uint32_t* d_tab8,
+               const uint32_t* d_lane_k, const uint32_t* d_x4k, uint32_t* d_page_crc,
+               uint32_t* d_chunk_crc, void* stream);
+
+// ---------------------------------------------------------------------------
+// CRC-32 helpers (crc32.cpp)
+// ---------------------------------------------------------------------------
+uint32_t gf_mul(uint32_t a, uint32_t b);          // a*b mod P, reflected
+uint32_t gf_x8n(uint64_t n);                      // x^(8n) mod P
+uint32_t crc_raw_update(uint32_t c, const uint8_t* p, uint64_t n);
+uint32_t crc_zeros(uint64_t n);                   // standard CRC-32 of n zero bytes
+const uint32_t* crc_tables8();                    // 8 x 256 slicing tables, contiguous
 
 }  // namespace fp

@@ -23,6 +23,7 @@
 //  fp_unpack_v4 : load path, slab -> tensors (zero items skipped).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cerrno>
 #include <cstdint>
 
@@ -227,6 +228,98 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------
+// CRC-32 of the packed bytes, raw form (init 0, no xorout; see
+// crc32.cpp): fp_crc_pages gives one raw CRC per 4 KiB page (warp per page,
+// lane l owns bytes [128 l, 128 l + 128), slicing-by-8 from shared-memory
+// tables, lanes combined with x^(8*128*(31-l)) and a warp XOR), then
+// fp_crc_chunks folds the pages of each ring chunk into one raw CRC (Horner
+// over x^(8*4096) per thread, then x^(8*4096*pages_after) and a block XOR).
+// ---------------------------------------------------------------------------
+constexpr uint32_t kCrcPoly = 0xEDB88320u;
+
+__device__ __forceinline__ uint32_t gf_mul_d(uint32_t a, uint32_t b) {
+  uint32_t p = 0;
+#pragma unroll 1
+  for (int i = 31; i >= 0 && a; --i) {
+    if (a & (1u << i)) {
+      p ^= b;
+      a &= ~(1u << i);
+    }
+    b = (b & 1) ? (b >> 1) ^ kCrcPoly : b >> 1;
+  }
+  return p;
+}
+
+__global__ void __launch_bounds__(256) fp_crc_pages(const uint8_t* __restrict__ buf,
+                                                    uint32_t n_pages,
+                                                    const uint32_t* __restrict__ tab8,
+                                                    const uint32_t* __restrict__ lane_k,
+                                                    uint32_t* __restrict__ out) {
+  __shared__ uint32_t t[8][256];
+  __shared__ uint32_t kl[32];
+  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) t[i >> 8][i & 255] = tab8[i];
+  if (threadIdx.x < 32) kl[threadIdx.x] = lane_k[threadIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const uint32_t wpb = blockDim.x >> 5;
+  for (uint32_t pg = blockIdx.x * wpb + (threadIdx.x >> 5); pg < n_pages; pg += gridDim.x * wpb) {
+    const uint4* src = reinterpret_cast<const uint4*>(buf + (size_t)pg * 4096 + lane * 128);
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = src[u];
+    uint32_t c = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      uint32_t lo = v[u].x ^ c, hi = v[u].y;
+      c = t[7][lo & 255] ^ t[6][(lo >> 8) & 255] ^ t[5][(lo >> 16) & 255] ^ t[4][lo >> 24] ^
+          t[3][hi & 255] ^ t[2][(hi >> 8) & 255] ^ t[1][(hi >> 16) & 255] ^ t[0][hi >> 24];
+      lo = v[u].z ^ c;
+      hi = v[u].w;
+      c = t[7][lo & 255] ^ t[6][(lo >> 8) & 255] ^ t[5][(lo >> 16) & 255] ^ t[4][lo >> 24] ^
+          t[3][hi & 255] ^ t[2][(hi >> 8) & 255] ^ t[1][(hi >> 16) & 255] ^ t[0][hi >> 24];
+    }
+    c = gf_mul_d(kl[lane], c);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c ^= __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) out[pg] = c;
+  }
+}
+
+// x^(8*4096*n) mod P from the table x4k[i] = x^(8*4096*2^i)
+__device__ __forceinline__ uint32_t x4k_pow(const uint32_t* x4k, uint32_t n) {
+  uint32_t p = 1u << 31;
+  for (int i = 0; n; ++i, n >>= 1)
+    if (n & 1) p = gf_mul_d(x4k[i], p);
+  return p;
+}
+
+__global__ void __launch_bounds__(256) fp_crc_chunks(const uint32_t* __restrict__ page_crc,
+                                                     uint32_t pages_per_chunk, uint32_t n_pages,
+                                                     const uint32_t* __restrict__ x4k_g,
+                                                     uint32_t* __restrict__ out) {
+  __shared__ uint32_t x4k[32];
+  __shared__ uint32_t red[8];
+  if (threadIdx.x < 32) x4k[threadIdx.x] = x4k_g[threadIdx.x];
+  __syncthreads();
+  const uint32_t p0 = blockIdx.x * pages_per_chunk;
+  const uint32_t p1 = min(p0 + pages_per_chunk, n_pages);
+  const uint32_t np = p1 - p0, per = (np + blockDim.x - 1) / blockDim.x;
+  const uint32_t b0 = min(np, threadIdx.x * per), b1 = min(np, b0 + per);
+  uint32_t acc = 0;
+  for (uint32_t i = b0; i < b1; ++i) acc = gf_mul_d(x4k[0], acc) ^ page_crc[p0 + i];
+  if (b1 > b0 && b1 < np) acc = gf_mul_d(x4k_pow(x4k, np - b1), acc);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t r = 0;
+    for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) r ^= red[w];
+    out[blockIdx.x] = r;
+  }
+}
+
 int sm_count(int device) {
   int d = device;
   if (d < 0 && cudaGetDevice(&d) != cudaSuccess) return 148;
@@ -260,6 +353,21 @@ int pack_launch(int impl, const Item* d_items, uint32_t n_items, uint8_t* d_slab
   } else {
     fp_pack_v4<<<grid, kV4Threads, 0, st>>>(d_items, n_items, d_slab);
   }
+  return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
+}
+
+int crc_launch(const uint8_t* d_buf, uint64_t bytes, uint64_t chunk_bytes, const uint32_t* d_tab8,
+               const uint32_t* d_lane_k, const uint32_t* d_x4k, uint32_t* d_page_crc,
+               uint32_t* d_chunk_crc, void* stream) {
+  if (!bytes) return 0;
+  if (bytes % 4096 || chunk_bytes % 4096) return -EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint32_t n_pages = (uint32_t)(bytes / 4096);
+  const uint32_t ppc = (uint32_t)(chunk_bytes / 4096);
+  const int grid_p = (int)std::min<uint32_t>((n_pages + 7) / 8, (uint32_t)sm_count(-1) * 8);
+  fp_crc_pages<<<grid_p, 256, 0, st>>>(d_buf, n_pages, d_tab8, d_lane_k, d_page_crc);
+  const uint32_t n_chunks = (n_pages + ppc - 1) / ppc;
+  fp_crc_chunks<<<n_chunks, 256, 0, st>>>(d_page_crc, ppc, n_pages, d_x4k, d_chunk_crc);
   return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
 }
 

@@ -30,6 +30,7 @@ FP_EMISMATCH, FP_ECORRUPT, FP_ECUDA, FP_ENODEV, FP_ECOMM = -1001, -1002, -1003, 
 FP_TENSOR_HOST = 1
 FP_CFG_NO_FSYNC = 1
 FP_CFG_PRIO_LOW = 2
+FP_CFG_NO_CRC = 4
 IO_ENGINES = {"uring": 0, "pwrite": 1, "buffered": 2, "null": 3}
 PACK_IMPLS = {"v4": 0, "bulk": 1, "host": 2, "ce": 3}
 SECTIONS = {"param": 0, "grad": 1, "master": 2, "exp_avg": 3, "exp_avg_sq": 4, "other": 5}
@@ -87,7 +88,7 @@ class fp_stats(C.Structure):
                 ("t_barrier", C.c_double), ("t_commit", C.c_double),
                 ("t_io_stall", C.c_double), ("max_inflight", C.c_uint32),
                 ("fallback", C.c_uint32), ("engine", C.c_int32), ("status", C.c_int32),
-                ("err_offset", C.c_int64)]
+                ("err_offset", C.c_int64), ("shard_crc32", C.c_uint32), ("crc_valid", C.c_uint32)]
 
 
 EXPORTS = ("fp_config_default", "fp_ckpt_init", "fp_ckpt_begin", "fp_ckpt_wait",
@@ -168,6 +169,8 @@ def make_config(**kw) -> fp_config:
             k, v = "pack_impl", PACK_IMPLS[v] if isinstance(v, str) else v
         elif k == "no_fsync":
             k, v = "flags", cfg.flags | (FP_CFG_NO_FSYNC if v else 0)
+        elif k == "no_crc":
+            k, v = "flags", cfg.flags | (FP_CFG_NO_CRC if v else 0)
         elif k == "prio":
             k, v = "flags", (cfg.flags & ~FP_CFG_PRIO_LOW) | (FP_CFG_PRIO_LOW if v == "low" else 0)
         elif k == "dirs":

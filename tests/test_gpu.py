@@ -31,9 +31,14 @@ def _state(cfg, rank=0, k=1, device=DEV):
     return make_state(config_specs(cfg, rank, k), device)
 
 
-def _check_rank_files(tmp, lay, k):
+def _check_rank_files(tmp, lay, k, crc=True):
     for r in range(k):
         assert file_sha(os.path.join(tmp, fpck.shard_name(r, k))) == fpck.shard_sha256(lay, r), r
+    if crc:   # per-shard CRC-32 computed on the GPU from the packed slab (f4)
+        import json
+        man = json.load(open(os.path.join(tmp, "manifest.json")))
+        for r in range(k):
+            assert man["shards"][r]["crc32"] == fpck.shard_crc32(lay, r), r
 
 
 @pytest.mark.parametrize("pack", ["v4", "bulk", "host", "ce"])
@@ -218,6 +223,38 @@ def test_load_parallel_device(tmp_path, cfg, k):
         for r in range(k):
             for (_, a), (_, b) in zip(states[r], dst[r]):
                 assert torch.equal(a.reshape(-1).view(torch.uint8), b.reshape(-1).view(torch.uint8))
+    finally:
+        for c in cks:
+            c.close()
+
+
+def test_load_parallel_device_detects_payload_corruption(tmp_path):
+    """The own-shard CRC-32 (GPU kernels over the H2D'd chunk) is checked
+    against the manifest on load: a flipped payload byte fails every rank."""
+    k = 2
+    states = [_state("gpt3_small", r, k) for r in range(k)]
+    comms = ThreadComm.group(k)
+    cks = [fp.Checkpointer(DEV, comm=comms[r], slot_bytes=1 << 20) for r in range(k)]
+    from paper_2406_13768_b200.fastpersist import FP_ECORRUPT, FastPersistError
+    try:
+        run_threads([lambda r=r: cks[r].save(entries(states[r]), str(tmp_path))
+                     for r in range(k)])
+        p1 = os.path.join(str(tmp_path), fpck.shard_name(1, k))
+        with open(p1, "r+b") as f:
+            f.seek(os.path.getsize(p1) - 5000)
+            b = f.read(1)
+            f.seek(os.path.getsize(p1) - 5000)
+            f.write(bytes([b[0] ^ 0x80]))
+        codes = [None] * k
+
+        def go(r):
+            try:
+                cks[r].load_parallel(entries(states[r]), str(tmp_path))
+                codes[r] = 0
+            except FastPersistError as e:
+                codes[r] = e.code
+        run_threads([lambda r=r: go(r) for r in range(k)])
+        assert codes == [FP_ECORRUPT] * k
     finally:
         for c in cks:
             c.close()

@@ -55,6 +55,8 @@ def test_host_save_matches_oracle(tmp_path, cfg, engine):
         assert ck.plan_info()["extents"] == [tuple(e) for e in fpck.shard_extents(lay)[0]]
     assert file_sha(tmp_path / "shard-0-of-1.fpck") == fpck.shard_sha256(lay, 0)
     man = json.load(open(tmp_path / "manifest.json"))
+    assert stats["crc_valid"] == 1
+    assert man["shards"][0]["crc32"] == stats["shard_crc32"] == fpck.shard_crc32(lay, 0)
     want = fpck.manifest_fields(lay)
     for key in ("image_bytes", "header_bytes", "alignment", "dp_size", "layout_digest"):
         assert man[key] == want[key], key
@@ -93,7 +95,9 @@ def test_dp_ranks_as_threads_match_oracle(tmp_path, cfg, k):
     try:
         res = run_threads([lambda r=r: cks[r].save(entries(states[r]), str(tmp_path))
                            for r in range(k)])
+        man = json.load(open(tmp_path / "manifest.json"))
         for r in range(k):
+            assert man["shards"][r]["crc32"] == res[r]["shard_crc32"] == fpck.shard_crc32(lay, r)
             assert cks[r].plan_info()["extents"] == [tuple(e) for e in
                                                      fpck.shard_extents(lay)[r]]
             assert res[r]["image_bytes"] == lay.image_bytes
@@ -271,6 +275,19 @@ def test_load_parallel_errors_surface_on_every_rank(tmp_path):
     try:
         run_threads([lambda r=r: cks[r].save(entries(states[r]), str(tmp_path))
                      for r in range(k)])
+        assert load_all() == [0, 0, 0]
+        # a flipped PAYLOAD byte in rank 1's shard: its CRC-32 no longer matches
+        # the manifest; the failure reaches every rank
+        p1 = tmp_path / fpck.shard_name(1, k)
+        with open(p1, "r+b") as f:
+            f.seek(os.path.getsize(p1) // 2)
+            b = f.read(1)
+            f.seek(os.path.getsize(p1) // 2)
+            f.write(bytes([b[0] ^ 1]))
+        assert load_all() == [FP_ECORRUPT] * k
+        with open(p1, "r+b") as f:           # restore
+            f.seek(os.path.getsize(p1) // 2)
+            f.write(b)
         assert load_all() == [0, 0, 0]
         # a flipped GHDR byte in rank 0's shard: every rank sees the gathered header
         path = tmp_path / fpck.shard_name(0, k)

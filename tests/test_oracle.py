@@ -294,3 +294,14 @@ def test_corruption_detected_by_decoder():
 def test_required_bandwidth_eq1():
     # Eq. 1: 107 GB over a 4.28 s fwd+bwd window needs 25 GB/s
     assert fpck.required_bandwidth(107e9, 2.14, 2.14) == pytest.approx(25e9, rel=1e-3)
+
+
+def test_crc32_library_pinned_to_check_value_and_oracle_shard_crc():
+    """zlib.crc32 is CRC-32/IEEE: the catalogue check value of b"123456789" is
+    0xCBF43926; the oracle's shard CRC is that routine over the shard bytes."""
+    import zlib
+    assert zlib.crc32(b"123456789") == 0xCBF43926
+    st = make_state(config_specs("gpt3_odd"), "cpu")
+    lay = fpck.Layout([fpck.OTensor(s.name, s.dtype, s.section, s.owner, s.shape, tbytes(t))
+                       for s, t in st])
+    assert fpck.shard_crc32(lay, 0) == zlib.crc32(lay.image())
