@@ -56,11 +56,13 @@ def ablate_pack(root):
     for sink in ["null", "uring"]:
         for pack in ["v4", "bulk", "host", "ce"]:
             for pb in ([64, 256] if pack in ("v4", "bulk") else [64]):
-                r = save_rate(ents, os.path.join(root, "ab"), io_engine=sink, pack=pack,
-                              pack_bytes=pb << 20, reps=2 if sink == "null" else 1)
-                r.update(sink=sink, pack=pack, pack_mib=pb)
-                print(json.dumps(r), flush=True)
-                res.append(r)
+                for crc in ([False, True] if pack == "v4" and pb == 256 else [False]):
+                    r = save_rate(ents, os.path.join(root, "ab"), io_engine=sink, pack=pack,
+                                  pack_bytes=pb << 20, reps=2 if sink == "null" else 1,
+                                  no_crc=not crc)
+                    r.update(sink=sink, pack=pack, pack_mib=pb, crc=crc)
+                    print(json.dumps(r), flush=True)
+                    res.append(r)
     return res
 
 
