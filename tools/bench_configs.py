@@ -40,11 +40,21 @@ T_FB_FLOPS = {  # 6 * P * GBS * seq at 40% of nominal bf16 over k ranks (SURVEY 
 
 
 class MirrorComm:
-    def __init__(self, rank, k):
+    """Answers the collectives of one rank of k. `peer_regions[r]` (optional)
+    = (region_bytes, n_local) rank r would report; by default every rank
+    reports this rank's own facts (exact for C3/C4, see module doc)."""
+
+    def __init__(self, rank, k, peer_regions=None):
         self.rank, self.world = rank, k
+        self.peer = peer_regions
 
     def allgather(self, vals):
-        return list(vals) * self.world
+        if self.peer is None or len(vals) != 4:   # 4 = the setup facts; else mirror
+            return list(vals) * self.world
+        out = []
+        for r in range(self.world):
+            out += [self.peer[r][0], self.peer[r][1]] + list(vals[2:])
+        return out
 
     def allreduce_min(self, v):
         return v
@@ -62,6 +72,7 @@ def main():
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--parity-pages", type=int, default=48)
     ap.add_argument("--pack", default="v4")
+    ap.add_argument("--full-crc", action="store_true")
     a = ap.parse_args()
     root = a.dir or os.path.join(os.environ.get("GRAFT_REPO_ROOT", "/tmp"), "cfg_ckpt")
     os.makedirs(root, exist_ok=True)
@@ -74,7 +85,20 @@ def main():
     ents = [(s.name, t, s.section, s.owner) for s, t in state]
     out = {"cfg": a.cfg, "k": a.k, "rank": a.rank, "state_bytes": sum(s.nbytes for s in specs),
            "tensors": len(specs), "gen_s": round(gen_s, 1), "dir": root}
-    comm = MirrorComm(a.rank, a.k)
+    peer = None
+    if a.cfg.startswith("c5"):
+        # experts have different names per rank (expert ids of 1 or 2 digits):
+        # each peer's local-region size is what that rank's own tensor list
+        # gives (header of 64 + 128 n + names, rounded to 4096, + payloads)
+        def rup(x, al=4096):
+            return (x + al - 1) // al * al
+        peer = []
+        for r in range(a.k):
+            loc = [x for x in config_specs(a.cfg, r, a.k) if x.owner >= 0]
+            names = sum(len(x.name.encode()) for x in loc)
+            peer.append((rup(64 + 128 * len(loc) + names) + sum(rup(x.nbytes) for x in loc),
+                         len(loc)))
+    comm = MirrorComm(a.rank, a.k, peer)
     ck = fp.Checkpointer(dev, comm=comm, pack=a.pack, no_fsync=a.no_fsync)
     lat, stats = [], []
     for i in range(a.steps + 1):
@@ -98,10 +122,11 @@ def main():
     from tests._util import otensor
     rep = [otensor(s, t, lazy=True) for s, t in state if s.owner < 0]
     mine = [otensor(s, t, lazy=True) for s, t in state if s.owner >= 0]
-    local = [mine if r == a.rank else [fpck.OTensor(x.name.replace(f"zero{a.rank}.", f"zero{r}."),
-                                                    x.dtype, x.section, r, x.shape,
-                                                    lambda o, n: b"\0" * n)
-                                       for x in mine] for r in range(a.k)] if mine else None
+    def stub(x, r):   # a peer's local tensor: only its size matters for this shard
+        return fpck.OTensor(x.name, x.dtype, x.section, r, x.shape, lambda o, n: b"\0" * n)
+    local = [mine if r == a.rank else [stub(x, r) for x in config_specs(a.cfg, r, a.k)
+                                       if x.owner >= 0]
+             for r in range(a.k)] if mine else None
     lay = fpck.Layout(rep, local, k=a.k)
     ext = fpck.shard_extents(lay)[a.rank]
     path = os.path.join(root, "step", fpck.shard_name(a.rank, a.k))
@@ -119,6 +144,16 @@ def main():
     out["parity_pages_bad"] = bad
     out["oracle_image_bytes"] = lay.image_bytes
     print(json.dumps(out), flush=True)
+    if a.full_crc:
+        # every byte of the shard: the GPU's CRC-32 (from the packed slabs)
+        # against zlib.crc32 over the oracle's shard bytes of the same tensors
+        t0 = time.time()
+        want = fpck.shard_crc32(lay, a.rank)
+        out["crc_gpu"] = stats[-1]["shard_crc32"]
+        out["crc_oracle"] = want
+        out["crc_match"] = bool(stats[-1]["crc_valid"]) and stats[-1]["shard_crc32"] == want
+        out["crc_oracle_s"] = round(time.time() - t0, 1)
+        print(json.dumps(out), flush=True)
     if a.overhead:
         n = 8192
         A = torch.randn(n, n, device=dev, dtype=torch.bfloat16)
