@@ -402,8 +402,12 @@ int fp_ctx::save_shard() {
       const uint64_t c1 = std::min<uint64_t>(g0 + G, C);
       const uint64_t gbytes = std::min<uint64_t>(c1 * S, plan.shard_bytes) - c * S;
       if (c == 0) CK(cudaStreamWaitEvent(stream, ev_producer, 0));
-      const bool gated = wait_value != nullptr;
-      if (gated && wait_value(stream, d_gate, gate_seq + 1, 0 /*GEQ*/)) return FP_ECUDA;
+      bool gated = wait_value != nullptr;
+      if (gated && wait_value(stream, d_gate, gate_seq + 1, 0 /*GEQ*/)) {
+        wait_value = nullptr;  // stream memory ops refused: run ungated from now on
+        gated = false;
+        cudaGetLastError();
+      }
       // the gate is opened on every path out of this block: a stream left
       // waiting on it would never drain
       int r = cudaEventRecord(ev_p0[s], stream) == cudaSuccess ? 0 : FP_ECUDA;
