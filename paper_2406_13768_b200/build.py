@@ -19,14 +19,14 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libfastpersist.so")
 BUILD = os.path.join(ROOT, "build")
 
-SOURCES = ["layout.cpp", "io.cpp", "crc32.cpp", "runtime.cpp", "pack.cu"]
+SOURCES = ["layout.cpp", "io.cpp", "crc32.cpp", "runtime.cpp", "load.cpp", "pack.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 
 def _newest_input():
     paths = [os.path.join(CSRC, s) for s in SOURCES]
-    paths += [os.path.join(CSRC, "fp_internal.h"), os.path.join(INCLUDE, "fastpersist.h"),
+    paths += [os.path.join(CSRC, "fp_internal.h"), os.path.join(CSRC, "ctx.h"), os.path.join(INCLUDE, "fastpersist.h"),
               os.path.abspath(__file__)]
     return max(os.path.getmtime(p) for p in paths)
 

@@ -1,0 +1,117 @@
+// Internal runtime context of libfastpersist (shared by runtime.cpp and
+// load.cpp; not part of the C-ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <condition_variable>
+#include <cstdio>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "fp_internal.h"
+
+namespace fp {
+
+// cuStreamWaitValue32 (driver API, fetched at run time so the library does
+// not link libcuda): the stream waits until *addr >= value.
+typedef int (*WaitValue32Fn)(cudaStream_t, uint64_t, uint32_t, unsigned int);
+
+double now_s();
+uint64_t env_u64(const char* k, uint64_t dflt);
+std::string join_path(const std::string& a, const std::string& b);
+int mkdirs(const std::string& path);
+int fsync_dir(const std::string& dir);
+std::string shard_file(int r, int k);
+
+#define CK(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess) {                                                         \
+      fprintf(stderr, "fastpersist: %s failed: %s\n", #x, cudaGetErrorString(e_));  \
+      return FP_ECUDA;                                                               \
+    }                                                                                \
+  } while (0)
+
+}  // namespace fp
+
+using fp::Extent;
+using fp::IoEngine;
+using fp::Item;
+using fp::Plan;
+using fp::TensorRef;
+using fp::WaitValue32Fn;
+
+struct fp_ctx {
+  fp_config cfg;
+  std::string dirs_copy;
+  std::vector<std::string> roots;
+  int dev = -1;
+  fp_comm comm;
+  bool has_comm = false;
+  // resources
+  uint8_t* ring = nullptr;
+  uint8_t* d_ring = nullptr;  // device alias of the mapped ring (FP_PACK_HOST)
+  size_t ring_bytes = 0;
+  bool ring_cuda_registered = false;
+  uint8_t* d_slab = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_producer = nullptr;
+  std::vector<cudaEvent_t> ev_p0, ev_p1, ev_d0, ev_d2h;
+  std::vector<uint8_t> has_pack;  // per ring slot: its chunk led a pack launch
+  // launch gate: the pack group's [event, kernel, event] are queued behind a
+  // cuStreamWaitValue32 on a mapped pinned flag that the host releases after
+  // the whole group is enqueued, so the events time the kernel, not the host
+  // API latency of an idle stream
+  WaitValue32Fn wait_value = nullptr;
+  volatile uint32_t* h_gate = nullptr;
+  uint64_t d_gate = 0;
+  uint32_t gate_seq = 0;
+  // CRC-32 of the shard
+  uint32_t *d_crc_tab8 = nullptr, *d_lane_k = nullptr, *d_x4k = nullptr;
+  uint32_t *d_page_crc = nullptr, *d_chunk_crc = nullptr, *h_crc = nullptr;
+  IoEngine* io = nullptr;
+  int pack_ctas = 0;
+  // plan cache
+  bool planned = false;
+  uint64_t sig_meta = 0, sig_ptr = 0;
+  Plan plan;
+  std::vector<TensorRef> rep, loc;
+  bool host = false;
+  std::vector<Item> items;
+  std::vector<uint32_t> item_lo;
+  std::vector<Item> runs;          // FP_PACK_CE: items merged into contiguous runs
+  std::vector<uint32_t> run_lo;
+  Item* d_items = nullptr;
+  size_t d_items_cap = 0;
+  uint8_t* d_hdr = nullptr;
+  size_t d_hdr_cap = 0;
+  std::vector<uint8_t> h_hdr;
+  std::vector<std::vector<Extent>> all_extents;
+  std::vector<uint64_t> shard_crcs;  // per rank: bit 32 = valid, low 32 = CRC-32
+  // request
+  std::string shard_dir, manifest_dir;
+  int rank = 0, k = 1;
+  // helper thread
+  std::thread th;
+  std::mutex mu;
+  std::condition_variable cv;
+  enum State { IDLE, PENDING, RUNNING, DONE } state = IDLE;
+  bool stop = false;
+  int result = 0;
+  fp_stats st;
+  double t_begin = 0;
+
+  int save_shard();
+  void helper();
+  int write_manifest();
+};
+
+namespace fp {
+// plan setup shared by save and load (runtime.cpp)
+int ensure_plan(fp_ctx* c, const fp_tensor* t, size_t n, int rank, int k);
+int build_items(fp_ctx* c, bool for_save);
+void resolve_dirs(fp_ctx* c, const char* path, int rank);
+}  // namespace fp

@@ -1,5 +1,5 @@
 // libfastpersist runtime: context, pinned ring, helper thread, begin/wait,
-// manifest commit and load.
+// manifest commit, storage roofline tool (load paths: load.cpp).
 //
 // PAPER.md §4.3: "The helper thread executes an infinite loop where
 // it blocks until woken by the main thread to create checkpoints ... writes the
@@ -9,7 +9,8 @@
 // request to the helper thread after optimizer." The paper needed a second
 // Python *process* per rank because of the GIL (§5.1); here the helper is
 // a native thread of the same process (no GIL, shared CUDA context), driving
-// the pack kernel on a lowest-priority stream, the copy engine into the pinned
+// the pack kernel on its own stream (greatest priority by default, see
+// DESIGN.md §6), the copy engine into the pinned
 // ring (double/multi buffering, §4.1) and io_uring (§4.1).
 // Durability precedes completion (§3.2: direct to persistent storage).
 #include <cuda_runtime.h>
@@ -30,15 +31,12 @@
 #include <string>
 #include <thread>
 
-#include "fp_internal.h"
+#include "ctx.h"
 
 using namespace fp;
 
-// cuStreamWaitValue32 (driver API, fetched at run time so the library does
-// not link libcuda): the stream waits until *addr >= value.
-typedef int (*WaitValue32Fn)(cudaStream_t, uint64_t, uint32_t, unsigned int);
 
-namespace {
+namespace fp {
 
 double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
@@ -83,192 +81,16 @@ int fsync_dir(const std::string& dir) {
   return r;
 }
 
-#define CK(x)                                                                        \
-  do {                                                                               \
-    cudaError_t e_ = (x);                                                            \
-    if (e_ != cudaSuccess) {                                                         \
-      fprintf(stderr, "fastpersist: %s failed: %s\n", #x, cudaGetErrorString(e_));  \
-      return FP_ECUDA;                                                               \
-    }                                                                                \
-  } while (0)
+
 
 std::string shard_file(int r, int k) {
   return "shard-" + std::to_string(r) + "-of-" + std::to_string(k) + ".fpck";
 }
 
-// --------------------------------------------------------------------------
-// minimal JSON reader for our own manifest (objects, arrays, ints, strings)
-// --------------------------------------------------------------------------
-struct JVal {
-  enum T { NUL, NUM, STR, ARR, OBJ } t = NUL;
-  unsigned long long num = 0;
-  std::string str;
-  std::vector<JVal> arr;
-  std::vector<std::pair<std::string, JVal>> obj;
-  const JVal* get(const char* k) const {
-    for (auto& kv : obj)
-      if (kv.first == k) return &kv.second;
-    return nullptr;
-  }
-};
 
-struct JParser {
-  const char* p;
-  const char* e;
-  bool ok = true;
-  void ws() {
-    while (p < e && (*p == ' ' || *p == '\n' || *p == '\t' || *p == '\r')) ++p;
-  }
-  bool str(std::string* out) {
-    if (p >= e || *p != '"') return ok = false;
-    ++p;
-    while (p < e && *p != '"') {
-      if (*p == '\\' && p + 1 < e) ++p;
-      out->push_back(*p++);
-    }
-    if (p >= e) return ok = false;
-    ++p;
-    return true;
-  }
-  JVal val() {
-    JVal v;
-    ws();
-    if (p >= e) {
-      ok = false;
-      return v;
-    }
-    if (*p == '{') {
-      v.t = JVal::OBJ;
-      ++p;
-      ws();
-      if (p < e && *p == '}') {
-        ++p;
-        return v;
-      }
-      while (ok) {
-        ws();
-        std::string k;
-        if (!str(&k)) break;
-        ws();
-        if (p >= e || *p != ':') {
-          ok = false;
-          break;
-        }
-        ++p;
-        v.obj.push_back({k, val()});
-        ws();
-        if (p < e && *p == ',') {
-          ++p;
-          continue;
-        }
-        if (p < e && *p == '}') {
-          ++p;
-          break;
-        }
-        ok = false;
-      }
-    } else if (*p == '[') {
-      v.t = JVal::ARR;
-      ++p;
-      ws();
-      if (p < e && *p == ']') {
-        ++p;
-        return v;
-      }
-      while (ok) {
-        v.arr.push_back(val());
-        ws();
-        if (p < e && *p == ',') {
-          ++p;
-          continue;
-        }
-        if (p < e && *p == ']') {
-          ++p;
-          break;
-        }
-        ok = false;
-      }
-    } else if (*p == '"') {
-      v.t = JVal::STR;
-      str(&v.str);
-    } else {
-      v.t = JVal::NUM;
-      char* end = nullptr;
-      v.num = strtoull(p, &end, 10);
-      if (end == p) ok = false;
-      p = end;
-    }
-    return v;
-  }
-};
-
-}  // namespace
+}  // namespace fp
 
 // ===========================================================================
-struct fp_ctx {
-  fp_config cfg;
-  std::string dirs_copy;
-  std::vector<std::string> roots;
-  int dev = -1;
-  fp_comm comm;
-  bool has_comm = false;
-  // resources
-  uint8_t* ring = nullptr;
-  uint8_t* d_ring = nullptr;  // device alias of the mapped ring (FP_PACK_HOST)
-  size_t ring_bytes = 0;
-  bool ring_cuda_registered = false;
-  uint8_t* d_slab = nullptr;
-  cudaStream_t stream = nullptr;
-  cudaEvent_t ev_producer = nullptr;
-  std::vector<cudaEvent_t> ev_p0, ev_p1, ev_d0, ev_d2h;
-  std::vector<uint8_t> has_pack;  // per ring slot: its chunk led a pack launch
-  // launch gate: the pack group's [event, kernel, event] are queued behind a
-  // cuStreamWaitValue32 on a mapped pinned flag that the host releases after
-  // the whole group is enqueued, so the events time the kernel, not the host
-  // API latency of an idle stream
-  WaitValue32Fn wait_value = nullptr;
-  volatile uint32_t* h_gate = nullptr;
-  uint64_t d_gate = 0;
-  uint32_t gate_seq = 0;
-  // CRC-32 of the shard
-  uint32_t *d_crc_tab8 = nullptr, *d_lane_k = nullptr, *d_x4k = nullptr;
-  uint32_t *d_page_crc = nullptr, *d_chunk_crc = nullptr, *h_crc = nullptr;
-  IoEngine* io = nullptr;
-  int pack_ctas = 0;
-  // plan cache
-  bool planned = false;
-  uint64_t sig_meta = 0, sig_ptr = 0;
-  Plan plan;
-  std::vector<TensorRef> rep, loc;
-  bool host = false;
-  std::vector<Item> items;
-  std::vector<uint32_t> item_lo;
-  std::vector<Item> runs;          // FP_PACK_CE: items merged into contiguous runs
-  std::vector<uint32_t> run_lo;
-  Item* d_items = nullptr;
-  size_t d_items_cap = 0;
-  uint8_t* d_hdr = nullptr;
-  size_t d_hdr_cap = 0;
-  std::vector<uint8_t> h_hdr;
-  std::vector<std::vector<Extent>> all_extents;
-  std::vector<uint64_t> shard_crcs;  // per rank: bit 32 = valid, low 32 = CRC-32
-  // request
-  std::string shard_dir, manifest_dir;
-  int rank = 0, k = 1;
-  // helper thread
-  std::thread th;
-  std::mutex mu;
-  std::condition_variable cv;
-  enum State { IDLE, PENDING, RUNNING, DONE } state = IDLE;
-  bool stop = false;
-  int result = 0;
-  fp_stats st;
-  double t_begin = 0;
-
-  int save_shard();
-  void helper();
-  int write_manifest();
-};
 
 // ---------------------------------------------------------------------------
 // the helper's chunk pipeline: pack -> D2H -> io_uring, ring of R slots
@@ -620,7 +442,7 @@ static uint64_t sig_hash(const std::vector<TensorRef>& rep, const std::vector<Te
 // (Re)plan when the tensor signature changed; (re)build items when pointers
 // changed. hdr_for_items: true for save (header pages are gathered), false for
 // load (header pieces become skip items).
-static int ensure_plan(fp_ctx* c, const fp_tensor* t, size_t n, int rank, int k) {
+int fp::ensure_plan(fp_ctx* c, const fp_tensor* t, size_t n, int rank, int k) {
   std::vector<TensorRef> rep, loc;
   bool host = false;
   int r = import_tensors(t, n, rank, &rep, &loc, &host);
@@ -694,7 +516,7 @@ static int ensure_plan(fp_ctx* c, const fp_tensor* t, size_t n, int rank, int k)
   return 0;
 }
 
-static int build_items(fp_ctx* c, bool for_save) {
+int fp::build_items(fp_ctx* c, bool for_save) {
   const uint64_t base = !for_save ? 0
                         : c->host ? (uint64_t)(uintptr_t)c->h_hdr.data()
                                   : (uint64_t)(uintptr_t)c->d_hdr;
@@ -738,7 +560,7 @@ static int build_items(fp_ctx* c, bool for_save) {
   return 0;
 }
 
-static void resolve_dirs(fp_ctx* c, const char* path, int rank) {
+void fp::resolve_dirs(fp_ctx* c, const char* path, int rank) {
   const std::string p = path ? path : "";
   if (c->roots.empty()) {
     c->shard_dir = p;
@@ -1015,573 +837,6 @@ int fp_ckpt_wait(fp_ctx* c, fp_stats* out) {
   if (out) *out = c->st;
   std::lock_guard<std::mutex> g(c->mu);
   c->state = fp_ctx::IDLE;
-  return status;
-}
-
-// ---------------------------------------------------------------------------
-// load: manifest -> header check -> O_DIRECT reads -> H2D -> unpack kernel
-// ---------------------------------------------------------------------------
-static int read_file(const std::string& path, std::string* out) {
-  int fd = open(path.c_str(), O_RDONLY);
-  if (fd < 0) return -errno;
-  char buf[65536];
-  for (;;) {
-    ssize_t n = read(fd, buf, sizeof(buf));
-    if (n < 0) {
-      if (errno == EINTR) continue;
-      int e = -errno;
-      close(fd);
-      return e;
-    }
-    if (n == 0) break;
-    out->append(buf, (size_t)n);
-  }
-  close(fd);
-  return 0;
-}
-
-static int pread_all(int fd, void* buf, uint64_t len, uint64_t off) {
-  uint64_t done = 0;
-  while (done < len) {
-    ssize_t n = pread(fd, (char*)buf + done, len - done, (off_t)(off + done));
-    if (n < 0) {
-      if (errno == EINTR) continue;
-      return -errno;
-    }
-    if (n == 0) return -EIO;
-    done += (uint64_t)n;
-  }
-  return 0;
-}
-
-int fp_ckpt_load(fp_ctx* c, const fp_tensor* t, size_t n, const char* path, int dp_rank,
-                 int dp_size, void* stream) {
-  if (!c || (!t && n) || !path || dp_size < 1 || dp_rank < 0 || dp_rank >= dp_size)
-    return -EINVAL;
-  if (dp_size > 1 && !c->has_comm) return -EINVAL;
-  if (c->cfg.io_engine == FP_IO_NULL) return -EINVAL;  // nothing was ever written
-  {
-    std::lock_guard<std::mutex> g(c->mu);
-    if (c->state != fp_ctx::IDLE) return -EBUSY;
-  }
-  resolve_dirs(c, path, dp_rank);
-  const std::string mpath = join_path(c->manifest_dir, "manifest.json");
-  std::string mtxt;
-  int r = read_file(mpath, &mtxt);
-  if (r) {
-    fprintf(stderr, "fastpersist: cannot read %s: %s\n", mpath.c_str(), strerror(-r));
-    return r;
-  }
-  JParser jp{mtxt.data(), mtxt.data() + mtxt.size()};
-  JVal m = jp.val();
-  if (!jp.ok || m.t != JVal::OBJ) return FP_ECORRUPT;
-  auto num = [&](const char* k) -> uint64_t {
-    const JVal* v = m.get(k);
-    return v && v->t == JVal::NUM ? v->num : ~0ull;
-  };
-  if (num("dp_size") != (uint64_t)dp_size || num("alignment") != c->cfg.alignment)
-    return FP_EMISMATCH;
-  r = ensure_plan(c, t, n, dp_rank, dp_size);
-  if (r) return r;
-  Plan& p = c->plan;
-  if (num("image_bytes") != p.image_bytes || num("layout_digest") != p.digest)
-    return FP_EMISMATCH;
-  const JVal* shards = m.get("shards");
-  if (!shards || shards->t != JVal::ARR || (int)shards->arr.size() != dp_size) return FP_ECORRUPT;
-  // open every shard we may read from (single box: all files visible; the
-  // NCCL all-gather variant of P:503 reads only its own shard)
-  const size_t nroots = c->roots.empty() ? 1 : c->roots.size();
-  std::vector<int> fds(dp_size, -1);
-  auto close_all = [&] {
-    for (int fd : fds)
-      if (fd >= 0) close(fd);
-  };
-  for (int w = 0; w < dp_size; ++w) {
-    const std::string dir =
-        c->roots.empty() ? std::string(path) : join_path(c->roots[w % nroots], path);
-    const std::string f = join_path(dir, shard_file(w, dp_size));
-    int fd = open(f.c_str(), O_RDONLY | O_DIRECT);
-    if (fd < 0 && errno == EINVAL) fd = open(f.c_str(), O_RDONLY);
-    if (fd < 0) {
-      r = -errno;
-      fprintf(stderr, "fastpersist: missing shard %s: %s\n", f.c_str(), strerror(errno));
-      close_all();
-      return r;
-    }
-    struct stat sb;
-    uint64_t want = 0;
-    for (auto& e : c->all_extents[w]) want += e.len;
-    if (fstat(fd, &sb) || (uint64_t)sb.st_size != want) {
-      fprintf(stderr, "fastpersist: shard %s has %lld bytes, expected %llu\n", f.c_str(),
-              (long long)sb.st_size, (unsigned long long)want);
-      fds[w] = fd;
-      close_all();
-      return FP_ECORRUPT;
-    }
-    fds[w] = fd;
-  }
-  // image offset -> (shard, file offset) for the bytes this rank needs
-  const uint32_t A = p.align;
-  auto locate = [&](uint64_t io, int* w_out, uint64_t* fo, uint64_t* avail) -> bool {
-    for (int w = 0; w < dp_size; ++w)
-      for (auto& e : c->all_extents[w])
-        if (io >= e.image_off && io < e.image_off + e.len) {
-          *w_out = w;
-          *fo = e.file_off + (io - e.image_off);
-          *avail = e.image_off + e.len - io;
-          return true;
-        }
-    return false;
-  };
-  // 1) header check: GHDR and our LREG header must match the target list
-  {
-    std::vector<std::pair<uint64_t, const std::vector<uint8_t>*>> hdrs = {{0, &p.ghdr.bytes}};
-    if (!p.regions.empty()) hdrs.push_back({p.regions[dp_rank].first, &p.lhdr.bytes});
-    for (auto& h : hdrs) {
-      std::vector<uint8_t> tmp;
-      uint64_t got = 0;
-      while (got < h.second->size()) {
-        int w;
-        uint64_t fo, avail;
-        if (!locate(h.first + got, &w, &fo, &avail)) {
-          close_all();
-          return FP_ECORRUPT;
-        }
-        const uint64_t nn = std::min<uint64_t>(avail, h.second->size() - got);
-        // bounce through an aligned buffer for O_DIRECT
-        const uint64_t span = round_up(nn, A);
-        void* bb = nullptr;
-        if (posix_memalign(&bb, A, span)) {
-          close_all();
-          return -ENOMEM;
-        }
-        int fd2 = open(join_path(c->roots.empty() ? std::string(path)
-                                                  : join_path(c->roots[w % nroots], path),
-                                 shard_file(w, dp_size))
-                           .c_str(),
-                       O_RDONLY);
-        r = fd2 < 0 ? -errno : pread_all(fd2, bb, nn, fo);
-        if (fd2 >= 0) close(fd2);
-        if (r) {
-          free(bb);
-          close_all();
-          return r;
-        }
-        tmp.insert(tmp.end(), (uint8_t*)bb, (uint8_t*)bb + nn);
-        free(bb);
-        got += nn;
-      }
-      if (memcmp(tmp.data(), h.second->data(), tmp.size())) {
-        fprintf(stderr, "fastpersist: header at image offset %llu does not match the target "
-                        "tensors (corrupt or different state)\n",
-                (unsigned long long)h.first);
-        close_all();
-        return FP_ECORRUPT;
-      }
-    }
-  }
-  // 2) load stream = replicated region, then our local region
-  Plan lp = p;
-  lp.extents.clear();
-  lp.extents.push_back({0, 0, p.rep_bytes});
-  uint64_t total = p.rep_bytes;
-  if (!p.regions.empty()) {
-    lp.extents.push_back({p.regions[dp_rank].first, total, p.regions[dp_rank].second});
-    total += p.regions[dp_rank].second;
-  }
-  lp.shard_bytes = total;
-  plan_pieces(&lp, c->rep, c->loc, 0);  // header pieces -> skip items
-  std::vector<Item> items;
-  std::vector<uint32_t> lo;
-  plan_items(lp, c->cfg.slot_bytes, c->cfg.slot_bytes, &items, &lo);
-  Item* d_items = nullptr;
-  if (!c->host && !items.empty()) {
-    if (cudaMalloc(&d_items, items.size() * sizeof(Item)) != cudaSuccess ||
-        cudaMemcpy(d_items, items.data(), items.size() * sizeof(Item), cudaMemcpyHostToDevice) !=
-            cudaSuccess) {
-      if (d_items) cudaFree(d_items);
-      close_all();
-      return FP_ECUDA;
-    }
-  }
-  const uint64_t S = c->cfg.slot_bytes, SQ = c->cfg.sqe_bytes;
-  const uint64_t C = lo.size() - 1;
-  cudaStream_t st = (cudaStream_t)stream;
-  int status = 0;
-  IoDone done[64];
-  for (uint64_t ch = 0; ch < C && !status; ++ch) {
-    const uint32_t s = (uint32_t)(ch % c->cfg.ring_slots);
-    uint8_t* slot = c->ring + (size_t)s * S;
-    const uint64_t len = std::min<uint64_t>(S, total - ch * S);
-    // read [ch*S, ch*S+len) of the load stream
-    uint32_t inflight = 0;
-    uint64_t pos = 0;
-    while (pos < len && !status) {
-      const uint64_t ls = ch * S + pos;  // load-stream offset -> image offset
-      uint64_t io = 0;
-      for (auto& e : lp.extents)
-        if (ls >= e.file_off && ls < e.file_off + e.len) io = e.image_off + (ls - e.file_off);
-      int w;
-      uint64_t fo, avail;
-      if (!locate(io, &w, &fo, &avail)) {
-        status = FP_ECORRUPT;
-        break;
-      }
-      const uint32_t nn = (uint32_t)std::min<uint64_t>({SQ, len - pos, avail});
-      while (inflight >= c->io->capacity()) {
-        c->io->submit();
-        int k2 = c->io->reap(done, 64, 1);
-        if (k2 < 0) {
-          status = k2;
-          break;
-        }
-        for (int i = 0; i < k2; ++i)
-          if (done[i].res < 0 && !status) status = done[i].res;
-        inflight -= (uint32_t)k2;
-      }
-      if (status) break;
-      int q = c->io->queue(false, fds[w], slot + pos, nn, fo, (int)s, nn);
-      if (q) {
-        status = q;
-        break;
-      }
-      ++inflight;
-      pos += nn;
-    }
-    c->io->submit();
-    while (inflight > 0) {
-      int k2 = c->io->reap(done, 64, 1);
-      if (k2 < 0) {
-        if (!status) status = k2;
-        break;
-      }
-      for (int i = 0; i < k2; ++i)
-        if (done[i].res != (int32_t)done[i].user && !status)
-          status = done[i].res < 0 ? done[i].res : -EIO;
-      inflight -= (uint32_t)k2;
-    }
-    if (status) break;
-    if (c->host) {
-      for (uint32_t i = lo[ch]; i < lo[ch + 1]; ++i)
-        if (items[i].src) memcpy((void*)(uintptr_t)items[i].src, slot + items[i].dst, items[i].len);
-    } else {
-      if (cudaMemcpyAsync(c->d_slab, slot, len, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-          unpack_launch(d_items + lo[ch], lo[ch + 1] - lo[ch], c->d_slab, c->pack_ctas, st) ||
-          cudaStreamSynchronize(st) != cudaSuccess)
-        status = FP_ECUDA;
-    }
-  }
-  if (d_items) cudaFree(d_items);
-  close_all();
-  return status;
-}
-
-// ---------------------------------------------------------------------------
-// parallel load: own shard only + one all-gather per chunk + unpack
-// ---------------------------------------------------------------------------
-static size_t total_chunks_hint(uint64_t nrep, uint64_t nloc) { return (size_t)(nrep + nloc); }
-
-static int status_min(fp_ctx* c, int k, int s) {
-  if (k <= 1) return s;
-  int32_t v = s;
-  if (c->comm.allreduce_min_i32(c->comm.ctx, &v)) return s ? s : FP_ECOMM;
-  return v;
-}
-
-// Read [off, off+len) of fd into buf (inside ring slot `slot`) with the I/O
-// engine in sqe_bytes requests; blocks until all complete. 0 or -errno.
-static int read_span(fp_ctx* c, int fd, uint8_t* buf, uint64_t len, uint64_t off, int slot) {
-  IoDone done[64];
-  uint32_t inflight = 0;
-  uint64_t pos = 0;
-  int status = 0;
-  while ((pos < len || inflight) && !status) {
-    while (pos < len && inflight < c->io->capacity()) {
-      const uint32_t nn = (uint32_t)std::min<uint64_t>(c->cfg.sqe_bytes, len - pos);
-      int q = c->io->queue(false, fd, buf + pos, nn, off + pos, slot, nn);
-      if (q == -EAGAIN) break;
-      if (q) return q;
-      ++inflight;
-      pos += nn;
-    }
-    int r = c->io->submit();
-    if (r) return r;
-    int k2 = c->io->reap(done, 64, 1);
-    if (k2 < 0) return k2;
-    for (int i = 0; i < k2; ++i)
-      if (done[i].res != (int32_t)done[i].user && !status)
-        status = done[i].res < 0 ? done[i].res : -EIO;
-    inflight -= (uint32_t)k2;
-  }
-  while (inflight) {  // drain after an error
-    int k2 = c->io->reap(done, 64, 1);
-    if (k2 < 0) break;
-    inflight -= (uint32_t)k2;
-  }
-  return status;
-}
-
-// Items scattering image range [io0, io0+len) (located at buffer offset
-// `base`) into the tensors; header/padding pieces are skipped.
-static void scatter_items(const std::vector<Piece>& pcs, uint64_t io0, uint64_t len, uint64_t base,
-                          std::vector<Item>* items) {
-  const uint64_t io1 = io0 + len;
-  size_t lo = 0, hi = pcs.size();
-  while (lo < hi) {  // first piece ending after io0
-    const size_t mid = (lo + hi) / 2;
-    if (pcs[mid].image_off + pcs[mid].len <= io0)
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  for (size_t i = lo; i < pcs.size() && pcs[i].image_off < io1; ++i) {
-    if (!pcs[i].src) continue;
-    uint64_t a = std::max(io0, pcs[i].image_off);
-    const uint64_t b = std::min(io1, pcs[i].image_off + pcs[i].len);
-    while (a < b) {
-      const uint64_t nn = std::min<uint64_t>(b - a, kTile);
-      items->push_back({pcs[i].src + (a - pcs[i].image_off), (uint32_t)(base + a - io0),
-                        (uint32_t)nn});
-      a += nn;
-    }
-  }
-}
-
-int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* path,
-                          int dp_rank, int dp_size, void* stream) {
-  if (!c || (!t && n) || !path || dp_size < 1 || dp_rank < 0 || dp_rank >= dp_size)
-    return -EINVAL;
-  if (dp_size > 1 && !c->has_comm) return -EINVAL;
-  if (dp_size > 1 && !c->comm.allgather_bytes) return -ENOSYS;
-  if (c->cfg.io_engine == FP_IO_NULL) return -EINVAL;
-  {
-    std::lock_guard<std::mutex> g(c->mu);
-    if (c->state != fp_ctx::IDLE) return -EBUSY;
-  }
-  const int k = dp_size, rank = dp_rank;
-  resolve_dirs(c, path, rank);
-  // 1) manifest; every rank must succeed before the (collective) plan setup
-  const std::string mpath = join_path(c->manifest_dir, "manifest.json");
-  std::string mtxt;
-  int r = read_file(mpath, &mtxt);
-  if (r) fprintf(stderr, "fastpersist: cannot read %s: %s\n", mpath.c_str(), strerror(-r));
-  JVal m;
-  if (!r) {
-    JParser jp{mtxt.data(), mtxt.data() + mtxt.size()};
-    m = jp.val();
-    if (!jp.ok || m.t != JVal::OBJ) r = FP_ECORRUPT;
-  }
-  auto num = [&](const char* key) -> uint64_t {
-    const JVal* v = m.get(key);
-    return v && v->t == JVal::NUM ? v->num : ~0ull;
-  };
-  if (!r && (num("dp_size") != (uint64_t)k || num("alignment") != c->cfg.alignment))
-    r = FP_EMISMATCH;
-  r = status_min(c, k, r);
-  if (r) return r;
-  r = ensure_plan(c, t, n, rank, k);  // all-gather of sizes when the signature is new
-  if (r) return r;
-  const Plan& p = c->plan;
-  if (num("image_bytes") != p.image_bytes || num("layout_digest") != p.digest) r = FP_EMISMATCH;
-  // 2) this rank's own shard, nothing else
-  const std::string sf = join_path(c->shard_dir, shard_file(rank, k));
-  int fd = -1;
-  if (!r) {
-    fd = open(sf.c_str(), O_RDONLY | O_DIRECT);
-    if (fd < 0 && errno == EINVAL) fd = open(sf.c_str(), O_RDONLY);
-    if (fd < 0) {
-      r = -errno;
-      fprintf(stderr, "fastpersist: missing shard %s: %s\n", sf.c_str(), strerror(errno));
-    } else {
-      struct stat sb;
-      uint64_t want = 0;
-      for (auto& e : c->all_extents[rank]) want += e.len;
-      if (fstat(fd, &sb) || (uint64_t)sb.st_size != want) {
-        fprintf(stderr, "fastpersist: shard %s has %lld bytes, expected %llu\n", sf.c_str(),
-                (long long)sb.st_size, (unsigned long long)want);
-        r = FP_ECORRUPT;
-      }
-    }
-  }
-  r = status_min(c, k, r);
-  if (r) {
-    if (fd >= 0) close(fd);
-    return r;
-  }
-  // 3) geometry: replicated partitions (the writer's page-balanced split)
-  const uint64_t A = p.align, Q = p.rep_bytes / A, q = Q / k, rem = Q % k;
-  auto first_pg = [&](int w) { return (uint64_t)w * q + std::min<uint64_t>(w, rem); };
-  auto part_bytes = [&](int w) { return (q + ((uint64_t)w < rem ? 1 : 0)) * A; };
-  const uint64_t CH = c->cfg.slot_bytes, M = part_bytes(0);
-  const uint64_t nrep = (M + CH - 1) / CH;
-  const bool dev = !c->host;
-  Plan rp = p;  // whole replicated region (+ own local region) as one source map
-  rp.extents.assign(1, {0, 0, p.rep_bytes});
-  if (!p.regions.empty()) rp.extents.push_back({p.regions[rank].first, p.rep_bytes,
-                                                p.regions[rank].second});
-  plan_pieces(&rp, c->rep, c->loc, 0);  // header pieces -> src 0 (skipped)
-  std::vector<Item> items;
-  std::vector<uint32_t> lo(1, 0);
-  for (uint64_t j = 0; j < nrep; ++j) {
-    for (int w = 0; w < k; ++w) {
-      const uint64_t pb = part_bytes(w);
-      if (j * CH >= pb) continue;
-      scatter_items(rp.pieces, first_pg(w) * A + j * CH, std::min(CH, pb - j * CH),
-                    (uint64_t)w * CH, &items);
-    }
-    lo.push_back((uint32_t)items.size());
-  }
-  const uint64_t lreg_off = p.regions.empty() ? 0 : p.regions[rank].first;
-  const uint64_t lreg_len = p.regions.empty() ? 0 : p.regions[rank].second;
-  const uint64_t nloc = (lreg_len + CH - 1) / CH;
-  for (uint64_t j = 0; j < nloc; ++j) {
-    scatter_items(rp.pieces, lreg_off + j * CH, std::min(CH, lreg_len - j * CH), 0, &items);
-    lo.push_back((uint32_t)items.size());
-  }
-  // 4) buffers: send = one chunk, recv = k chunks (device, or host for host state)
-  uint8_t *send = nullptr, *recv = nullptr;
-  Item* d_items = nullptr;
-  cudaStream_t st = (cudaStream_t)stream;
-  int status = 0;
-  if (dev) {
-    if (cudaMalloc(&send, CH) != cudaSuccess || cudaMalloc(&recv, CH * k) != cudaSuccess ||
-        (!items.empty() && (cudaMalloc(&d_items, items.size() * sizeof(Item)) != cudaSuccess ||
-                            cudaMemcpy(d_items, items.data(), items.size() * sizeof(Item),
-                                       cudaMemcpyHostToDevice) != cudaSuccess)))
-      status = -ENOMEM;
-  } else {
-    send = (uint8_t*)aligned_alloc(4096, round_up(CH, 4096));
-    recv = (uint8_t*)aligned_alloc(4096, round_up(CH * k, 4096));
-    if (!send || !recv) status = -ENOMEM;
-  }
-  status = status_min(c, k, status);
-  std::vector<uint8_t> ghdr_got(p.ghdr.bytes.size(), 0), lhdr_got(p.lhdr.bytes.size(), 0);
-  const uint32_t R = c->cfg.ring_slots;
-  auto fetch_hdr = [&](const uint8_t* buf, uint64_t io0, uint64_t len, uint64_t base,
-                       uint64_t h0, std::vector<uint8_t>* out) {
-    // copy the header bytes [h0, h0+out.size()) that fall in this buffer
-    const uint64_t a = std::max(io0, h0), b = std::min(io0 + len, h0 + out->size());
-    if (a >= b) return;
-    if (dev)
-      cudaMemcpyAsync(out->data() + (a - h0), buf + base + (a - io0), b - a,
-                      cudaMemcpyDeviceToHost, st);
-    else
-      memcpy(out->data() + (a - h0), buf + base + (a - io0), b - a);
-  };
-  const uint64_t total_chunks = nrep + nloc;
-  // CRC-32 of the own shard as it is read, checked against the manifest
-  const JVal* shard_rec = nullptr;
-  if (const JVal* sh = m.get("shards"))
-    if (sh->t == JVal::ARR && (int)sh->arr.size() == k) shard_rec = &sh->arr[rank];
-  const JVal* want_crc = shard_rec ? shard_rec->get("crc32") : nullptr;
-  const bool check_crc = want_crc && want_crc->t == JVal::NUM && !(c->cfg.flags & FP_CFG_NO_CRC);
-  uint32_t* chunk_crc = nullptr;  // raw CRC per chunk (pinned when the GPU computes it)
-  std::vector<uint64_t> chunk_len(total_chunks_hint(nrep, nloc), 0);
-  bool crc_pinned = false;
-  if (check_crc) {
-    crc_pinned = dev && cudaHostAlloc(&chunk_crc, (chunk_len.size() + 1) * 4,
-                                      cudaHostAllocPortable) == cudaSuccess;
-    if (!crc_pinned) chunk_crc = (uint32_t*)calloc(chunk_len.size() + 1, 4);
-  }
-  const bool run = status == 0;  // agreed on every rank by the all-reduce above
-  for (uint64_t j = 0; run && j < total_chunks; ++j) {  // every rank runs every exchange
-    const bool is_rep = j < nrep;
-    const uint32_t s = (uint32_t)(j % R);
-    uint8_t* slot = c->ring + (size_t)s * c->cfg.slot_bytes;
-    if (dev && j >= R) cudaEventSynchronize(c->ev_d2h[s]);  // H2D out of this slot done
-    uint64_t mylen, foff;
-    if (is_rep) {
-      const uint64_t pb = part_bytes(rank);
-      mylen = j * CH < pb ? std::min(CH, pb - j * CH) : 0;
-      foff = j * CH;
-    } else {
-      const uint64_t jj = j - nrep;
-      mylen = std::min(CH, lreg_len - jj * CH);
-      foff = part_bytes(rank) + jj * CH;
-    }
-    int rr = mylen ? read_span(c, fd, slot, mylen, foff, (int)s) : 0;
-    if (rr && !status) status = rr;  // keep exchanging so the collectives stay matched
-    const bool gpu_crc = check_crc && dev && mylen % 4096 == 0 && c->d_crc_tab8;
-    if (check_crc && mylen && !gpu_crc) chunk_crc[j] = crc_raw_update(0, slot, mylen);
-    chunk_len[j] = mylen;
-    if (dev) {
-      if (mylen && cudaMemcpyAsync(send, slot, mylen, cudaMemcpyHostToDevice, st) != cudaSuccess)
-        status = status ? status : FP_ECUDA;
-      cudaEventRecord(c->ev_d2h[s], st);
-      if (gpu_crc && mylen &&
-          (crc_launch(send, mylen, mylen, c->d_crc_tab8, c->d_lane_k, c->d_x4k, c->d_page_crc,
-                      c->d_chunk_crc, st) ||
-           cudaMemcpyAsync(&chunk_crc[j], c->d_chunk_crc, 4, cudaMemcpyDeviceToHost, st) !=
-               cudaSuccess))
-        status = status ? status : FP_ECUDA;
-    } else if (mylen) {
-      memcpy(send, slot, mylen);
-    }
-    const uint8_t* src = send;
-    if (is_rep) {
-      if (k > 1) {
-        if (c->comm.allgather_bytes(c->comm.ctx, send, recv, CH, dev ? 1 : 0, stream)) {
-          status = status ? status : FP_ECOMM;
-          break;
-        }
-        src = recv;
-      }
-      for (int w = 0; w < k; ++w) {
-        const uint64_t pb = part_bytes(w);
-        if (j * CH >= pb) continue;
-        fetch_hdr(src, first_pg(w) * A + j * CH, std::min(CH, pb - j * CH),
-                  k > 1 ? (uint64_t)w * CH : 0, 0, &ghdr_got);
-      }
-    } else {
-      const uint64_t jj = j - nrep;
-      fetch_hdr(src, lreg_off + jj * CH, mylen, 0, lreg_off, &lhdr_got);
-    }
-    const uint32_t i0 = lo[j], i1 = lo[j + 1];
-    if (i1 > i0 && status == 0) {
-      if (dev) {
-        if (unpack_launch(d_items + i0, i1 - i0, src, c->pack_ctas, st)) status = FP_ECUDA;
-      } else {
-        for (uint32_t i = i0; i < i1; ++i)
-          memcpy((void*)(uintptr_t)items[i].src, src + items[i].dst, items[i].len);
-      }
-    }
-  }
-  if (dev && cudaStreamSynchronize(st) != cudaSuccess && !status) status = FP_ECUDA;
-  if (!status && check_crc && run) {
-    uint32_t raw = 0;
-    uint64_t tot = 0;
-    for (size_t j = 0; j < chunk_len.size(); ++j) {
-      if (!chunk_len[j]) continue;
-      raw = gf_mul(gf_x8n(chunk_len[j]), raw) ^ chunk_crc[j];
-      tot += chunk_len[j];
-    }
-    const uint32_t got = raw ^ crc_zeros(tot);
-    if (got != (uint32_t)want_crc->num) {
-      fprintf(stderr, "fastpersist: shard %s CRC-32 %08x != manifest %08x (corrupt data)\n",
-              sf.c_str(), got, (unsigned)want_crc->num);
-      status = FP_ECORRUPT;
-    }
-  }
-  if (crc_pinned)
-    cudaFreeHost(chunk_crc);
-  else
-    free(chunk_crc);
-  if (!status && (memcmp(ghdr_got.data(), p.ghdr.bytes.data(), ghdr_got.size()) ||
-                  memcmp(lhdr_got.data(), p.lhdr.bytes.data(), lhdr_got.size()))) {
-    fprintf(stderr, "fastpersist: header bytes gathered from the shards do not match the "
-                    "target tensors (corrupt or different state)\n");
-    status = FP_ECORRUPT;
-  }
-  status = status_min(c, k, status);
-  if (dev) {
-    if (send) cudaFree(send);
-    if (recv) cudaFree(recv);
-    if (d_items) cudaFree(d_items);
-  } else {
-    free(send);
-    free(recv);
-  }
-  close(fd);
   return status;
 }
 
