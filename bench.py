@@ -493,6 +493,15 @@ def our_arm(a):
 
     if rank == 0:
         hbm = float(peaks["hbm_gbs"])
+        kname = {"v4": "fp_pack_v4", "bulk": "fp_pack_bulk"}.get(a.pack)
+        traffic = a.traffic
+        try:   # ncu-measured DRAM bytes per launch of this launch shape (profiles/)
+            with open(os.path.join(ROOT, "profiles", "pack_traffic.json")) as f:
+                tr = json.load(f).get(kname or "", {})
+            if traffic is None and tr.get("bytes_per_launch") == (a.pack_mib << 21):
+                traffic = tr["dram_bytes"]
+        except (OSError, ValueError):
+            pass
         launch_avg_ms = pk_ms / max(1, pk_launches)
         line = {
             "metric": METRIC,
@@ -512,7 +521,7 @@ def our_arm(a):
             "roofline": {"bound": "hbm", "kernel": {"v4": "fp_pack_v4", "bulk": "fp_pack_bulk",
                                     "host": "fp_pack_v4 (to mapped host)", "ce": None}[a.pack],
                          "achieved": round(pack_gbs, 1), "peak": hbm, "unit": "GB/s",
-                         "frac": round(pack_gbs / hbm, 4), "traffic": a.traffic,
+                         "frac": round(pack_gbs / hbm, 4), "traffic": traffic,
                          "peak_source": peak_src, "launch_avg_ms": round(launch_avg_ms, 5),
                          "bytes_per_launch": int(2 * pk_bytes / max(1, pk_launches))},
             "nvme": {"measured_gbs": round(nvme_gbs, 3), "frac": round(gbs / nvme_gbs, 4),
@@ -522,7 +531,7 @@ def our_arm(a):
             "pcie_d2h": {"measured_gbs": round(d2h_gbs, 2), "frac": round(gbs / d2h_gbs, 4),
                          "ring_d2h_gbs": round(pk_bytes / (d2h_ms / 1e3) / 1e9, 2)
                          if d2h_ms > 0 else None},
-            "hbm": {"frac_of_ckpt": round(gbs / (hbm * world), 6)},
+            "hbm": {"peak_gbs_all_gpus": hbm * world, "frac": round(gbs / (hbm * world), 6)},
             "phase_s_last": {k: round(stats[-1][k], 4) for k in
                              ("t_helper", "t_fsync", "t_barrier", "t_commit", "t_io_stall")},
             "gpu_launches": int(launches_all),
