@@ -130,6 +130,12 @@ typedef struct fp_config {
   const char *dirs;      /* nullable: comma-separated roots; rank r's shard goes
                             under dirs[r % n]; the manifest under dirs[0].
                             NULL: `path` is used as given.                       */
+  uint32_t writer_stride;/* writer subset: only ranks r with
+                            r % writer_stride == 0 write replicated bytes
+                            (e.g. one writer per CPU socket, the paper's
+                            "Socket" strategy); 0/1 = every rank ("Replica").
+                            Rank-local regions are always written by their
+                            owner. Default 1 (env FP_WRITER_STRIDE).          */
   uint64_t pack_bytes;   /* bytes gathered per pack-kernel launch (device slab
                             size); rounded up to a multiple of slot_bytes, so one
                             launch feeds pack_bytes/slot_bytes ring slots; 0 =

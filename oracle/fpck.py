@@ -248,19 +248,23 @@ def partition_units(Q, k):
     return out
 
 
-def shard_extents(layout: Layout):
+def shard_extents(layout: Layout, writer_stride=1):
     """Per rank: [(image_offset, file_offset, length)] in image order.
 
-    The replicated region is split page-granular (reading R5); rank r's local
-    region LREG_r goes wholly to rank r (reading R9)."""
+    The replicated region is split page-granular (reading R5) over the
+    writers — every rank, or with writer_stride s only ranks 0, s, 2s, ...
+    (the paper's writer subsets, "use a subset of DP ranks", P:495-499);
+    rank r's local region LREG_r goes wholly to rank r (reading R9)."""
     A = layout.align
     Q = layout.rep_bytes // A
-    parts = partition_units(Q, layout.k)
+    s = max(1, writer_stride)
+    writers = [r for r in range(layout.k) if r % s == 0]
+    wparts = dict(zip(writers, partition_units(Q, len(writers))))
     ext = []
     for r in range(layout.k):
         e = []
         fo = 0
-        p0, npg = parts[r]
+        p0, npg = wparts.get(r, (0, 0))
         if npg:
             e.append((p0 * A, 0, npg * A))
             fo = npg * A
@@ -275,12 +279,12 @@ def shard_name(r, k):
     return f"shard-{r}-of-{k}.fpck"
 
 
-def shard_bytes(layout, r):
-    return b"".join(layout.read(io, n) for io, _, n in shard_extents(layout)[r])
+def shard_bytes(layout, r, writer_stride=1):
+    return b"".join(layout.read(io, n) for io, _, n in shard_extents(layout, writer_stride)[r])
 
 
-def iter_shard(layout, r, piece=64 << 20):
-    for io, _, n in shard_extents(layout)[r]:
+def iter_shard(layout, r, piece=64 << 20, writer_stride=1):
+    for io, _, n in shard_extents(layout, writer_stride)[r]:
         p = 0
         while p < n:
             m = min(piece, n - p)
@@ -288,19 +292,19 @@ def iter_shard(layout, r, piece=64 << 20):
             p += m
 
 
-def shard_sha256(layout, r):
+def shard_sha256(layout, r, writer_stride=1):
     h = hashlib.sha256()
-    for b in iter_shard(layout, r):
+    for b in iter_shard(layout, r, writer_stride=writer_stride):
         h.update(b)
     return h.hexdigest()
 
 
-def shard_crc32(layout, r):
+def shard_crc32(layout, r, writer_stride=1):
     """CRC-32 (IEEE 802.3 / zlib) of shard r's bytes — the integrity record the
     manifest carries per shard (SPEC.md S:157 checksums in the
     manifest). zlib.crc32 is the library routine; no custom arithmetic."""
     c = 0
-    for b in iter_shard(layout, r):
+    for b in iter_shard(layout, r, writer_stride=writer_stride):
         c = zlib.crc32(b, c)
     return c
 

@@ -60,7 +60,7 @@ struct Piece {
 
 // Everything rank `rank` needs to write (or read) its shard.
 struct Plan {
-  uint32_t align = 4096;
+  uint32_t align = 4096, writer_stride = 1;
   int rank = 0, k = 1;
   uint64_t header_bytes = 0, rep_bytes = 0, image_bytes = 0, digest = 0;
   std::vector<std::pair<uint64_t, uint64_t>> regions;  // (offset, bytes) per rank or empty
@@ -80,9 +80,16 @@ struct LocalFacts {
 };
 void plan_local_facts(const std::vector<TensorRef>& rep, const std::vector<TensorRef>& loc,
                       uint32_t align, LocalFacts* out);
+// Replicated-region partition (writer subsets P:495-499): the Q
+// pages go to the writers w = 0, s, 2s, ... (s = writer_stride, 0/1 = every
+// rank) in contiguous page-balanced ranges in rank order, the lowest writers
+// taking the extra pages; a non-writer gets no pages.
+void rep_partition(uint64_t Q, int k, uint32_t writer_stride, int w, uint64_t* first_page,
+                   uint64_t* n_pages);
 // Layout pass 2: needs all ranks' facts (k entries). Returns 0 / FP_EMISMATCH.
 int plan_build(const std::vector<TensorRef>& rep, const std::vector<TensorRef>& loc,
-               uint32_t align, int rank, int k, const std::vector<LocalFacts>& all, Plan* out);
+               uint32_t align, int rank, int k, uint32_t writer_stride,
+               const std::vector<LocalFacts>& all, Plan* out);
 // Rebase header pieces onto hdr_base (ghdr at +0, lhdr at +ghdr.size());
 // hdr_base == 0 turns header pieces into skip (zero) items, as load needs.
 void plan_pieces(Plan* p, const std::vector<TensorRef>& rep, const std::vector<TensorRef>& loc,

@@ -168,8 +168,25 @@ void plan_local_facts(const std::vector<TensorRef>& rep, const std::vector<Tenso
   out->rep_bytes = rb;
 }
 
+void rep_partition(uint64_t Q, int k, uint32_t writer_stride, int w, uint64_t* first_page,
+                   uint64_t* n_pages) {
+  const uint64_t s = writer_stride > 1 ? writer_stride : 1;
+  const uint64_t nw = ((uint64_t)k + s - 1) / s;  // writers: ranks 0, s, 2s, ...
+  const uint64_t q = Q / nw, rem = Q % nw;
+  if ((uint64_t)w % s) {  // not a writer: empty range at the next writer's start
+    const uint64_t i = (uint64_t)w / s + 1;
+    *first_page = i >= nw ? Q : i * q + std::min<uint64_t>(i, rem);
+    *n_pages = 0;
+    return;
+  }
+  const uint64_t i = (uint64_t)w / s;
+  *first_page = i * q + std::min<uint64_t>(i, rem);
+  *n_pages = q + (i < rem ? 1 : 0);
+}
+
 int plan_build(const std::vector<TensorRef>& rep, const std::vector<TensorRef>& loc,
-               uint32_t align, int rank, int k, const std::vector<LocalFacts>& all, Plan* p) {
+               uint32_t align, int rank, int k, uint32_t writer_stride,
+               const std::vector<LocalFacts>& all, Plan* p) {
   for (int r = 1; r < k; ++r)
     if (all[r].digest != all[0].digest || all[r].rep_bytes != all[0].rep_bytes)
       return FP_EMISMATCH;
@@ -177,6 +194,7 @@ int plan_build(const std::vector<TensorRef>& rep, const std::vector<TensorRef>& 
   for (int r = 0; r < k; ++r) has_local |= all[r].n_local > 0;
   const uint64_t n_reg = has_local ? (uint64_t)k : 0;
   p->align = align;
+  p->writer_stride = writer_stride > 1 ? writer_stride : 1;
   p->rank = rank;
   p->k = k;
   p->header_bytes = header_len(rep.size(), n_reg, names_bytes(rep), align);
@@ -208,12 +226,10 @@ int plan_build(const std::vector<TensorRef>& rep, const std::vector<TensorRef>& 
     if (c - start != p->regions[rank].second) return FP_EMISMATCH;
     encode_header(loc, p->loc_off, {}, align, c - start, rank, kFlagLocal, &p->lhdr);
   }
-  // partition of the replicated region: Q pages over k ranks, contiguous in
-  // rank order, sizes differ by <= 1 page, lowest ranks take the extra pages
-  const uint64_t Q = p->rep_bytes / align;
-  const uint64_t q = Q / k, rem = Q % k;
-  const uint64_t first = (uint64_t)rank * q + std::min<uint64_t>(rank, rem);
-  const uint64_t npg = q + ((uint64_t)rank < rem ? 1 : 0);
+  // partition of the replicated region: Q pages over the writers, contiguous
+  // in rank order, sizes differ by <= 1 page, lowest writers take the extras
+  uint64_t first = 0, npg = 0;
+  rep_partition(p->rep_bytes / align, k, p->writer_stride, rank, &first, &npg);
   p->extents.clear();
   uint64_t fo = 0;
   if (npg) {

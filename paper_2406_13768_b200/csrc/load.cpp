@@ -123,6 +123,16 @@ struct JParser {
   }
 };
 
+// Loads plan with the writer subset recorded in the manifest (absent = 1).
+struct WriterStrideScope {
+  fp_ctx* c;
+  uint32_t saved;
+  WriterStrideScope(fp_ctx* ctx, unsigned long long ws) : c(ctx), saved(ctx->cfg.writer_stride) {
+    c->cfg.writer_stride = (ws == ~0ull || ws == 0) ? 1u : (uint32_t)ws;
+  }
+  ~WriterStrideScope() { c->cfg.writer_stride = saved; }
+};
+
 }  // namespace
 
 extern "C" {
@@ -190,6 +200,8 @@ int fp_ckpt_load(fp_ctx* c, const fp_tensor* t, size_t n, const char* path, int 
   };
   if (num("dp_size") != (uint64_t)dp_size || num("alignment") != c->cfg.alignment)
     return FP_EMISMATCH;
+  // the partition is the writer's (its writer subset), not this context's
+  WriterStrideScope wss(c, num("writer_stride"));
   r = ensure_plan(c, t, n, dp_rank, dp_size);
   if (r) return r;
   Plan& p = c->plan;
@@ -488,6 +500,7 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
     r = FP_EMISMATCH;
   r = status_min(c, k, r);
   if (r) return r;
+  WriterStrideScope wss(c, num("writer_stride"));  // the writer's partition
   r = ensure_plan(c, t, n, rank, k);  // all-gather of sizes when the signature is new
   if (r) return r;
   const Plan& p = c->plan;
@@ -518,10 +531,18 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
     return r;
   }
   // 3) geometry: replicated partitions (the writer's page-balanced split)
-  const uint64_t A = p.align, Q = p.rep_bytes / A, q = Q / k, rem = Q % k;
-  auto first_pg = [&](int w) { return (uint64_t)w * q + std::min<uint64_t>(w, rem); };
-  auto part_bytes = [&](int w) { return (q + ((uint64_t)w < rem ? 1 : 0)) * A; };
-  const uint64_t CH = c->cfg.slot_bytes, M = part_bytes(0);
+  const uint64_t A = p.align, Q = p.rep_bytes / A;
+  auto first_pg = [&](int w) {
+    uint64_t f, n;
+    rep_partition(Q, k, p.writer_stride, w, &f, &n);
+    return f;
+  };
+  auto part_bytes = [&](int w) {
+    uint64_t f, n;
+    rep_partition(Q, k, p.writer_stride, w, &f, &n);
+    return n * A;
+  };
+  const uint64_t CH = c->cfg.slot_bytes, M = part_bytes(0);  // writer 0 has the largest part
   const uint64_t nrep = (M + CH - 1) / CH;
   const bool dev = !c->host;
   Plan rp = p;  // whole replicated region (+ own local region) as one source map

@@ -364,10 +364,11 @@ int fp_ctx::write_manifest() {
   char buf[512];
   snprintf(buf, sizeof(buf),
            "  \"alignment\": %u,\n  \"image_bytes\": %llu,\n  \"header_bytes\": %llu,\n"
-           "  \"dp_size\": %d,\n  \"layout_digest\": %llu,\n  \"n_roots\": %zu,\n"
+           "  \"dp_size\": %d,\n  \"writer_stride\": %u,\n  \"layout_digest\": %llu,\n  \"n_roots\": %zu,\n"
            "  \"shards\": [\n",
            plan.align, (unsigned long long)plan.image_bytes,
-           (unsigned long long)plan.header_bytes, k, (unsigned long long)plan.digest,
+           (unsigned long long)plan.header_bytes, k, plan.writer_stride,
+           (unsigned long long)plan.digest,
            roots.empty() ? (size_t)1 : roots.size());
   j += buf;
   for (int r = 0; r < k; ++r) {
@@ -419,9 +420,10 @@ int fp_ctx::write_manifest() {
 // plan setup shared by begin and load
 // ---------------------------------------------------------------------------
 static uint64_t sig_hash(const std::vector<TensorRef>& rep, const std::vector<TensorRef>& loc,
-                         int rank, int k, uint32_t align, bool ptrs) {
+                         int rank, int k, uint32_t align, uint32_t writer_stride, bool ptrs) {
   uint64_t h = fnv1a64((const uint8_t*)&rank, 4);
   h = fnv1a64((const uint8_t*)&k, 4, h);
+  h = fnv1a64((const uint8_t*)&writer_stride, 4, h);
   h = fnv1a64((const uint8_t*)&align, 4, h);
   for (const auto* v : {&rep, &loc})
     for (const TensorRef& t : *v) {
@@ -453,8 +455,8 @@ int fp::ensure_plan(fp_ctx* c, const fp_tensor* t, size_t n, int rank, int k) {
     if (any) return FP_ENODEV;
   }
   const uint32_t A = c->cfg.alignment;
-  const uint64_t sm = sig_hash(rep, loc, rank, k, A, false);
-  const uint64_t sp = sig_hash(rep, loc, rank, k, A, true) ^ (host ? 1 : 0);
+  const uint64_t sm = sig_hash(rep, loc, rank, k, A, c->cfg.writer_stride, false);
+  const uint64_t sp = sig_hash(rep, loc, rank, k, A, c->cfg.writer_stride, true) ^ (host ? 1 : 0);
   const bool new_meta = !c->planned || sm != c->sig_meta;
   if (new_meta) {
     LocalFacts mine;
@@ -471,7 +473,7 @@ int fp::ensure_plan(fp_ctx* c, const fp_tensor* t, size_t n, int rank, int k) {
       all[0] = mine;
     }
     Plan p;
-    r = plan_build(rep, loc, A, rank, k, all, &p);
+    r = plan_build(rep, loc, A, rank, k, c->cfg.writer_stride, all, &p);
     if (r) {
       c->planned = false;
       return r;
@@ -479,10 +481,9 @@ int fp::ensure_plan(fp_ctx* c, const fp_tensor* t, size_t n, int rank, int k) {
     // every rank's extents (for the manifest): plan each rank's partition
     c->all_extents.assign(k, {});
     {
-      const uint64_t Q = p.rep_bytes / A, q = Q / k, rem = Q % k;
       for (int w = 0; w < k; ++w) {
-        const uint64_t first = (uint64_t)w * q + std::min<uint64_t>(w, rem);
-        const uint64_t npg = q + ((uint64_t)w < rem ? 1 : 0);
+        uint64_t first = 0, npg = 0;
+        rep_partition(p.rep_bytes / A, k, p.writer_stride, w, &first, &npg);
         uint64_t fo = 0;
         if (npg) {
           c->all_extents[w].push_back({first * A, 0, npg * A});
@@ -586,6 +587,7 @@ int fp_config_default(fp_config* cfg) {
   cfg->alignment = (uint32_t)env_u64("FP_ALIGN", 4096);
   cfg->pack_ctas = (uint32_t)env_u64("FP_PACK_CTAS", 0);
   cfg->pack_bytes = env_u64("FP_PACK_BYTES", 256ull << 20);
+  cfg->writer_stride = (uint32_t)env_u64("FP_WRITER_STRIDE", 1);
   const char* pr = getenv("FP_PACK_PRIO");
   if (pr && !strcmp(pr, "low")) cfg->flags |= FP_CFG_PRIO_LOW;
   const char* e = getenv("FP_IO_ENGINE");

@@ -76,7 +76,7 @@ class fp_config(C.Structure):
     _fields_ = [("ring_slots", C.c_uint32), ("io_depth", C.c_uint32), ("slot_bytes", C.c_uint64),
                 ("sqe_bytes", C.c_uint32), ("alignment", C.c_uint32), ("io_engine", C.c_uint32),
                 ("pack_impl", C.c_uint32), ("pack_ctas", C.c_uint32), ("flags", C.c_uint32),
-                ("dirs", C.c_char_p), ("pack_bytes", C.c_uint64)]
+                ("dirs", C.c_char_p), ("writer_stride", C.c_uint32), ("pack_bytes", C.c_uint64)]
 
 
 class fp_stats(C.Structure):

@@ -303,3 +303,40 @@ def test_load_parallel_errors_surface_on_every_rank(tmp_path):
     finally:
         for c in cks:
             c.close()
+
+
+@pytest.mark.parametrize("cfg,k,stride", [("gpt3_odd", 4, 2), ("moe_small", 4, 4),
+                                          ("c1_tiny", 3, 2), ("zero_small", 2, 2)])
+def test_writer_subset_matches_oracle_and_loads(tmp_path, cfg, k, stride):
+    """The paper's writer subsets: with writer_stride s only ranks
+    0, s, 2s, ... write replicated bytes; files == oracle's shards; both loads
+    read the partition back from the manifest."""
+    states = [_state(cfg, r, k) for r in range(k)]
+    lay = oracle_layout(states, k)
+    comms = ThreadComm.group(k)
+    cks = [fp.Checkpointer(None, comm=comms[r], slot_bytes=1 << 20, writer_stride=stride)
+           for r in range(k)]
+    try:
+        run_threads([lambda r=r: cks[r].save(entries(states[r]), str(tmp_path))
+                     for r in range(k)])
+        man = json.load(open(tmp_path / "manifest.json"))
+        assert man["writer_stride"] == stride
+        ext = fpck.shard_extents(lay, stride)
+        for r in range(k):
+            assert man["shards"][r]["extents"] == [list(e) for e in ext[r]]
+            assert file_sha(tmp_path / fpck.shard_name(r, k)) == fpck.shard_sha256(lay, r, stride)
+            assert man["shards"][r]["crc32"] == fpck.shard_crc32(lay, r, stride)
+        for loader in ("load", "load_parallel"):
+            # loaders configured with the default stride: the manifest decides
+            lcks = [fp.Checkpointer(None, comm=comms[r], slot_bytes=1 << 20) for r in range(k)]
+            dst = [[(s, torch.zeros_like(t)) for s, t in states[r]] for r in range(k)]
+            run_threads([lambda r=r: getattr(lcks[r], loader)(entries(dst[r]), str(tmp_path))
+                         for r in range(k)])
+            for r in range(k):
+                lcks[r].close()
+                for (_, a), (_, b) in zip(states[r], dst[r]):
+                    assert torch.equal(a.reshape(-1).view(torch.uint8),
+                                       b.reshape(-1).view(torch.uint8)), loader
+    finally:
+        for c in cks:
+            c.close()

@@ -305,3 +305,34 @@ def test_crc32_library_pinned_to_check_value_and_oracle_shard_crc():
     lay = fpck.Layout([fpck.OTensor(s.name, s.dtype, s.section, s.owner, s.shape, tbytes(t))
                        for s, t in st])
     assert fpck.shard_crc32(lay, 0) == zlib.crc32(lay.image())
+
+
+@pytest.mark.parametrize("stride", [1, 2, 3, 4, 8])
+def test_writer_subset_extents_brute_force(stride):
+    """Writer subsets: only ranks 0, s, 2s, ... receive replicated
+    pages; together they tile the replicated region once, page-balanced; the
+    shards still reassemble into the image."""
+    rng = random.Random(stride)
+    for k in range(1, 9):
+        rep, local = _rand_state(rng, rng.randint(0, 6), rng.randint(0, 4), k)
+        lay = fpck.Layout(rep, local, k=k)
+        ext = fpck.shard_extents(lay, stride)
+        A = lay.align
+        writers = [r for r in range(k) if r % stride == 0]
+        rep_pages = []
+        for r in range(k):
+            rp = [(io, n) for io, _, n in ext[r] if io < lay.rep_bytes]
+            if r not in writers:
+                assert rp == []
+            for io, n in rp:
+                rep_pages.extend(range(io // A, (io + n) // A))
+        assert rep_pages == list(range(lay.rep_bytes // A))
+        sizes = [sum(n for io, _, n in ext[r] if io < lay.rep_bytes) for r in writers]
+        assert max(sizes) - min(sizes) <= A
+        # bytes of all shards placed at their image offsets give the image
+        img = bytearray(lay.image_bytes)
+        for r in range(k):
+            data = fpck.shard_bytes(lay, r, stride)
+            for io, fo, n in ext[r]:
+                img[io:io + n] = data[fo:fo + n]
+        assert bytes(img) == lay.image()
