@@ -358,7 +358,7 @@ def our_arm(a):
 
     cfg = dict(pack=a.pack, slot_bytes=a.slot_mib << 20, ring_slots=a.ring_slots,
                io_depth=a.qd, sqe_bytes=a.sqe_kib << 10, pack_bytes=a.pack_mib << 20,
-               prio=a.prio)
+               prio=a.prio, writer_stride=a.writer_stride)
     peaks, peak_src = measured_peaks()
 
     # ---- rooflines measured in the same run --------------------------------
@@ -513,6 +513,7 @@ def our_arm(a):
                        "shard_bytes_rank0": shard_bytes, "profile": "adam16",
                        "pack": a.pack, "ring": f"{a.ring_slots}x{a.slot_mib}MiB",
                        "pack_launch_mib": a.pack_mib, "pack_stream_prio": a.prio,
+                       "writer_stride": a.writer_stride,
                        "sqe_kib": a.sqe_kib, "qd": a.qd, "engine": stats[-1]["engine"],
                        "l2": "inputs (21 GB of state) larger than L2; no flush needed",
                        "dir": root},
@@ -555,6 +556,8 @@ def main():
     ap.add_argument("--pack", default="v4", choices=["v4", "bulk", "host", "ce"])
     ap.add_argument("--pack-mib", type=int, default=256)
     ap.add_argument("--prio", default="high", choices=["high", "low"])
+    ap.add_argument("--writer-stride", type=int, default=1,
+                    help="writer subset (P:495-499): ranks r %% s == 0 write replicated bytes")
     ap.add_argument("--slot-mib", type=int, default=64)
     ap.add_argument("--ring-slots", type=int, default=4)
     ap.add_argument("--qd", type=int, default=64)
