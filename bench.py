@@ -369,13 +369,14 @@ def our_arm(a):
     shard_bytes = sum(e[2] for e in shard_bytes)
     shutil.rmtree(os.path.join(root, "plan"), ignore_errors=True) if rank == 0 else None
     barrier()
-    nv_bytes = min(shard_bytes, int(a.nvme_bytes))
+    # every rank writes the same amount (a writer subset still has N ranks
+    # on the box): the image's per-rank share, capped
+    img_total = int(allreduce_sum(shard_bytes, dev))
+    nv_bytes = min(-(-img_total // world), int(a.nvme_bytes))
     barrier()
-    t0 = time.perf_counter()
-    fp.io_bench(root, nv_bytes, tag=rank, io_depth=a.qd, sqe_bytes=a.sqe_kib << 10,
-                ring_slots=a.ring_slots, slot_bytes=a.slot_mib << 20)
-    dt = allreduce_max(time.perf_counter() - t0, dev)
-    nvme_gbs = nv_bytes * world / dt / 1e9
+    g = fp.io_bench(root, nv_bytes, tag=rank, io_depth=a.qd, sqe_bytes=a.sqe_kib << 10,
+                    ring_slots=a.ring_slots, slot_bytes=a.slot_mib << 20)
+    nvme_gbs = allreduce_sum(g, dev)          # concurrent writers: aggregate
     d2h_gbs = allreduce_sum(d2h_roofline(dev), dev)
 
     # ---- the checkpoint steps ----------------------------------------------
