@@ -200,6 +200,16 @@ int fp_ckpt_init(const fp_config *cfg, int cuda_device, const fp_comm *comm,
 int fp_ckpt_begin(fp_ctx *ctx, const fp_tensor *t, size_t n, const char *path,
                   int dp_rank, int dp_size, void *producer_stream);
 
+/* Stream-ordered fence: enqueue on `stream` (cudaStream_t)
+ * a wait that holds every later operation of that stream until this rank's
+ * shard of the outstanding checkpoint is durable (fdatasync'd) — or has
+ * failed. Returns at once: the host thread keeps enqueueing the optimizer
+ * while the GPU, not the host, waits (the paper's main thread blocks).
+ * fp_ckpt_wait is still required afterwards for the cross-rank barrier,
+ * error status and manifest commit. 0 if nothing is outstanding; -ENOSYS if
+ * the driver refuses stream memory operations; FP_ECUDA.                      */
+int fp_ckpt_fence(fp_ctx *ctx, void *stream);
+
 /* Block until the outstanding checkpoint is durable everywhere: this rank's
  * shard is fdatasync'd, the status all-reduce (barrier) has completed, and
  * rank 0 has committed manifest.json (tmp + rename + dir fsync). Collective

@@ -69,6 +69,12 @@ struct fp_ctx {
   volatile uint32_t* h_gate = nullptr;
   uint64_t d_gate = 0;
   uint32_t gate_seq = 0;
+  // stream-ordered fence (fp_ckpt_fence): the helper stores the id of the
+  // checkpoint whose shard became durable (or failed) into a mapped pinned
+  // word that a cuStreamWaitValue32 on the caller's stream waits for
+  volatile uint32_t* h_done = nullptr;
+  uint64_t d_done = 0;
+  uint32_t ckpt_seq = 0;
   // CRC-32 of the shard
   uint32_t *d_crc_tab8 = nullptr, *d_lane_k = nullptr, *d_x4k = nullptr;
   uint32_t *d_page_crc = nullptr, *d_chunk_crc = nullptr, *h_crc = nullptr;

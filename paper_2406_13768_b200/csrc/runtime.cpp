@@ -350,6 +350,9 @@ void fp_ctx::helper() {
     state = RUNNING;
     g.unlock();
     int r = save_shard();
+    // release any stream fenced on this checkpoint — on failure too (the
+    // error reaches the caller through fp_ckpt_wait), never leave it waiting
+    if (h_done) __atomic_store_n(h_done, ckpt_seq, __ATOMIC_RELEASE);
     g.lock();
     result = r;
     state = DONE;
@@ -729,12 +732,14 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
                                            &q) == cudaSuccess &&
           q == cudaDriverEntryPointSuccess && fn && !getenv("FP_NO_GATE")) {
         void* hg = nullptr;
-        if (cudaHostAlloc(&hg, 64, cudaHostAllocMapped | cudaHostAllocPortable) == cudaSuccess) {
-          memset(hg, 0, 64);
+        if (cudaHostAlloc(&hg, 4096, cudaHostAllocMapped | cudaHostAllocPortable) == cudaSuccess) {
+          memset(hg, 0, 4096);
           void* dg = nullptr;
           if (cudaHostGetDevicePointer(&dg, hg, 0) == cudaSuccess) {
             c->h_gate = (volatile uint32_t*)hg;
             c->d_gate = (uint64_t)(uintptr_t)dg;
+            c->h_done = (volatile uint32_t*)hg + 16;  // separate 64-B line of the page
+            c->d_done = c->d_gate + 64;
             c->wait_value = (WaitValue32Fn)fn;
           } else {
             cudaFreeHost(hg);
@@ -796,8 +801,18 @@ int fp_ckpt_begin(fp_ctx* c, const fp_tensor* t, size_t n, const char* path, int
   if (!c->host) CK(cudaEventRecord(c->ev_producer, (cudaStream_t)producer_stream));
   std::lock_guard<std::mutex> g(c->mu);
   c->t_begin = t0;
+  ++c->ckpt_seq;
   c->state = fp_ctx::PENDING;
   c->cv.notify_all();
+  return 0;
+}
+
+int fp_ckpt_fence(fp_ctx* c, void* stream) {
+  if (!c) return -EINVAL;
+  std::lock_guard<std::mutex> g(c->mu);
+  if (c->state == fp_ctx::IDLE) return 0;
+  if (!c->wait_value || !c->h_done) return -ENOSYS;
+  if (c->wait_value((cudaStream_t)stream, c->d_done, c->ckpt_seq, 0 /*GEQ*/)) return FP_ECUDA;
   return 0;
 }
 

@@ -91,7 +91,7 @@ class fp_stats(C.Structure):
                 ("err_offset", C.c_int64), ("shard_crc32", C.c_uint32), ("crc_valid", C.c_uint32)]
 
 
-EXPORTS = ("fp_config_default", "fp_ckpt_init", "fp_ckpt_begin", "fp_ckpt_wait",
+EXPORTS = ("fp_config_default", "fp_ckpt_init", "fp_ckpt_begin", "fp_ckpt_fence", "fp_ckpt_wait",
            "fp_ckpt_load", "fp_ckpt_load_parallel", "fp_ckpt_plan_info", "fp_ckpt_destroy", "fp_strerror",
            "fp_io_bench")
 
@@ -113,6 +113,7 @@ def lib():
     L.fp_ckpt_begin.argtypes = [C.c_void_p, C.POINTER(fp_tensor), C.c_size_t, C.c_char_p,
                                 C.c_int, C.c_int, C.c_void_p]
     L.fp_ckpt_wait.argtypes = [C.c_void_p, C.POINTER(fp_stats)]
+    L.fp_ckpt_fence.argtypes = [C.c_void_p, C.c_void_p]
     L.fp_ckpt_load.argtypes = [C.c_void_p, C.POINTER(fp_tensor), C.c_size_t, C.c_char_p,
                                C.c_int, C.c_int, C.c_void_p]
     L.fp_ckpt_load_parallel.argtypes = [C.c_void_p, C.POINTER(fp_tensor), C.c_size_t,
@@ -355,6 +356,11 @@ class Checkpointer:
         self._keep = (arr, keep)   # borrowed until wait() returns
         _check(lib().fp_ckpt_begin(self.h, arr, n, os.fsencode(path), self.rank, self.world,
                                    _stream_handle(stream, self.device)), "fp_ckpt_begin")
+
+    def fence(self, stream=None):
+        """Hold `stream` (default: current) on the GPU until this rank's shard
+        is durable; returns immediately. Call wait() later for the commit."""
+        _check(lib().fp_ckpt_fence(self.h, _stream_handle(stream, self.device)), "fp_ckpt_fence")
 
     def wait(self):
         st = fp_stats()

@@ -258,3 +258,27 @@ def test_load_parallel_device_detects_payload_corruption(tmp_path):
     finally:
         for c in cks:
             c.close()
+
+
+def test_stream_ordered_fence_holds_the_optimizer(tmp_path):
+    """fp_ckpt_fence (a9): the 'optimizer' enqueued on the fenced stream right
+    after begin() must not run before this rank's shard is durable, yet
+    fence() itself returns without blocking the host."""
+    import time
+    st = _state("gpt3_small")
+    lay = oracle_layout([st], 1)              # bytes BEFORE the update
+    s = torch.cuda.Stream(DEV)
+    with fp.Checkpointer(DEV, slot_bytes=64 << 10, ring_slots=2) as ck:
+        ck.begin(entries(st), str(tmp_path), stream=s)
+        t0 = time.perf_counter()
+        ck.fence(stream=s)
+        dt = time.perf_counter() - t0
+        with torch.cuda.stream(s):            # the next optimizer step
+            for _, t in st:
+                if t.is_floating_point():
+                    t.fill_(-7.0)
+        ck.wait()
+        torch.cuda.synchronize()
+    assert dt < 0.05, f"fence blocked the host for {dt:.3f} s"
+    _check_rank_files(str(tmp_path), lay, 1)   # the checkpoint is the pre-update state
+    assert all(bool((t == -7.0).all()) for _, t in st if t.is_floating_point())
