@@ -591,6 +591,7 @@ int fp_config_default(fp_config* cfg) {
   cfg->pack_ctas = (uint32_t)env_u64("FP_PACK_CTAS", 0);
   cfg->pack_bytes = env_u64("FP_PACK_BYTES", 256ull << 20);
   cfg->writer_stride = (uint32_t)env_u64("FP_WRITER_STRIDE", 1);
+  if (getenv("FP_NO_CRC")) cfg->flags |= FP_CFG_NO_CRC;
   const char* pr = getenv("FP_PACK_PRIO");
   if (pr && !strcmp(pr, "low")) cfg->flags |= FP_CFG_PRIO_LOW;
   const char* e = getenv("FP_IO_ENGINE");
