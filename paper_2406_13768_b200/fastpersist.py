@@ -68,6 +68,13 @@ def dev_bytes(ptr, nbytes, device):
     return torch.as_tensor(_DevBuf(ptr, nbytes), device=device)
 
 
+def torch_stream(handle, device):
+    """torch view of a cudaStream_t handle (None/0 = the legacy default stream)."""
+    if not handle:
+        return torch.cuda.default_stream(device)
+    return torch.cuda.ExternalStream(int(handle), device=device)
+
+
 def host_bytes(ptr, nbytes):
     return torch.frombuffer((C.c_uint8 * int(nbytes)).from_address(int(ptr)), dtype=torch.uint8)
 
@@ -244,7 +251,7 @@ class _Comm:
             if on_device:
                 s = dev_bytes(send, n, self.device)
                 r = dev_bytes(recv, n * self.world, self.device)
-                with torch.cuda.stream(torch.cuda.ExternalStream(stream, device=self.device)):
+                with torch.cuda.stream(torch_stream(stream, self.device)):
                     if self.dev.type == "cuda":
                         self.dist.all_gather_into_tensor(r, s, group=self.group)
                     else:                    # non-NCCL group: stage through host memory

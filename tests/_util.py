@@ -95,8 +95,8 @@ class ThreadComm:
         ordered after each rank's stream work)."""
         import ctypes
         if on_device:
-            from paper_2406_13768_b200.fastpersist import dev_bytes
-            st = torch.cuda.ExternalStream(stream)
+            from paper_2406_13768_b200.fastpersist import dev_bytes, torch_stream
+            st = torch_stream(stream, torch.device("cuda", 0))
             st.synchronize()                       # our send is complete
         self.sh.slots[self.rank] = send
         self.sh.bar.wait()
