@@ -414,7 +414,7 @@ def our_arm(a):
     pack_gbs = 2 * pk_bytes / (pk_ms / 1e3) / 1e9 if pk_ms > 0 else None
     d2h_ms = sum(s["d2h_ms"] for s in stats)
     pack_gbs = pack_gbs or 0.0                       # this rank's own GPU (rank 0 reports)
-    launches_all = allreduce_sum(pk_launches, dev)
+    launches_all = allreduce_sum(sum(s["kernel_launches"] for s in stats), dev)
 
     # ---- e2e: public API with the state sourced from pinned HOST memory ------
     e2e = None

@@ -168,6 +168,7 @@ typedef struct fp_stats {
                               file; computed on the GPU from the packed slab
                               (host tensors: on the CPU); also in the manifest  */
   uint32_t crc_valid;      /* 1 if shard_crc32 was computed                       */
+  uint64_t kernel_launches;/* all library kernels launched (pack, CRC, gate)      */
 } fp_stats;
 
 typedef struct fp_ctx fp_ctx;
@@ -201,13 +202,14 @@ int fp_ckpt_begin(fp_ctx *ctx, const fp_tensor *t, size_t n, const char *path,
                   int dp_rank, int dp_size, void *producer_stream);
 
 /* Stream-ordered fence: enqueue on `stream` (cudaStream_t)
- * a wait that holds every later operation of that stream until this rank's
- * shard of the outstanding checkpoint is durable (fdatasync'd) — or has
- * failed. Returns at once: the host thread keeps enqueueing the optimizer
- * while the GPU, not the host, waits (the paper's main thread blocks).
- * fp_ckpt_wait is still required afterwards for the cross-rank barrier,
- * error status and manifest commit. 0 if nothing is outstanding; -ENOSYS if
- * the driver refuses stream memory operations; FP_ECUDA.                      */
+ * a wait (a one-warp kernel polling a mapped pinned word) that holds every
+ * later operation of that stream until this rank's shard of the outstanding
+ * checkpoint is durable (fdatasync'd) — or has failed. Returns at once: the
+ * host thread keeps enqueueing the optimizer while the GPU, not the host,
+ * waits (the paper's main thread blocks). fp_ckpt_wait is still
+ * required afterwards for the cross-rank barrier, error status and manifest
+ * commit; it returns -ETIMEDOUT if a fence gave up after one hour. 0 if
+ * nothing is outstanding; -ENOSYS for a host-only context; FP_ECUDA.          */
 int fp_ckpt_fence(fp_ctx *ctx, void *stream);
 
 /* Block until the outstanding checkpoint is durable everywhere: this rank's

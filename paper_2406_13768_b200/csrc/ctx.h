@@ -15,9 +15,6 @@
 
 namespace fp {
 
-// cuStreamWaitValue32 (driver API, fetched at run time so the library does
-// not link libcuda): the stream waits until *addr >= value.
-typedef int (*WaitValue32Fn)(cudaStream_t, uint64_t, uint32_t, unsigned int);
 
 double now_s();
 uint64_t env_u64(const char* k, uint64_t dflt);
@@ -42,7 +39,6 @@ using fp::IoEngine;
 using fp::Item;
 using fp::Plan;
 using fp::TensorRef;
-using fp::WaitValue32Fn;
 
 struct fp_ctx {
   fp_config cfg;
@@ -61,19 +57,20 @@ struct fp_ctx {
   cudaEvent_t ev_producer = nullptr;
   std::vector<cudaEvent_t> ev_p0, ev_p1, ev_d0, ev_d2h;
   std::vector<uint8_t> has_pack;  // per ring slot: its chunk led a pack launch
-  // launch gate: the pack group's [event, kernel, event] are queued behind a
-  // cuStreamWaitValue32 on a mapped pinned flag that the host releases after
-  // the whole group is enqueued, so the events time the kernel, not the host
-  // API latency of an idle stream
-  WaitValue32Fn wait_value = nullptr;
-  volatile uint32_t* h_gate = nullptr;
-  uint64_t d_gate = 0;
+  // Host -> GPU signals live in one mapped pinned page, read on the GPU by
+  // fp_wait_flag (a 1-warp kernel spinning with ld.acquire.sys; stream
+  // memory operations, cuStreamWaitValue32, are disabled on some platforms —
+  // the gpurun B200s report CAN_USE_STREAM_MEM_OPS = 0 and the wait never
+  // releases).
+  //  gate: the pack group's [event, kernel, event, crc] are queued behind a
+  //  wait on `gate` that the host releases after the whole group is enqueued,
+  //  so the events time the kernel, not the host API latency of an idle stream
+  //  done: id of the checkpoint whose shard became durable (or failed), waited
+  //  for on the caller's stream by fp_ckpt_fence
+  volatile uint32_t* h_sig = nullptr;  // [0] gate, [16] done, [32] fence timeout
+  uint32_t* d_sig = nullptr;
+  bool gate_on = false;
   uint32_t gate_seq = 0;
-  // stream-ordered fence (fp_ckpt_fence): the helper stores the id of the
-  // checkpoint whose shard became durable (or failed) into a mapped pinned
-  // word that a cuStreamWaitValue32 on the caller's stream waits for
-  volatile uint32_t* h_done = nullptr;
-  uint64_t d_done = 0;
   uint32_t ckpt_seq = 0;
   // CRC-32 of the shard
   uint32_t *d_crc_tab8 = nullptr, *d_lane_k = nullptr, *d_x4k = nullptr;

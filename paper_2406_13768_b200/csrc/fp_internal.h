@@ -146,6 +146,10 @@ int pack_launch(int impl, const Item* d_items, uint32_t n_items, uint8_t* d_slab
 int unpack_launch(const Item* d_items, uint32_t n_items, const uint8_t* d_slab, int ctas,
                   void* stream);
 int pack_default_ctas(int impl, int device);
+// one-warp kernel on `stream` that waits until the mapped word *d_flag
+// reaches `value` (or max_ns passes; then *d_timed_out = 1 if non-null)
+int flag_wait_launch(const uint32_t* d_flag, uint32_t value, uint64_t max_ns,
+                     uint32_t* d_timed_out, void* stream);
 // raw CRC-32 of d_buf[0, bytes) per chunk_bytes chunk -> d_chunk_crc[]
 // (bytes, chunk_bytes: multiples of 4096; d_page_crc: bytes/4096 entries)
 int crc_launch(const uint8_t* d_buf, uint64_t bytes, uint64_t chunk_bytes, const uint32_t* d_tab8,

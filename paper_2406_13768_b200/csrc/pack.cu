@@ -320,6 +320,29 @@ __global__ void __launch_bounds__(256) fp_crc_chunks(const uint32_t* __restrict_
   }
 }
 
+// ---------------------------------------------------------------------------
+// host -> GPU signal: one warp spins (acquire loads at system scope, so the
+// host's store to the mapped pinned word is observed) until the word reaches
+// `value` (cyclic >=); gives up after max_ns and then sets *timed_out.
+// ---------------------------------------------------------------------------
+__global__ void fp_wait_flag(const uint32_t* __restrict__ flag, uint32_t value, uint64_t max_ns,
+                             uint32_t* __restrict__ timed_out) {
+  if (threadIdx.x) return;
+  uint64_t t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint32_t x;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(x) : "l"(flag) : "memory");
+    if ((int32_t)(x - value) >= 0) return;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > max_ns) {
+      if (timed_out) asm volatile("st.release.sys.global.u32 [%0], 1;" ::"l"(timed_out) : "memory");
+      return;
+    }
+    __nanosleep(256);
+  }
+}
+
 int sm_count(int device) {
   int d = device;
   if (d < 0 && cudaGetDevice(&d) != cudaSuccess) return 148;
@@ -353,6 +376,12 @@ int pack_launch(int impl, const Item* d_items, uint32_t n_items, uint8_t* d_slab
   } else {
     fp_pack_v4<<<grid, kV4Threads, 0, st>>>(d_items, n_items, d_slab);
   }
+  return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
+}
+
+int flag_wait_launch(const uint32_t* d_flag, uint32_t value, uint64_t max_ns,
+                     uint32_t* d_timed_out, void* stream) {
+  fp_wait_flag<<<1, 32, 0, (cudaStream_t)stream>>>(d_flag, value, max_ns, d_timed_out);
   return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
 }
 

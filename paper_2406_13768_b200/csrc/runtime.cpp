@@ -190,6 +190,7 @@ int fp_ctx::save_shard() {
     has_pack[s] = 0;
     if (cfg.pack_impl == FP_PACK_HOST) {
       // fused pack -> mapped pinned slot: the kernel's stores cross PCIe
+      ++st.kernel_launches;
       if (c == 0) CK(cudaStreamWaitEvent(stream, ev_producer, 0));
       CK(cudaEventRecord(ev_p0[s], stream));
       int r = pack_launch(FP_PACK_V4, d_items + item_lo[c], item_lo[c + 1] - item_lo[c],
@@ -224,12 +225,12 @@ int fp_ctx::save_shard() {
       const uint64_t c1 = std::min<uint64_t>(g0 + G, C);
       const uint64_t gbytes = std::min<uint64_t>(c1 * S, plan.shard_bytes) - c * S;
       if (c == 0) CK(cudaStreamWaitEvent(stream, ev_producer, 0));
-      bool gated = wait_value != nullptr;
-      if (gated && wait_value(stream, d_gate, gate_seq + 1, 0 /*GEQ*/)) {
-        wait_value = nullptr;  // stream memory ops refused: run ungated from now on
-        gated = false;
+      bool gated = gate_on;
+      if (gated && flag_wait_launch(d_sig, gate_seq + 1, 2000000000ull, nullptr, stream)) {
+        gate_on = gated = false;  // could not launch the gate: run ungated from now on
         cudaGetLastError();
       }
+      st.kernel_launches += (gated ? 1 : 0) + 1 + (gpu_crc ? 2 : 0);
       // the gate is opened on every path out of this block: a stream left
       // waiting on it would never drain
       int r = cudaEventRecord(ev_p0[s], stream) == cudaSuccess ? 0 : FP_ECUDA;
@@ -240,7 +241,7 @@ int fp_ctx::save_shard() {
       if (!r && gpu_crc)
         r = crc_launch(d_slab, round_up(gbytes, 4096), S, d_crc_tab8, d_lane_k, d_x4k,
                        d_page_crc, d_chunk_crc, stream);
-      if (gated) __atomic_store_n(h_gate, ++gate_seq, __ATOMIC_RELEASE);  // open the gate
+      if (gated) __atomic_store_n(&h_sig[0], ++gate_seq, __ATOMIC_RELEASE);  // open the gate
       if (r) return r;
       has_pack[s] = 1;
       ++st.pack_launches;
@@ -352,7 +353,7 @@ void fp_ctx::helper() {
     int r = save_shard();
     // release any stream fenced on this checkpoint — on failure too (the
     // error reaches the caller through fp_ckpt_wait), never leave it waiting
-    if (h_done) __atomic_store_n(h_done, ckpt_seq, __ATOMIC_RELEASE);
+    if (h_sig) __atomic_store_n(&h_sig[16], ckpt_seq, __ATOMIC_RELEASE);
     g.lock();
     result = r;
     state = DONE;
@@ -725,29 +726,17 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
           cudaEventCreateWithFlags(&c->ev_d2h[s], cudaEventBlockingSync) != cudaSuccess)
         return fail(FP_ECUDA);
     }
-    // launch gate (optional: without it the pack events also time host latency)
+    // host -> GPU signal page (launch gate, fence)
     {
-      void* fn = nullptr;
-      cudaDriverEntryPointQueryResult q;
-      if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &fn, 11070, cudaEnableDefault,
-                                           &q) == cudaSuccess &&
-          q == cudaDriverEntryPointSuccess && fn && !getenv("FP_NO_GATE")) {
-        void* hg = nullptr;
-        if (cudaHostAlloc(&hg, 4096, cudaHostAllocMapped | cudaHostAllocPortable) == cudaSuccess) {
-          memset(hg, 0, 4096);
-          void* dg = nullptr;
-          if (cudaHostGetDevicePointer(&dg, hg, 0) == cudaSuccess) {
-            c->h_gate = (volatile uint32_t*)hg;
-            c->d_gate = (uint64_t)(uintptr_t)dg;
-            c->h_done = (volatile uint32_t*)hg + 16;  // separate 64-B line of the page
-            c->d_done = c->d_gate + 64;
-            c->wait_value = (WaitValue32Fn)fn;
-          } else {
-            cudaFreeHost(hg);
-          }
-        }
-      }
-      cudaGetLastError();
+      void* hg = nullptr;
+      void* dg = nullptr;
+      if (cudaHostAlloc(&hg, 4096, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess)
+        return fail(-ENOMEM);
+      memset(hg, 0, 4096);
+      c->h_sig = (volatile uint32_t*)hg;
+      if (cudaHostGetDevicePointer(&dg, hg, 0) != cudaSuccess) return fail(FP_ECUDA);
+      c->d_sig = (uint32_t*)dg;
+      c->gate_on = !getenv("FP_NO_GATE");
     }
     // CRC tables + scratch: slicing tables, lane multipliers x^(8*128*(31-l)),
     // x^(8*4096*2^i), page CRCs of one pack group, chunk CRCs
@@ -812,9 +801,10 @@ int fp_ckpt_fence(fp_ctx* c, void* stream) {
   if (!c) return -EINVAL;
   std::lock_guard<std::mutex> g(c->mu);
   if (c->state == fp_ctx::IDLE) return 0;
-  if (!c->wait_value || !c->h_done) return -ENOSYS;
-  if (c->wait_value((cudaStream_t)stream, c->d_done, c->ckpt_seq, 0 /*GEQ*/)) return FP_ECUDA;
-  return 0;
+  if (!c->d_sig) return -ENOSYS;  // host-only context
+  // bounded at one hour; a timeout sets sig[32], reported by fp_ckpt_wait
+  return flag_wait_launch(c->d_sig + 16, c->ckpt_seq, 3600ull * 1000000000ull, c->d_sig + 32,
+                          stream);
 }
 
 int fp_ckpt_wait(fp_ctx* c, fp_stats* out) {
@@ -825,6 +815,8 @@ int fp_ckpt_wait(fp_ctx* c, fp_stats* out) {
     c->cv.wait(g, [&] { return c->state == fp_ctx::DONE; });
   }
   int32_t status = c->result;
+  if (c->h_sig && __atomic_exchange_n(&c->h_sig[32], 0u, __ATOMIC_ACQ_REL))
+    status = status ? status : -ETIMEDOUT;  // a fence gave up waiting
   if (c->k > 1) {
     const double tb = now_s();
     int32_t s = status;
@@ -897,7 +889,7 @@ void fp_ckpt_destroy(fp_ctx* c) {
     if (c->d_page_crc) cudaFree(c->d_page_crc);
     if (c->d_chunk_crc) cudaFree(c->d_chunk_crc);
     if (c->h_crc) cudaFreeHost(c->h_crc);
-    if (c->h_gate) cudaFreeHost((void*)c->h_gate);
+    if (c->h_sig) cudaFreeHost((void*)c->h_sig);
     if (c->d_hdr) cudaFree(c->d_hdr);
     if (c->ring_cuda_registered) cudaHostUnregister(c->ring);
   }

@@ -8,7 +8,6 @@ group uses on the GPU box. Host-resident state (FP_TENSOR_HOST) stands in for
 device tensors, so everything but the pack kernel runs here.
 """
 import os
-import socket
 
 import pytest
 import torch
@@ -21,21 +20,13 @@ from workloads import config_specs, make_state
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
-
-
-def _worker(rank, world, port, cfg, out_dir, mode, q):
+def _worker(rank, world, rdzv, cfg, out_dir, mode, q):
     import sys
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
     import paper_2406_13768_b200 as fp
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # file rendezvous: no TCP port to race for between test processes
+    dist.init_process_group("gloo", init_method=f"file://{rdzv}", rank=rank, world_size=world)
     try:
         st = make_state(config_specs(cfg, rank, world), "cpu")
         with fp.Checkpointer(None, slot_bytes=1 << 20) as ck:
@@ -61,8 +52,8 @@ def _worker(rank, world, port, cfg, out_dir, mode, q):
 def _run(cfg, world, out_dir, mode="ok"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = _free_port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, cfg, out_dir, mode, q))
+    rdzv = os.path.join(out_dir, ".rdzv")
+    ps = [ctx.Process(target=_worker, args=(r, world, rdzv, cfg, out_dir, mode, q))
           for r in range(world)]
     for p in ps:
         p.start()
