@@ -313,8 +313,14 @@ def test_writer_subset_extents_brute_force(stride):
     pages; together they tile the replicated region once, page-balanced; the
     shards still reassemble into the image."""
     rng = random.Random(stride)
-    for k in range(1, 9):
-        rep, local = _rand_state(rng, rng.randint(0, 6), rng.randint(0, 4), k)
+    nrng = np.random.default_rng(stride)
+    for k in list(range(1, 9)) * 4:
+        rep = [fpck.OTensor(f"r{i}", "u8", "other", -1, (n,), nrng.bytes(n))
+               for i, n in enumerate(rng.randint(0, 20000) for _ in range(rng.randint(0, 6)))]
+        local = [[] for _ in range(k)]
+        for j in range(rng.randint(0, 4)):
+            r, n = rng.randrange(k), rng.randint(0, 9000)
+            local[r].append(fpck.OTensor(f"l{j}", "u8", "other", r, (n,), nrng.bytes(n)))
         lay = fpck.Layout(rep, local, k=k)
         ext = fpck.shard_extents(lay, stride)
         A = lay.align
