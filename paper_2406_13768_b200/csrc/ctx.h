@@ -12,9 +12,16 @@
 #include <vector>
 
 #include "fp_internal.h"
+#include "nvtx3/nvToolsExt.h"  // header-only NVTX v3 (no link; no-op without a tool)
 
 namespace fp {
 
+
+// NVTX range for nsys / ncu timelines (SURVEY §5 tracing)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 double now_s();
 uint64_t env_u64(const char* k, uint64_t dflt);
@@ -72,6 +79,10 @@ struct fp_ctx {
   bool gate_on = false;
   uint32_t gate_seq = 0;
   uint32_t ckpt_seq = 0;
+  // fault injection (tests): FP_FAULT_EIO_AT=<n>[@<rank>] turns the n-th write
+  // completion of a checkpoint (of that rank, or any rank) into -EIO
+  int64_t fault_eio_at = -1;
+  int fault_rank = -1;
   // CRC-32 of the shard
   uint32_t *d_crc_tab8 = nullptr, *d_lane_k = nullptr, *d_x4k = nullptr;
   uint32_t *d_page_crc = nullptr, *d_chunk_crc = nullptr, *h_crc = nullptr;

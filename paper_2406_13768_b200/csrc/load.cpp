@@ -175,6 +175,7 @@ static int pread_all(int fd, void* buf, uint64_t len, uint64_t off) {
 
 int fp_ckpt_load(fp_ctx* c, const fp_tensor* t, size_t n, const char* path, int dp_rank,
                  int dp_size, void* stream) {
+  NvtxRange nv("fp.load");
   if (!c || (!t && n) || !path || dp_size < 1 || dp_rank < 0 || dp_rank >= dp_size)
     return -EINVAL;
   if (dp_size > 1 && !c->has_comm) return -EINVAL;
@@ -470,6 +471,7 @@ static void scatter_items(const std::vector<Piece>& pcs, uint64_t io0, uint64_t 
 
 int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* path,
                           int dp_rank, int dp_size, void* stream) {
+  NvtxRange nv("fp.load_parallel");
   if (!c || (!t && n) || !path || dp_size < 1 || dp_rank < 0 || dp_rank >= dp_size)
     return -EINVAL;
   if (dp_size > 1 && !c->has_comm) return -EINVAL;

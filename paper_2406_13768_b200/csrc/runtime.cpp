@@ -96,6 +96,7 @@ std::string shard_file(int r, int k) {
 // the helper's chunk pipeline: pack -> D2H -> io_uring, ring of R slots
 // ---------------------------------------------------------------------------
 int fp_ctx::save_shard() {
+  NvtxRange nv("fp.save_shard");
   const double t0 = now_s();
   const uint64_t S = cfg.slot_bytes, SQ = cfg.sqe_bytes, A = plan.align;
   const uint32_t R = cfg.ring_slots;
@@ -140,6 +141,7 @@ int fp_ctx::save_shard() {
   int status = 0;
   IoDone done[64];
 
+  int64_t completions = 0;
   auto reap = [&](int min_wait) -> int {
     int r = io->submit();
     if (r) return r;
@@ -148,6 +150,9 @@ int fp_ctx::save_shard() {
     if (min_wait) st.t_io_stall += now_s() - tw;
     if (n < 0) return n;
     for (int i = 0; i < n; ++i) {
+      ++completions;
+      if (completions == fault_eio_at && (fault_rank < 0 || fault_rank == rank))
+        done[i].res = -EIO;  // injected (FP_FAULT_EIO_AT)
       const uint64_t u = done[i].user;
       const uint32_t s = (uint32_t)(u >> 56);
       const int64_t expect = (int64_t)((u >> 32) & 0xFFFFFF) * 512;
@@ -329,6 +334,7 @@ int fp_ctx::save_shard() {
   if (!host && stream) cudaStreamSynchronize(stream);  // never leave D2H into the ring pending
   if (status == 0 && !(cfg.flags & FP_CFG_NO_FSYNC)) {
     const double tf = now_s();
+    NvtxRange nvf("fp.fdatasync");
     status = io->fdatasync(fd);
     st.t_fsync = now_s() - tf;
   }
@@ -681,6 +687,10 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
     c->has_comm = true;
   }
   c->dev = cuda_device;
+  if (const char* f = getenv("FP_FAULT_EIO_AT")) {
+    c->fault_eio_at = strtoll(f, nullptr, 10);
+    if (const char* at = strchr(f, '@')) c->fault_rank = atoi(at + 1);
+  }
   c->ring_bytes = (size_t)cfg.ring_slots * cfg.slot_bytes;
   c->ring = alloc_ring(c->ring_bytes);
   if (!c->ring) {
@@ -839,6 +849,7 @@ int fp_ckpt_wait(fp_ctx* c, fp_stats* out) {
   }
   if (status == 0 && c->rank == 0 && c->cfg.io_engine != FP_IO_NULL) {  // null sink: no commit
     const double tc = now_s();
+    NvtxRange nvm("fp.commit");
     status = c->write_manifest();
     c->st.t_commit = now_s() - tc;
   }

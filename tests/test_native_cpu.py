@@ -340,3 +340,50 @@ def test_writer_subset_matches_oracle_and_loads(tmp_path, cfg, k, stride):
     finally:
         for c in cks:
             c.close()
+
+
+def test_injected_io_error_fails_every_rank_and_keeps_the_previous_generation(tmp_path,
+                                                                              monkeypatch):
+    """T5 fault: an EIO on one rank's 3rd write surfaces as -EIO on EVERY rank
+    (status all-reduce), no manifest is committed for that generation, and the
+    previous generation's checkpoint stays loadable."""
+    k = 2
+    states = [_state("gpt3_odd", r, k) for r in range(k)]
+    comms = ThreadComm.group(k)
+    g0, g1 = str(tmp_path / "gen0"), str(tmp_path / "gen1")
+    cks = [fp.Checkpointer(None, comm=comms[r], slot_bytes=64 << 10, sqe_bytes=16 << 10)
+           for r in range(k)]
+    try:
+        run_threads([lambda r=r: cks[r].save(entries(states[r]), g0) for r in range(k)])
+    finally:
+        for c in cks:
+            c.close()
+    monkeypatch.setenv("FP_FAULT_EIO_AT", "3@1")
+    cks = [fp.Checkpointer(None, comm=comms[r], slot_bytes=64 << 10, sqe_bytes=16 << 10)
+           for r in range(k)]
+    codes = [None] * k
+
+    def go(r):
+        try:
+            cks[r].save(entries(states[r]), g1)
+            codes[r] = 0
+        except FastPersistError as e:
+            codes[r] = e.code
+    try:
+        run_threads([lambda r=r: go(r) for r in range(k)])
+    finally:
+        for c in cks:
+            c.close()
+    assert codes == [-5, -5]
+    assert not os.path.exists(os.path.join(g1, "manifest.json"))
+    monkeypatch.delenv("FP_FAULT_EIO_AT")
+    dst = [[(s, torch.zeros_like(t)) for s, t in states[r]] for r in range(k)]
+    cks = [fp.Checkpointer(None, comm=comms[r]) for r in range(k)]
+    try:
+        run_threads([lambda r=r: cks[r].load_parallel(entries(dst[r]), g0) for r in range(k)])
+    finally:
+        for c in cks:
+            c.close()
+    for r in range(k):
+        for (_, a), (_, b) in zip(states[r], dst[r]):
+            assert torch.equal(a.reshape(-1).view(torch.uint8), b.reshape(-1).view(torch.uint8))
