@@ -387,3 +387,33 @@ def test_injected_io_error_fails_every_rank_and_keeps_the_previous_generation(tm
     for r in range(k):
         for (_, a), (_, b) in zip(states[r], dst[r]):
             assert torch.equal(a.reshape(-1).view(torch.uint8), b.reshape(-1).view(torch.uint8))
+
+
+def test_multiple_roots_place_shards_per_rank(tmp_path):
+    """fp_config.dirs (FP_CKPT_DIRS): rank r's shard goes under dirs[r % n]
+    (e.g. one local NVMe per GPU), the manifest under dirs[0]; both loads
+    find every shard through the same mapping."""
+    k = 3
+    roots = [str(tmp_path / "nvme0"), str(tmp_path / "nvme1")]
+    states = [_state("gpt3_odd", r, k) for r in range(k)]
+    lay = oracle_layout(states, k)
+    comms = ThreadComm.group(k)
+    cks = [fp.Checkpointer(None, comm=comms[r], slot_bytes=1 << 20, dirs=roots) for r in range(k)]
+    try:
+        run_threads([lambda r=r: cks[r].save(entries(states[r]), "step-7") for r in range(k)])
+        for r in range(k):
+            path = os.path.join(roots[r % 2], "step-7", fpck.shard_name(r, k))
+            assert file_sha(path) == fpck.shard_sha256(lay, r)
+        man = json.load(open(os.path.join(roots[0], "step-7", "manifest.json")))
+        assert [s["root"] for s in man["shards"]] == [0, 1, 0] and man["n_roots"] == 2
+        assert not os.path.exists(os.path.join(roots[1], "step-7", "manifest.json"))
+        for loader in ("load", "load_parallel"):
+            dst = [[(s, torch.zeros_like(t)) for s, t in states[r]] for r in range(k)]
+            run_threads([lambda r=r: getattr(cks[r], loader)(entries(dst[r]), "step-7")
+                         for r in range(k)])
+            for r in range(k):
+                for (_, a), (_, b) in zip(states[r], dst[r]):
+                    assert torch.equal(a.reshape(-1).view(torch.uint8), b.reshape(-1).view(torch.uint8))
+    finally:
+        for c in cks:
+            c.close()
