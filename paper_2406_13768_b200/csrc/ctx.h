@@ -91,6 +91,7 @@ struct fp_ctx {
   // plan cache
   bool planned = false;
   uint64_t sig_meta = 0, sig_ptr = 0;
+  uint64_t items_key = 0;  // (sig_meta, sig_ptr) the uploaded work items belong to; 0 = stale
   Plan plan;
   std::vector<TensorRef> rep, loc;
   bool host = false;

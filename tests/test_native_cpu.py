@@ -417,3 +417,17 @@ def test_multiple_roots_place_shards_per_rank(tmp_path):
     finally:
         for c in cks:
             c.close()
+
+
+def test_same_signature_new_addresses_rebuilds_work_items(tmp_path):
+    """The work-item table is cached per (layout, tensor addresses): a second
+    state with the same signature at other addresses must not reuse it."""
+    a = _state("gpt3_odd")
+    b = [(s, t + 1 if t.is_floating_point() else t + 1) for s, t in a]
+    with fp.Checkpointer(None, slot_bytes=1 << 20) as ck:
+        ck.save(entries(a), str(tmp_path / "a"))
+        ck.save(entries(b), str(tmp_path / "b"))
+        ck.save(entries(a), str(tmp_path / "a2"))
+    for d, st in (("a", a), ("b", b), ("a2", a)):
+        lay = oracle_layout([st], 1)
+        assert file_sha(tmp_path / d / "shard-0-of-1.fpck") == fpck.shard_sha256(lay, 0), d
