@@ -416,6 +416,35 @@ def our_arm(a):
     pack_gbs = pack_gbs or 0.0                       # this rank's own GPU (rank 0 reports)
     launches_all = allreduce_sum(sum(s["kernel_launches"] for s in stats), dev)
 
+    # ---- restore: the paper's two-step parallel load of the last
+    # committed generation, own shard -> all-gather -> unpack, into the same
+    # tensors (identical bytes); vs the same-run O_DIRECT read roofline
+    restore = None
+    if not a.no_restore:
+        last = os.path.join(root, f"gen{(a.warmup + a.steps - 1) % 2}")
+        gr = fp.io_bench(root, nv_bytes, tag=rank, read=True, io_depth=a.qd,
+                         sqe_bytes=a.sqe_kib << 10, ring_slots=a.ring_slots,
+                         slot_bytes=a.slot_mib << 20)
+        nvme_read = allreduce_sum(gr, dev)
+        rl = []
+        for _ in range(a.restore_steps):
+            barrier()
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            ck.load_parallel(ents, last, stream=stream)   # synchronous; checks the CRC
+            torch.cuda.synchronize(dev)
+            rl.append(allreduce_max(time.perf_counter() - t0, dev))
+        rt = statistics.median(rl)
+        restore = {"value": round(image_bytes / rt / 1e9, 4), "unit": "GB/s",
+                   "latency_s": round(rt, 4), "steps": len(rl),
+                   "nvme_read_gbs": round(nvme_read, 3),
+                   "frac": round(image_bytes / rt / 1e9 / nvme_read, 4),
+                   "call": "fp_ckpt_load_parallel (own shard O_DIRECT read-ahead over the "
+                           "pinned ring -> H2D -> all-gather -> unpack kernel, CRC-32 checked)",
+                   "roofline_how": f"fp_io_bench_read: O_DIRECT io_uring seq read, {a.qd} x "
+                                   f"{a.sqe_kib} KiB in flight, best of 2, {world} concurrent "
+                                   f"readers x {nv_bytes} B, same dir, same run"}
+
     # ---- e2e: public API with the state sourced from pinned HOST memory ------
     e2e = None
     if not a.no_e2e:
@@ -539,6 +568,7 @@ def our_arm(a):
             "gpu_launches": int(launches_all),
             "clocks": ck_clock,
             "e2e": e2e,
+            "restore": restore,
             "overhead": overhead,
             "cpu_baseline": cpu,
         }
@@ -573,6 +603,8 @@ def main():
                     help="ncu dram bytes per pack launch (from profiles/), echoed into roofline")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-overhead", action="store_true")
+    ap.add_argument("--no-restore", action="store_true")
+    ap.add_argument("--restore-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     a = ap.parse_args()
     if a.warmup < 3 and a.impl == "ours":

@@ -269,6 +269,15 @@ const char *fp_strerror(int err);
 int fp_io_bench(const char *dir, uint64_t bytes, const fp_config *cfg, int tag,
                 double *gbps);
 
+/* Read roofline for the restore path: write `bytes` to
+ * `<dir>/fp_iobench.<tag>` as fp_io_bench does (untimed, fdatasync'd), then
+ * read the file back sequentially with the configured engine (O_DIRECT,
+ * io_depth x sqe_bytes into the registered pinned ring), twice (timed), unlink.
+ * *gbps = bytes / (faster timed read pass seconds) / 1e9. Same errors as
+ * fp_io_bench.                                                                */
+int fp_io_bench_read(const char *dir, uint64_t bytes, const fp_config *cfg, int tag,
+                     double *gbps);
+
 #ifdef __cplusplus
 }
 #endif

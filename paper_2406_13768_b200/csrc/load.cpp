@@ -10,6 +10,7 @@
 #include <cerrno>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 
 #include "ctx.h"
 
@@ -131,6 +132,144 @@ struct WriterStrideScope {
     c->cfg.writer_stride = (ws == ~0ull || ws == 0) ? 1u : (uint32_t)ws;
   }
   ~WriterStrideScope() { c->cfg.writer_stride = saved; }
+};
+
+// Read-ahead over the pinned ring (the load-side mirror of the save pipeline,
+// §4.1 P:473 double buffering): chunk j's reads land in ring slot j % R and up
+// to R chunks are in flight, so the NVMe queue does not drain while chunk j is
+// copied to the GPU and scattered. A slot is refilled only after the consumer
+// released the chunk that used it and, on the device path, after the H2D copy
+// out of it (the event the consumer recorded) has completed.
+struct ReadReq {
+  int fd;
+  uint64_t file_off;
+  uint64_t buf_off;  // inside the slot
+  uint32_t len;
+};
+
+class ReadAhead {
+ public:
+  using ReqFn = std::function<int(uint64_t chunk, std::vector<ReadReq>* out)>;
+  ReadAhead(fp_ctx* c, uint64_t n_chunks, bool dev_events, ReqFn fn)
+      : c_(c), n_(n_chunks), R_(c->cfg.ring_slots), dev_(dev_events), fn_(std::move(fn)),
+        outstanding_(R_, 0) {}
+  ~ReadAhead() { drain(); }
+
+  uint8_t* slot_of(uint64_t j) const { return c_->ring + (size_t)(j % R_) * c_->cfg.slot_bytes; }
+
+  // Block until every read of chunk j has completed; 0 or the first error.
+  int wait(uint64_t j) {
+    for (;;) {
+      issue(false);
+      if (status_) return status_;
+      // slot j % R holds chunk j only (issue() stays below released_ + R)
+      if (next_ > j && outstanding_[j % R_] == 0) return 0;
+      if (inflight_ > 0) {
+        int r = pump(1);
+        if (r && !status_) status_ = r;
+        continue;
+      }
+      // nothing in flight and chunk j not fully queued: its slot is still
+      // being copied to the GPU; wait for that copy
+      issue(true);
+      if (!status_ && inflight_ == 0 && next_ <= j) status_ = -EIO;  // no progress possible
+    }
+  }
+  // The consumer is done with chunk j (its slot may be refilled once the
+  // device has finished reading it: ev_d2h[slot], recorded by the consumer).
+  void release(uint64_t j) { released_ = j + 1; }
+  void finish() { drain(); }
+  int status() const { return status_; }
+
+ private:
+  // queue requests of chunks [next_, released_ + R) while the engine has room
+  void issue(bool block_on_slot) {
+    while (next_ < n_ && next_ < released_ + R_ && !status_) {
+      const uint32_t s = (uint32_t)(next_ % R_);
+      if (cur_.empty() && pos_ == 0) {
+        if (outstanding_[s]) return;  // previous user of the slot still reading
+        if (dev_ && next_ >= R_) {
+          cudaEvent_t e = c_->ev_d2h[s];
+          cudaError_t q = cudaEventQuery(e);
+          if (q == cudaErrorNotReady) {
+            if (!block_on_slot) return;
+            q = cudaEventSynchronize(e);
+          }
+          if (q != cudaSuccess) {
+            status_ = FP_ECUDA;
+            return;
+          }
+        }
+        int r = fn_(next_, &cur_);
+        if (r) {
+          status_ = r;
+          return;
+        }
+        if (cur_.empty()) {  // nothing to read for this chunk
+          ++next_;
+          continue;
+        }
+      }
+      while (pos_ < cur_.size()) {
+        if (inflight_ >= c_->io->capacity()) {
+          c_->io->submit();
+          return;
+        }
+        const ReadReq& q = cur_[pos_];
+        const uint64_t user = ((uint64_t)s << 56) | q.len;
+        int r = c_->io->queue(false, q.fd, slot_of(next_) + q.buf_off, q.len, q.file_off, (int)s,
+                              user);
+        if (r == -EAGAIN) {
+          c_->io->submit();
+          return;
+        }
+        if (r) {
+          status_ = r;
+          return;
+        }
+        ++outstanding_[s];
+        ++inflight_;
+        ++pos_;
+      }
+      cur_.clear();
+      pos_ = 0;
+      ++next_;
+      block_on_slot = false;
+    }
+    int r = c_->io->submit();
+    if (r && !status_) status_ = r;
+  }
+  int pump(int min_wait) {
+    int r = c_->io->submit();
+    if (r) return r;
+    IoDone done[64];
+    int n = c_->io->reap(done, 64, min_wait);
+    if (n < 0) return n;
+    for (int i = 0; i < n; ++i) {
+      const uint32_t s = (uint32_t)(done[i].user >> 56);
+      const int64_t want = (int64_t)(done[i].user & 0xFFFFFFFFull);
+      if (done[i].res != want && !status_) status_ = done[i].res < 0 ? done[i].res : -EIO;
+      --outstanding_[s];
+      --inflight_;
+    }
+    return 0;
+  }
+  void drain() {
+    while (inflight_ > 0)
+      if (pump(1)) break;
+  }
+
+  fp_ctx* c_;
+  uint64_t n_;
+  uint32_t R_;
+  bool dev_;
+  ReqFn fn_;
+  std::vector<uint32_t> outstanding_;
+  uint64_t next_ = 0, released_ = 0;
+  std::vector<ReadReq> cur_;
+  size_t pos_ = 0;
+  uint32_t inflight_ = 0;
+  int status_ = 0;
 };
 
 }  // namespace
@@ -330,69 +469,45 @@ int fp_ckpt_load(fp_ctx* c, const fp_tensor* t, size_t n, const char* path, int 
   const uint64_t C = lo.size() - 1;
   cudaStream_t st = (cudaStream_t)stream;
   int status = 0;
-  IoDone done[64];
-  for (uint64_t ch = 0; ch < C && !status; ++ch) {
-    const uint32_t s = (uint32_t)(ch % c->cfg.ring_slots);
-    uint8_t* slot = c->ring + (size_t)s * S;
-    const uint64_t len = std::min<uint64_t>(S, total - ch * S);
-    // read [ch*S, ch*S+len) of the load stream
-    uint32_t inflight = 0;
-    uint64_t pos = 0;
-    while (pos < len && !status) {
-      const uint64_t ls = ch * S + pos;  // load-stream offset -> image offset
-      uint64_t io = 0;
-      for (auto& e : lp.extents)
-        if (ls >= e.file_off && ls < e.file_off + e.len) io = e.image_off + (ls - e.file_off);
-      int w;
-      uint64_t fo, avail;
-      if (!locate(io, &w, &fo, &avail)) {
-        status = FP_ECORRUPT;
-        break;
+  {
+    // chunk ch = [ch*S, ch*S+len) of the load stream, read from whichever
+    // shard holds each piece, R chunks ahead of the GPU scatter
+    ReadAhead ra(c, C, !c->host, [&](uint64_t ch, std::vector<ReadReq>* out) -> int {
+      const uint64_t len = std::min<uint64_t>(S, total - ch * S);
+      for (uint64_t pos = 0; pos < len;) {
+        const uint64_t ls = ch * S + pos;  // load-stream offset -> image offset
+        uint64_t io = 0;
+        for (auto& e : lp.extents)
+          if (ls >= e.file_off && ls < e.file_off + e.len) io = e.image_off + (ls - e.file_off);
+        int w;
+        uint64_t fo, avail;
+        if (!locate(io, &w, &fo, &avail)) return FP_ECORRUPT;
+        const uint32_t nn = (uint32_t)std::min<uint64_t>({SQ, len - pos, avail});
+        out->push_back({fds[w], fo, pos, nn});
+        pos += nn;
       }
-      const uint32_t nn = (uint32_t)std::min<uint64_t>({SQ, len - pos, avail});
-      while (inflight >= c->io->capacity()) {
-        c->io->submit();
-        int k2 = c->io->reap(done, 64, 1);
-        if (k2 < 0) {
-          status = k2;
-          break;
-        }
-        for (int i = 0; i < k2; ++i)
-          if (done[i].res < 0 && !status) status = done[i].res;
-        inflight -= (uint32_t)k2;
-      }
+      return 0;
+    });
+    for (uint64_t ch = 0; ch < C && !status; ++ch) {
+      const uint32_t s = (uint32_t)(ch % c->cfg.ring_slots);
+      const uint64_t len = std::min<uint64_t>(S, total - ch * S);
+      status = ra.wait(ch);
       if (status) break;
-      int q = c->io->queue(false, fds[w], slot + pos, nn, fo, (int)s, nn);
-      if (q) {
-        status = q;
-        break;
-      }
-      ++inflight;
-      pos += nn;
-    }
-    c->io->submit();
-    while (inflight > 0) {
-      int k2 = c->io->reap(done, 64, 1);
-      if (k2 < 0) {
-        if (!status) status = k2;
-        break;
-      }
-      for (int i = 0; i < k2; ++i)
-        if (done[i].res != (int32_t)done[i].user && !status)
-          status = done[i].res < 0 ? done[i].res : -EIO;
-      inflight -= (uint32_t)k2;
-    }
-    if (status) break;
-    if (c->host) {
-      for (uint32_t i = lo[ch]; i < lo[ch + 1]; ++i)
-        if (items[i].src) memcpy((void*)(uintptr_t)items[i].src, slot + items[i].dst, items[i].len);
-    } else {
-      if (cudaMemcpyAsync(c->d_slab, slot, len, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-          unpack_launch(d_items + lo[ch], lo[ch + 1] - lo[ch], c->d_slab, c->pack_ctas, st) ||
-          cudaStreamSynchronize(st) != cudaSuccess)
+      const uint8_t* slot = ra.slot_of(ch);
+      if (c->host) {
+        for (uint32_t i = lo[ch]; i < lo[ch + 1]; ++i)
+          if (items[i].src)
+            memcpy((void*)(uintptr_t)items[i].src, slot + items[i].dst, items[i].len);
+      } else if (cudaMemcpyAsync(c->d_slab, slot, len, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+                 cudaEventRecord(c->ev_d2h[s], st) != cudaSuccess ||
+                 unpack_launch(d_items + lo[ch], lo[ch + 1] - lo[ch], c->d_slab, c->pack_ctas,
+                               st)) {
         status = FP_ECUDA;
+      }
+      ra.release(ch);
     }
-  }
+  }  // ~ReadAhead drains reads still in flight (error paths)
+  if (!c->host && cudaStreamSynchronize(st) != cudaSuccess && !status) status = FP_ECUDA;
   if (d_items) cudaFree(d_items);
   close_all();
   return status;
@@ -408,39 +523,6 @@ static int status_min(fp_ctx* c, int k, int s) {
   int32_t v = s;
   if (c->comm.allreduce_min_i32(c->comm.ctx, &v)) return s ? s : FP_ECOMM;
   return v;
-}
-
-// Read [off, off+len) of fd into buf (inside ring slot `slot`) with the I/O
-// engine in sqe_bytes requests; blocks until all complete. 0 or -errno.
-static int read_span(fp_ctx* c, int fd, uint8_t* buf, uint64_t len, uint64_t off, int slot) {
-  IoDone done[64];
-  uint32_t inflight = 0;
-  uint64_t pos = 0;
-  int status = 0;
-  while ((pos < len || inflight) && !status) {
-    while (pos < len && inflight < c->io->capacity()) {
-      const uint32_t nn = (uint32_t)std::min<uint64_t>(c->cfg.sqe_bytes, len - pos);
-      int q = c->io->queue(false, fd, buf + pos, nn, off + pos, slot, nn);
-      if (q == -EAGAIN) break;
-      if (q) return q;
-      ++inflight;
-      pos += nn;
-    }
-    int r = c->io->submit();
-    if (r) return r;
-    int k2 = c->io->reap(done, 64, 1);
-    if (k2 < 0) return k2;
-    for (int i = 0; i < k2; ++i)
-      if (done[i].res != (int32_t)done[i].user && !status)
-        status = done[i].res < 0 ? done[i].res : -EIO;
-    inflight -= (uint32_t)k2;
-  }
-  while (inflight) {  // drain after an error
-    int k2 = c->io->reap(done, 64, 1);
-    if (k2 < 0) break;
-    inflight -= (uint32_t)k2;
-  }
-  return status;
 }
 
 // Items scattering image range [io0, io0+len) (located at buffer offset
@@ -616,22 +698,33 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
     if (!crc_pinned) chunk_crc = (uint32_t*)calloc(chunk_len.size() + 1, 4);
   }
   const bool run = status == 0;  // agreed on every rank by the all-reduce above
+  // this rank's bytes of chunk j: (length, offset in the own shard file)
+  auto my_span = [&](uint64_t j, uint64_t* foff) -> uint64_t {
+    if (j < nrep) {
+      const uint64_t pb = part_bytes(rank);
+      *foff = j * CH;
+      return j * CH < pb ? std::min(CH, pb - j * CH) : 0;
+    }
+    const uint64_t jj = j - nrep;
+    *foff = part_bytes(rank) + jj * CH;
+    return std::min(CH, lreg_len - jj * CH);
+  };
+  // own-shard reads run R chunks ahead of the exchange + scatter
+  ReadAhead ra(c, run ? total_chunks : 0, dev, [&](uint64_t j, std::vector<ReadReq>* out) -> int {
+    uint64_t foff = 0;
+    const uint64_t len = my_span(j, &foff);
+    for (uint64_t pos = 0; pos < len; pos += c->cfg.sqe_bytes)
+      out->push_back({fd, foff + pos, pos,
+                      (uint32_t)std::min<uint64_t>(c->cfg.sqe_bytes, len - pos)});
+    return 0;
+  });
   for (uint64_t j = 0; run && j < total_chunks; ++j) {  // every rank runs every exchange
     const bool is_rep = j < nrep;
     const uint32_t s = (uint32_t)(j % R);
-    uint8_t* slot = c->ring + (size_t)s * c->cfg.slot_bytes;
-    if (dev && j >= R) cudaEventSynchronize(c->ev_d2h[s]);  // H2D out of this slot done
-    uint64_t mylen, foff;
-    if (is_rep) {
-      const uint64_t pb = part_bytes(rank);
-      mylen = j * CH < pb ? std::min(CH, pb - j * CH) : 0;
-      foff = j * CH;
-    } else {
-      const uint64_t jj = j - nrep;
-      mylen = std::min(CH, lreg_len - jj * CH);
-      foff = part_bytes(rank) + jj * CH;
-    }
-    int rr = mylen ? read_span(c, fd, slot, mylen, foff, (int)s) : 0;
+    uint8_t* slot = ra.slot_of(j);
+    uint64_t foff = 0;
+    const uint64_t mylen = my_span(j, &foff);
+    int rr = status ? 0 : ra.wait(j);
     if (rr && !status) status = rr;  // keep exchanging so the collectives stay matched
     const bool gpu_crc = check_crc && dev && mylen % 4096 == 0 && c->d_crc_tab8;
     if (check_crc && mylen && !gpu_crc) chunk_crc[j] = crc_raw_update(0, slot, mylen);
@@ -677,7 +770,9 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
           memcpy((void*)(uintptr_t)items[i].src, src + items[i].dst, items[i].len);
       }
     }
+    ra.release(j);
   }
+  ra.finish();  // reads still in flight after an error land before the ring is reused
   if (dev && cudaStreamSynchronize(st) != cudaSuccess && !status) status = FP_ECUDA;
   if (!status && check_crc && run) {
     uint32_t raw = 0;

@@ -934,7 +934,8 @@ const char* fp_strerror(int err) {
   return "unknown error";
 }
 
-int fp_io_bench(const char* dir, uint64_t bytes, const fp_config* cfg_in, int tag, double* gbps) {
+static int io_bench(const char* dir, uint64_t bytes, const fp_config* cfg_in, int tag,
+                    bool timed_read, double* gbps) {
   if (!dir || !gbps) return -EINVAL;
   fp_config cfg;
   if (cfg_in)
@@ -973,7 +974,7 @@ int fp_io_bench(const char* dir, uint64_t bytes, const fp_config* cfg_in, int ta
   IoDone done[64];
   int status = 0;
   const uint64_t span = ring_bytes;
-  auto pass = [&]() {
+  auto pass = [&](bool write) {
     uint64_t off = 0;
     uint32_t inflight = 0;
     while ((off < bytes || inflight) && !status) {
@@ -982,7 +983,7 @@ int fp_io_bench(const char* dir, uint64_t bytes, const fp_config* cfg_in, int ta
         const uint64_t ro = off % span;
         const uint32_t slot = (uint32_t)(ro / cfg.slot_bytes);
         const uint32_t nn = (uint32_t)std::min<uint64_t>(n, cfg.slot_bytes - ro % cfg.slot_bytes);
-        if (io->queue(true, fd, ring + ro, nn, off, (int)slot, nn)) break;
+        if (io->queue(write, fd, ring + ro, nn, off, (int)slot, nn)) break;
         ++inflight;
         off += nn;
       }
@@ -997,15 +998,28 @@ int fp_io_bench(const char* dir, uint64_t bytes, const fp_config* cfg_in, int ta
           status = done[i].res < 0 ? done[i].res : -EIO;
       inflight -= (uint32_t)k2;
     }
-    if (!status && !(cfg.flags & FP_CFG_NO_FSYNC)) status = io->fdatasync(fd);
+    if (write && !status && !(cfg.flags & FP_CFG_NO_FSYNC)) status = io->fdatasync(fd);
   };
-  pass();
+  pass(true);
+  int rfd = -1;
+  if (timed_read && !status) {  // O_DIRECT reads of the file just written
+    rfd = open(f.c_str(), O_RDONLY | (direct ? O_DIRECT : 0));
+    if (rfd < 0 && direct && errno == EINVAL) rfd = open(f.c_str(), O_RDONLY);
+    if (rfd < 0) status = -errno;
+  }
   double dt = 1e30;
-  for (int rep = 0; rep < 2 && !status; ++rep) {  // best of two timed overwrites
+  for (int rep = 0; rep < 2 && !status; ++rep) {  // best of two timed passes
     const double t0 = now_s();
-    pass();
+    if (timed_read) {
+      std::swap(fd, rfd);
+      pass(false);
+      std::swap(fd, rfd);
+    } else {
+      pass(true);
+    }
     dt = std::min(dt, now_s() - t0);
   }
+  if (rfd >= 0) close(rfd);
   close(fd);
   unlink(f.c_str());
   delete io;
@@ -1013,6 +1027,15 @@ int fp_io_bench(const char* dir, uint64_t bytes, const fp_config* cfg_in, int ta
   if (status) return status;
   *gbps = (double)bytes / dt / 1e9;
   return 0;
+}
+
+int fp_io_bench(const char* dir, uint64_t bytes, const fp_config* cfg, int tag, double* gbps) {
+  return io_bench(dir, bytes, cfg, tag, false, gbps);
+}
+
+int fp_io_bench_read(const char* dir, uint64_t bytes, const fp_config* cfg, int tag,
+                     double* gbps) {
+  return io_bench(dir, bytes, cfg, tag, true, gbps);
 }
 
 }  // extern "C"

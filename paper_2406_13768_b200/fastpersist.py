@@ -101,7 +101,7 @@ class fp_stats(C.Structure):
 
 EXPORTS = ("fp_config_default", "fp_ckpt_init", "fp_ckpt_begin", "fp_ckpt_fence", "fp_ckpt_wait",
            "fp_ckpt_load", "fp_ckpt_load_parallel", "fp_ckpt_plan_info", "fp_ckpt_destroy", "fp_strerror",
-           "fp_io_bench")
+           "fp_io_bench", "fp_io_bench_read")
 
 _lib = None
 
@@ -134,6 +134,8 @@ def lib():
     L.fp_strerror.restype = C.c_char_p
     L.fp_io_bench.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(fp_config), C.c_int,
                               C.POINTER(C.c_double)]
+    L.fp_io_bench_read.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(fp_config), C.c_int,
+                                   C.POINTER(C.c_double)]
     _lib = L
     return L
 
@@ -419,10 +421,12 @@ class Checkpointer:
         self.close()
 
 
-def io_bench(directory, nbytes, tag=0, **cfg):
-    """Built-in O_DIRECT sequential-write roofline (fio substitute): GB/s."""
+def io_bench(directory, nbytes, tag=0, read=False, **cfg):
+    """Built-in O_DIRECT sequential-write (read=True: read-back) roofline
+    (fio substitute): GB/s."""
     c = make_config(**cfg)
     g = C.c_double()
-    _check(lib().fp_io_bench(os.fsencode(directory), int(nbytes), C.byref(c), int(tag),
-                             C.byref(g)), "fp_io_bench")
+    fn = lib().fp_io_bench_read if read else lib().fp_io_bench
+    _check(fn(os.fsencode(directory), int(nbytes), C.byref(c), int(tag), C.byref(g)),
+           "fp_io_bench_read" if read else "fp_io_bench")
     return g.value

@@ -217,6 +217,9 @@ def test_io_bench_runs(tmp_path):
     g = fp.io_bench(str(tmp_path), 8 << 20, slot_bytes=1 << 20, ring_slots=2)
     assert g > 0
     assert not os.listdir(tmp_path)
+    g = fp.io_bench(str(tmp_path), 8 << 20, read=True, slot_bytes=1 << 20, ring_slots=2)
+    assert g > 0
+    assert not os.listdir(tmp_path)
 
 
 def test_null_sink_engine_runs_the_pipeline_but_commits_nothing(tmp_path):
@@ -431,3 +434,21 @@ def test_same_signature_new_addresses_rebuilds_work_items(tmp_path):
     for d, st in (("a", a), ("b", b), ("a2", a)):
         lay = oracle_layout([st], 1)
         assert file_sha(tmp_path / d / "shard-0-of-1.fpck") == fpck.shard_sha256(lay, 0), d
+
+
+@pytest.mark.parametrize("slots", [1, 2, 3])
+@pytest.mark.parametrize("engine", ["uring", "pwrite"])
+@pytest.mark.parametrize("how", ["load", "load_parallel"])
+def test_load_read_ahead_ring_depths_host(tmp_path, slots, engine, how):
+    """Read-ahead over the ring (chunk j -> slot j % R, up to R chunks in
+    flight): bit-exact round trip for ring depths 1..3, ~56 chunks of 1 MiB,
+    request size below the chunk size, both engines."""
+    st = _state("gpt3_odd")
+    d = str(tmp_path / "ck")
+    with fp.Checkpointer(None, slot_bytes=1 << 20, ring_slots=slots, io_engine=engine,
+                         sqe_bytes=256 << 10, io_depth=6) as ck:
+        ck.save(entries(st), d)
+        dst = [(s, torch.full_like(t, 7)) for s, t in st]
+        getattr(ck, how)(entries(dst), d)
+    for (_, a), (_, b) in zip(st, dst):
+        assert torch.equal(a.view(-1).view(torch.uint8), b.view(-1).view(torch.uint8))
