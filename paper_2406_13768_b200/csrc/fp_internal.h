@@ -107,9 +107,11 @@ static_assert(sizeof(Item) == 16, "Item must be 16 bytes");
 // Items for every chunk of the shard file (chunk = slot_bytes of file bytes).
 // item_lo has n_chunks+1 entries. Item.dst is relative to the start of the
 // chunk's pack group (group = group_bytes/slot_bytes consecutive chunks that
-// one pack launch gathers into one device slab).
+// one pack launch gathers into one device slab). An item never spans two
+// pieces (so never two allocations) and is at most max_item bytes.
 void plan_items(const Plan& p, uint64_t slot_bytes, uint64_t group_bytes,
-                std::vector<Item>* items, std::vector<uint32_t>* item_lo);
+                std::vector<Item>* items, std::vector<uint32_t>* item_lo,
+                uint64_t max_item = kTile);
 
 // ---------------------------------------------------------------------------
 // I/O engines

@@ -283,7 +283,7 @@ void plan_pieces(Plan* p, const std::vector<TensorRef>& rep, const std::vector<T
 }
 
 void plan_items(const Plan& p, uint64_t slot_bytes, uint64_t group_bytes,
-                std::vector<Item>* items, std::vector<uint32_t>* item_lo) {
+                std::vector<Item>* items, std::vector<uint32_t>* item_lo, uint64_t max_item) {
   const uint64_t per_group = group_bytes / slot_bytes;
   items->clear();
   item_lo->clear();
@@ -302,7 +302,7 @@ void plan_items(const Plan& p, uint64_t slot_bytes, uint64_t group_bytes,
         ++chunk;
       }
       const uint64_t cend = (chunk + 1) * slot_bytes;
-      const uint64_t n = std::min<uint64_t>({left, (uint64_t)kTile, cend - fo});
+      const uint64_t n = std::min<uint64_t>({left, max_item, cend - fo});
       const uint64_t gbase = chunk / per_group * per_group * slot_bytes;
       items->push_back({src, (uint32_t)(fo - gbase), (uint32_t)n});
       fo += n;

@@ -541,25 +541,11 @@ int fp::build_items(fp_ctx* c, bool for_save) {
              c->host || slabless ? c->cfg.slot_bytes : c->cfg.pack_bytes, &c->items,
              &c->item_lo);
   if (c->cfg.pack_impl == FP_PACK_CE && !c->host) {
-    // merge consecutive items of a chunk that continue the same source run
-    c->runs.clear();
-    c->run_lo.assign(1, 0);
-    for (size_t ch = 0; ch + 1 < c->item_lo.size(); ++ch) {
-      for (uint32_t i = c->item_lo[ch]; i < c->item_lo[ch + 1]; ++i) {
-        const Item& it = c->items[i];
-        if (c->runs.size() > c->run_lo.back()) {
-          Item& b = c->runs.back();
-          const bool contig = b.dst + b.len == it.dst && ((!b.src && !it.src) ||
-                                                           (b.src && it.src && b.src + b.len == it.src));
-          if (contig) {
-            b.len += it.len;
-            continue;
-          }
-        }
-        c->runs.push_back(it);
-      }
-      c->run_lo.push_back((uint32_t)c->runs.size());
-    }
+    // one copy-engine run per (piece ∩ chunk): never merged across pieces,
+    // since two tensors adjacent in the address space may still be separate
+    // allocations and one cudaMemcpyAsync must not span both
+    plan_items(c->plan, c->cfg.slot_bytes, c->cfg.slot_bytes, &c->runs, &c->run_lo,
+               c->cfg.slot_bytes);
   }
   if (!c->host && c->dev >= 0 && !c->items.empty()) {
     const size_t need = c->items.size() * sizeof(Item);
@@ -750,7 +736,10 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
       c->h_sig = (volatile uint32_t*)hg;
       if (cudaHostGetDevicePointer(&dg, hg, 0) != cudaSuccess) return fail(FP_ECUDA);
       c->d_sig = (uint32_t*)dg;
-      c->gate_on = !getenv("FP_NO_GATE");
+      // the gate relies on asynchronous launches: a profiler that serialises
+      // kernels (ncu, injected through CUDA_INJECTION64_PATH) would run the
+      // gate kernel to its timeout before the host could open it
+      c->gate_on = !getenv("FP_NO_GATE") && !getenv("CUDA_INJECTION64_PATH");
     }
     // CRC tables + scratch: slicing tables, lane multipliers x^(8*128*(31-l)),
     // x^(8*4096*2^i), page CRCs of one pack group, chunk CRCs
@@ -858,11 +847,24 @@ int fp_ckpt_wait(fp_ctx* c, fp_stats* out) {
       c->shard_crcs[0] = mine;
     }
   }
+  const bool agreed_ok = status == 0;  // the same on every rank
   if (status == 0 && c->rank == 0 && c->cfg.io_engine != FP_IO_NULL) {  // null sink: no commit
     const double tc = now_s();
     NvtxRange nvm("fp.commit");
     status = c->write_manifest();
     c->st.t_commit = now_s() - tc;
+  }
+  if (agreed_ok && c->k > 1) {
+    // second barrier: no rank returns before rank 0's commit is durable (a
+    // rank that loads right after wait() must find the manifest), and a
+    // failed commit is every rank's error (R12)
+    const double tb = now_s();
+    int32_t s = status;
+    if (c->comm.allreduce_min_i32(c->comm.ctx, &s))
+      status = status ? status : FP_ECOMM;
+    else
+      status = s;
+    c->st.t_barrier += now_s() - tb;
   }
   c->st.status = status;
   c->st.t_total = now_s() - c->t_begin;

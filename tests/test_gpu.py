@@ -201,6 +201,7 @@ def test_c2_gpt3_1p3b_full_size_parity(tmp_path):
             f.seek(pg * 4096)
             assert f.read(4096) == lay.read(pg * 4096, 4096), pg
     assert file_sha(path) == fpck.shard_sha256(lay, 0)
+    os.remove(path)          # pytest keeps tmp dirs: do not leave 21 GB on the disk
 
 
 @pytest.mark.parametrize("cfg,k", [("gpt3_small", 4), ("moe_small", 2), ("c1_tiny", 3),
