@@ -358,7 +358,7 @@ def our_arm(a):
 
     cfg = dict(pack=a.pack, slot_bytes=a.slot_mib << 20, ring_slots=a.ring_slots,
                io_depth=a.qd, sqe_bytes=a.sqe_kib << 10, pack_bytes=a.pack_mib << 20,
-               prio=a.prio, writer_stride=a.writer_stride)
+               prio=a.prio, writer_stride=a.writer_stride, io_engine=a.io_engine)
     peaks, peak_src = measured_peaks()
 
     # ---- rooflines measured in the same run --------------------------------
@@ -554,6 +554,7 @@ def our_arm(a):
                        "pack_launch_mib": a.pack_mib, "pack_stream_prio": a.prio,
                        "writer_stride": a.writer_stride,
                        "sqe_kib": a.sqe_kib, "qd": a.qd, "engine": stats[-1]["engine"],
+                       "io_fallback": stats[-1]["fallback"],
                        "l2": "inputs (21 GB of state) larger than L2; no flush needed",
                        "dir": root},
             "latency_s": {"median": round(statistics.median(lat_max), 4),
@@ -601,6 +602,8 @@ def main():
     ap.add_argument("--writer-stride", type=int, default=1,
                     help="writer subset (P:495-499): ranks r %% s == 0 write replicated bytes")
     ap.add_argument("--slot-mib", type=int, default=64)
+    ap.add_argument("--io-engine", default="uring", choices=["uring", "pwrite", "gds"],
+                    help="gds: GPUDirect Storage (SURVEY f2), device slab -> cuFileWrite")
     ap.add_argument("--ring-slots", type=int, default=4)
     ap.add_argument("--qd", type=int, default=64)
     ap.add_argument("--sqe-kib", type=int, default=1024)

@@ -96,9 +96,19 @@ typedef struct fp_comm {
 enum fp_io_engine { FP_IO_URING = 0,    /* io_uring, O_DIRECT, registered bufs */
                     FP_IO_PWRITE = 1,   /* pwrite thread pool, O_DIRECT         */
                     FP_IO_BUFFERED = 2, /* pwrite through the page cache        */
-                    FP_IO_NULL = 3      /* ablation: requests complete at once,
+                    FP_IO_NULL = 3,     /* ablation: requests complete at once,
                                            nothing is written (measures the
-                                           pack + D2H + ring ceiling)           */ };
+                                           pack + D2H + ring ceiling)           */
+                    FP_IO_GDS = 4       /* GPUDirect Storage: device
+                                           state is packed into a doubled device
+                                           slab and written with cuFileWrite from
+                                           HBM (no pinned ring); libcufile is
+                                           loaded at run time (fp_ckpt_init ->
+                                           -ENOSYS without it). Without nvidia-fs
+                                           libcufile runs in compatibility mode:
+                                           stats.fallback = 2. Needs a device and
+                                           a slab pack (v4/bulk); loads and host
+                                           state use io_uring.                   */ };
 enum fp_pack_impl { FP_PACK_V4 = 0,     /* LSU 16-B vector gather -> device slab,
                                            then copy engine -> pinned ring       */
                     FP_PACK_BULK = 1,   /* cp.async.bulk (TMA engine) via smem
@@ -160,7 +170,8 @@ typedef struct fp_stats {
   double   t_commit;       /* s, manifest write + rename + dir fsync (rank 0)     */
   double   t_io_stall;     /* s, helper time blocked waiting for I/O completions  */
   uint32_t max_inflight;   /* peak in-flight I/O requests                         */
-  uint32_t fallback;       /* 1 if O_DIRECT was unavailable -> buffered I/O       */
+  uint32_t fallback;       /* 1 if O_DIRECT was unavailable -> buffered I/O;
+                              2 if FP_IO_GDS ran in cuFile compatibility mode  */
   int32_t  engine;         /* enum fp_io_engine actually used                     */
   int32_t  status;         /* final status of this checkpoint                     */
   int64_t  err_offset;     /* file offset of the first failed request, or -1      */
@@ -174,7 +185,7 @@ typedef struct fp_stats {
 typedef struct fp_ctx fp_ctx;
 
 /* Fill *cfg with the defaults above (env overrides: FP_RING_SLOTS,
- * FP_SLOT_BYTES, FP_SQE_BYTES, FP_QD, FP_IO_ENGINE=uring|pwrite|buffered|null,
+ * FP_SLOT_BYTES, FP_SQE_BYTES, FP_QD, FP_IO_ENGINE=uring|pwrite|buffered|null|gds,
  * FP_PACK=v4|bulk|host|ce, FP_PACK_PRIO=low, FP_PACK_CTAS, FP_ALIGN, FP_PACK_BYTES). Returns 0.         */
 int fp_config_default(fp_config *cfg);
 

@@ -39,6 +39,19 @@ std::string shard_file(int r, int k);
     }                                                                                \
   } while (0)
 
+// GPUDirect Storage (gds.cpp): libcufile loaded at run time
+class GdsPool;
+int gds_available(bool* p2p);  // 0 or -ENOSYS; *p2p: NVMe P2P (not compat mode)
+GdsPool* gds_pool_new(uint32_t threads);
+void gds_pool_delete(GdsPool* p);
+int gds_buf_register(void* d, uint64_t bytes);
+void gds_buf_deregister(void* d);
+int gds_handle_open(int fd, void** fh);
+void gds_handle_close(void* fh);
+void gds_post(GdsPool* pool, bool write, void* fh, void* base, uint64_t buf_off,
+              uint64_t file_off, uint64_t len, uint64_t piece);
+int gds_wait(GdsPool* pool, double* stall);
+
 }  // namespace fp
 
 using fp::Extent;
@@ -88,6 +101,12 @@ struct fp_ctx {
   uint32_t *d_page_crc = nullptr, *d_chunk_crc = nullptr, *h_crc = nullptr;
   IoEngine* io = nullptr;
   int pack_ctas = 0;
+  // GPUDirect Storage (FP_IO_GDS): writer pool, per-half events
+  // [pack start, pack end, group done] x 2, pinned chunk CRCs of both halves
+  bool gds = false, gds_p2p = false, gds_slab_registered = false;
+  fp::GdsPool* gds_pool = nullptr;
+  cudaEvent_t gds_ev[6] = {};
+  uint32_t* h_gds_crc = nullptr;
   // plan cache
   bool planned = false;
   uint64_t sig_meta = 0, sig_ptr = 0;
@@ -120,6 +139,8 @@ struct fp_ctx {
   double t_begin = 0;
 
   int save_shard();
+  int save_shard_gds(int fd, uint32_t* shard_raw);
+  int finish_shard(int fd, int status, uint32_t shard_raw, double t0);
   void helper();
   int write_manifest();
 };

@@ -657,8 +657,14 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
   Item* d_items = nullptr;
   cudaStream_t st = (cudaStream_t)stream;
   int status = 0;
+  // GPUDirect Storage: own-shard chunks are read with cuFileRead
+  // straight into a double-buffered device `send` (no ring, no H2D)
+  const bool use_gds = dev && c->gds;
+  void* gfh = nullptr;
+  if (use_gds && !status && fd >= 0) status = gds_handle_open(fd, &gfh);
   if (dev) {
-    if (cudaMalloc(&send, CH) != cudaSuccess || cudaMalloc(&recv, CH * k) != cudaSuccess ||
+    if (cudaMalloc(&send, CH * (use_gds ? 2 : 1)) != cudaSuccess ||
+        cudaMalloc(&recv, CH * k) != cudaSuccess ||
         (!items.empty() && (cudaMalloc(&d_items, items.size() * sizeof(Item)) != cudaSuccess ||
                             cudaMemcpy(d_items, items.data(), items.size() * sizeof(Item),
                                        cudaMemcpyHostToDevice) != cudaSuccess)))
@@ -710,7 +716,8 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
     return std::min(CH, lreg_len - jj * CH);
   };
   // own-shard reads run R chunks ahead of the exchange + scatter
-  ReadAhead ra(c, run ? total_chunks : 0, dev, [&](uint64_t j, std::vector<ReadReq>* out) -> int {
+  ReadAhead ra(c, run && !use_gds ? total_chunks : 0, dev,
+               [&](uint64_t j, std::vector<ReadReq>* out) -> int {
     uint64_t foff = 0;
     const uint64_t len = my_span(j, &foff);
     for (uint64_t pos = 0; pos < len; pos += c->cfg.sqe_bytes)
@@ -724,17 +731,38 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
     uint8_t* slot = ra.slot_of(j);
     uint64_t foff = 0;
     const uint64_t mylen = my_span(j, &foff);
-    int rr = status ? 0 : ra.wait(j);
-    if (rr && !status) status = rr;  // keep exchanging so the collectives stay matched
     const bool gpu_crc = check_crc && dev && mylen % 4096 == 0 && c->d_crc_tab8;
-    if (check_crc && mylen && !gpu_crc) chunk_crc[j] = crc_raw_update(0, slot, mylen);
+    uint8_t* sbuf = use_gds ? send + (j & 1) * CH : send;
+    if (use_gds) {
+      // the unpack of chunk j-2 read this half: wait for it, then read into it
+      if (j >= 2 && cudaEventSynchronize(c->gds_ev[j & 1]) != cudaSuccess && !status)
+        status = FP_ECUDA;
+      if (mylen && !status) {
+        gds_post(c->gds_pool, false, gfh, send, (j & 1) * CH, foff, mylen,
+                 std::max<uint64_t>(c->cfg.sqe_bytes, 4ull << 20));
+        int rr = gds_wait(c->gds_pool, nullptr);
+        if (rr && !status) status = rr;  // keep exchanging so the collectives stay matched
+      }
+      if (check_crc && mylen && !gpu_crc && !status) {  // ragged chunk: CRC on the host
+        if (cudaMemcpy(slot, sbuf, mylen, cudaMemcpyDeviceToHost) != cudaSuccess)
+          status = FP_ECUDA;
+        else
+          chunk_crc[j] = crc_raw_update(0, slot, mylen);
+      }
+    } else {
+      int rr = status ? 0 : ra.wait(j);
+      if (rr && !status) status = rr;  // keep exchanging so the collectives stay matched
+      if (check_crc && mylen && !gpu_crc) chunk_crc[j] = crc_raw_update(0, slot, mylen);
+    }
     chunk_len[j] = mylen;
     if (dev) {
-      if (mylen && cudaMemcpyAsync(send, slot, mylen, cudaMemcpyHostToDevice, st) != cudaSuccess)
-        status = status ? status : FP_ECUDA;
-      cudaEventRecord(c->ev_d2h[s], st);
+      if (!use_gds) {
+        if (mylen && cudaMemcpyAsync(send, slot, mylen, cudaMemcpyHostToDevice, st) != cudaSuccess)
+          status = status ? status : FP_ECUDA;
+        cudaEventRecord(c->ev_d2h[s], st);
+      }
       if (gpu_crc && mylen &&
-          (crc_launch(send, mylen, mylen, c->d_crc_tab8, c->d_lane_k, c->d_x4k, c->d_page_crc,
+          (crc_launch(sbuf, mylen, mylen, c->d_crc_tab8, c->d_lane_k, c->d_x4k, c->d_page_crc,
                       c->d_chunk_crc, st) ||
            cudaMemcpyAsync(&chunk_crc[j], c->d_chunk_crc, 4, cudaMemcpyDeviceToHost, st) !=
                cudaSuccess))
@@ -742,10 +770,10 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
     } else if (mylen) {
       memcpy(send, slot, mylen);
     }
-    const uint8_t* src = send;
+    const uint8_t* src = sbuf;
     if (is_rep) {
       if (k > 1) {
-        if (c->comm.allgather_bytes(c->comm.ctx, send, recv, CH, dev ? 1 : 0, stream)) {
+        if (c->comm.allgather_bytes(c->comm.ctx, sbuf, recv, CH, dev ? 1 : 0, stream)) {
           status = status ? status : FP_ECOMM;
           break;
         }
@@ -770,6 +798,8 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
           memcpy((void*)(uintptr_t)items[i].src, src + items[i].dst, items[i].len);
       }
     }
+    if (use_gds && cudaEventRecord(c->gds_ev[j & 1], st) != cudaSuccess && !status)
+      status = FP_ECUDA;  // this half is free once the work above has run
     ra.release(j);
   }
   ra.finish();  // reads still in flight after an error land before the ring is reused
@@ -800,6 +830,7 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
     status = FP_ECORRUPT;
   }
   status = status_min(c, k, status);
+  if (gfh) gds_handle_close(gfh);
   if (dev) {
     if (send) cudaFree(send);
     if (recv) cudaFree(recv);

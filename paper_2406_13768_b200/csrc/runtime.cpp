@@ -134,6 +134,13 @@ int fp_ctx::save_shard() {
     }
   }
   st.engine = io->kind();
+  if (gds && !host) {  // device slab -> cuFileWrite, no host ring
+    st.engine = FP_IO_GDS;
+    st.fallback = gds_p2p ? 0 : 2;
+    uint32_t raw = 0;
+    const int status = save_shard_gds(fd, &raw);
+    return finish_shard(fd, status, raw, t0);
+  }
   const uint64_t C = item_lo.size() - 1;
   std::vector<uint32_t> slot_out(R, 0);
   uint64_t next_gpu = 0, next_io = 0;
@@ -332,6 +339,11 @@ int fp_ctx::save_shard() {
     }
   }
   if (!host && stream) cudaStreamSynchronize(stream);  // never leave D2H into the ring pending
+  return finish_shard(fd, status, shard_raw, t0);
+}
+
+// durability (a7) + close + CRC finalisation, shared by the ring and GDS paths
+int fp_ctx::finish_shard(int fd, int status, uint32_t shard_raw, double t0) {
   if (status == 0 && !(cfg.flags & FP_CFG_NO_FSYNC)) {
     const double tf = now_s();
     NvtxRange nvf("fp.fdatasync");
@@ -340,7 +352,7 @@ int fp_ctx::save_shard() {
   }
   if (close(fd) && status == 0) status = -errno;
   st.shard_bytes = plan.shard_bytes;
-  if (status == 0 && want_crc) {
+  if (status == 0 && !(cfg.flags & FP_CFG_NO_CRC)) {
     st.shard_crc32 = shard_raw ^ crc_zeros(plan.shard_bytes);
     st.crc_valid = 1;
   }
@@ -596,6 +608,7 @@ int fp_config_default(fp_config* cfg) {
                    : !strcmp(e, "pwrite") ? FP_IO_PWRITE
                    : !strcmp(e, "buffered") ? FP_IO_BUFFERED
                    : !strcmp(e, "null")     ? FP_IO_NULL
+                   : !strcmp(e, "gds")      ? FP_IO_GDS
                                              : FP_IO_URING;
   const char* pk = getenv("FP_PACK");
   cfg->pack_impl = !pk                   ? FP_PACK_V4
@@ -614,7 +627,9 @@ static int check_cfg(const fp_config& c) {
   if (!c.slot_bytes || c.slot_bytes % A || c.slot_bytes > (1ull << 31)) return -EINVAL;
   if (!c.sqe_bytes || c.sqe_bytes % A || c.sqe_bytes > (1u << 30)) return -EINVAL;
   if (c.sqe_bytes / 512 >= (1u << 24)) return -EINVAL;
-  if (c.io_engine > FP_IO_NULL || c.pack_impl > FP_PACK_CE) return -EINVAL;
+  if (c.io_engine > FP_IO_GDS || c.pack_impl > FP_PACK_CE) return -EINVAL;
+  if (c.io_engine == FP_IO_GDS && (c.pack_impl == FP_PACK_HOST || c.pack_impl == FP_PACK_CE))
+    return -EINVAL;  // GDS writes from the device slab: a slab-producing pack is needed
   if (c.pack_bytes > (2ull << 30)) return -EINVAL;
   return 0;
 }
@@ -626,8 +641,8 @@ static IoEngine* open_engine(const fp_config& cfg, int* kind_used) {
     *kind_used = io->kind();
     return io;
   }
-  if (cfg.io_engine == FP_IO_URING) {
-    int err = 0;
+  if (cfg.io_engine == FP_IO_URING || cfg.io_engine == FP_IO_GDS) {  // GDS: ring engine for
+    int err = 0;                                                          // loads / host state
     io = make_uring(cfg.io_depth, &err);
     if (!io) fprintf(stderr, "fastpersist: io_uring unavailable (%s); using pwrite pool\n",
                      strerror(-err));
@@ -677,6 +692,19 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
     c->has_comm = true;
   }
   c->dev = cuda_device;
+  if (cfg.io_engine == FP_IO_GDS) {
+    if (cuda_device < 0) {
+      delete c;
+      return -EINVAL;  // GDS moves device memory
+    }
+    int g = gds_available(&c->gds_p2p);
+    if (g) {
+      fprintf(stderr, "fastpersist: FP_IO_GDS requested but libcufile is unavailable\n");
+      delete c;
+      return g;
+    }
+    c->gds = true;
+  }
   if (const char* f = getenv("FP_FAULT_EIO_AT")) {
     c->fault_eio_at = strtoll(f, nullptr, 10);
     if (const char* at = strchr(f, '@')) c->fault_rank = atoi(at + 1);
@@ -702,7 +730,18 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
     c->ring_cuda_registered = true;
     if (cudaHostGetDevicePointer((void**)&c->d_ring, c->ring, 0) != cudaSuccess)
       return fail(FP_ECUDA);
-    if (cudaMalloc(&c->d_slab, cfg.pack_bytes) != cudaSuccess) return fail(-ENOMEM);
+    // GDS doubles the slab: group g+1 is packed while group g is written
+    const size_t slab_bytes = (size_t)cfg.pack_bytes * (c->gds ? 2 : 1);
+    if (cudaMalloc(&c->d_slab, slab_bytes) != cudaSuccess) return fail(-ENOMEM);
+    if (c->gds) {
+      c->gds_slab_registered = gds_buf_register(c->d_slab, slab_bytes) == 0;  // best effort
+      c->gds_pool = gds_pool_new(std::min<uint32_t>(cfg.io_depth, 16));
+      const uint64_t G = cfg.pack_bytes / cfg.slot_bytes;
+      if (cudaHostAlloc(&c->h_gds_crc, 2 * (G + 1) * 4, cudaHostAllocPortable) != cudaSuccess)
+        return fail(-ENOMEM);
+      for (auto& e : c->gds_ev)
+        if (cudaEventCreate(&e) != cudaSuccess) return fail(FP_ECUDA);
+    }
     // The pack is short (a 256 MiB group is ~85 us of HBM time) and is what
     // feeds the ring: by default it runs at the GREATEST priority so its CTAs
     // are dispatched in the gaps of a saturating compute stream instead of
@@ -907,6 +946,11 @@ void fp_ckpt_destroy(fp_ctx* c) {
         if (e) cudaEventDestroy(e);
     if (c->ev_producer) cudaEventDestroy(c->ev_producer);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->gds_pool) gds_pool_delete(c->gds_pool);
+    for (cudaEvent_t e : c->gds_ev)
+      if (e) cudaEventDestroy(e);
+    if (c->h_gds_crc) cudaFreeHost(c->h_gds_crc);
+    if (c->gds_slab_registered) gds_buf_deregister(c->d_slab);
     if (c->d_slab) cudaFree(c->d_slab);
     if (c->d_items) cudaFree(c->d_items);
     if (c->d_crc_tab8) cudaFree(c->d_crc_tab8);

@@ -31,7 +31,7 @@ FP_TENSOR_HOST = 1
 FP_CFG_NO_FSYNC = 1
 FP_CFG_PRIO_LOW = 2
 FP_CFG_NO_CRC = 4
-IO_ENGINES = {"uring": 0, "pwrite": 1, "buffered": 2, "null": 3}
+IO_ENGINES = {"uring": 0, "pwrite": 1, "buffered": 2, "null": 3, "gds": 4}
 PACK_IMPLS = {"v4": 0, "bulk": 1, "host": 2, "ce": 3}
 SECTIONS = {"param": 0, "grad": 1, "master": 2, "exp_avg": 3, "exp_avg_sq": 4, "other": 5}
 DTYPES = {torch.float32: 1, torch.bfloat16: 2, torch.float16: 3, torch.float64: 4,

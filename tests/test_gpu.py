@@ -300,3 +300,28 @@ def test_load_read_ahead_ring_depths(tmp_path, slots, how):
         torch.cuda.synchronize()
     for (_, a), (_, b) in zip(st, dst):
         assert torch.equal(a.reshape(-1).view(torch.uint8), b.reshape(-1).view(torch.uint8))
+
+
+@pytest.mark.parametrize("cfg,slot,pack_bytes,pack", [("c1_tiny", 64 << 20, 256 << 20, "v4"),
+                                                      ("gpt3_odd", 1 << 20, 3 << 20, "v4"),
+                                                      ("gpt3_odd", 1 << 20, 1 << 20, "bulk"),
+                                                      ("moe_small", 4096, 8192, "v4")])
+def test_gds_engine_parity(tmp_path, cfg, slot, pack_bytes, pack):
+    """device slab -> cuFileWrite (GPUDirect Storage; compatibility
+    mode on a box without nvidia-fs): shard sha256 and CRC-32 == oracle, and
+    the shard loads back bit-exact."""
+    st = _state(cfg)
+    lay = oracle_layout([st], 1)
+    with fp.Checkpointer(DEV, io_engine="gds", slot_bytes=slot, pack_bytes=pack_bytes,
+                         pack=pack) as ck:
+        for _ in range(2):                       # second generation overwrites in place
+            s = ck.save(entries(st), str(tmp_path))
+        assert s["engine"] == 4 and s["pack_launches"] > 0
+        assert s["fallback"] in (0, 2)
+        _check_rank_files(str(tmp_path), lay, 1)
+        dst = [(x, torch.full_like(t, 5) if t.is_floating_point() else torch.zeros_like(t))
+               for x, t in st]
+        ck.load_parallel(entries(dst), str(tmp_path))
+        torch.cuda.synchronize()
+    for (_, a), (_, b) in zip(st, dst):
+        assert torch.equal(a.reshape(-1).view(torch.uint8), b.reshape(-1).view(torch.uint8))

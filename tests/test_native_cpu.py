@@ -452,3 +452,10 @@ def test_load_read_ahead_ring_depths_host(tmp_path, slots, engine, how):
         getattr(ck, how)(entries(dst), d)
     for (_, a), (_, b) in zip(st, dst):
         assert torch.equal(a.view(-1).view(torch.uint8), b.view(-1).view(torch.uint8))
+
+
+def test_gds_engine_needs_a_device():
+    """FP_IO_GDS moves device memory: a host-only context is refused."""
+    with pytest.raises(FastPersistError) as ei:
+        fp.Checkpointer(None, io_engine="gds")
+    assert ei.value.code == -22
