@@ -92,6 +92,21 @@ uint32_t crc_raw_update(uint32_t c, const uint8_t* p, uint64_t n) {
   return c;
 }
 
+// four 256-entry tables for the product by the constant k: M[i][b] = k*(b << 8i)
+static void mul_tables(uint32_t k, uint32_t* m) {
+  for (int i = 0; i < 4; ++i)
+    for (uint32_t b = 0; b < 256; ++b) m[256 * i + b] = gf_mul(k, b << (8 * i));
+}
+
+std::vector<uint32_t> crc_device_tables() {
+  init_tab();
+  std::vector<uint32_t> t(kTabWords, 0);
+  for (int k = 0; k < 4; ++k) memcpy(&t[kTabS4 + 256 * k], tab[k], 256 * 4);
+  for (int v = 0; v < 5; ++v) mul_tables(gf_x8n(128ull << v), &t[kTabLane + 1024 * v]);
+  for (uint32_t j = 0; j < kCrcPageLevels; ++j) mul_tables(gf_x8n(4096ull << j), &t[kTabPage + 1024 * j]);
+  return t;
+}
+
 uint32_t crc_zeros(uint64_t n) {  // standard CRC-32 of n zero bytes
   return gf_mul(gf_x8n(n), 0xFFFFFFFFu) ^ 0xFFFFFFFFu;
 }

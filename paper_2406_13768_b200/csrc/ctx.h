@@ -97,7 +97,7 @@ struct fp_ctx {
   int64_t fault_eio_at = -1;
   int fault_rank = -1;
   // CRC-32 of the shard
-  uint32_t *d_crc_tab8 = nullptr, *d_lane_k = nullptr, *d_x4k = nullptr;
+  uint32_t* d_crc_tabs = nullptr;  // crc_device_tables() blob
   uint32_t *d_page_crc = nullptr, *d_chunk_crc = nullptr, *h_crc = nullptr;
   IoEngine* io = nullptr;
   int pack_ctas = 0;

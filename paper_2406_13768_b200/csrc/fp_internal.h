@@ -153,10 +153,16 @@ int pack_default_ctas(int impl, int device);
 int flag_wait_launch(const uint32_t* d_flag, uint32_t value, uint64_t max_ns,
                      uint32_t* d_timed_out, void* stream);
 // raw CRC-32 of d_buf[0, bytes) per chunk_bytes chunk -> d_chunk_crc[]
-// (bytes, chunk_bytes: multiples of 4096; d_page_crc: bytes/4096 entries)
-int crc_launch(const uint8_t* d_buf, uint64_t bytes, uint64_t chunk_bytes, const uint32_t* d_tab8,
-               const uint32_t* d_lane_k, const uint32_t* d_x4k, uint32_t* d_page_crc,
-               uint32_t* d_chunk_crc, void* stream);
+// (bytes, chunk_bytes: multiples of 4096; d_page_crc: bytes/4096 entries of
+// scratch; d_tabs: the blob of crc_device_tables; chunk <= 2^29 pages / 1024)
+int crc_launch(const uint8_t* d_buf, uint64_t bytes, uint64_t chunk_bytes, const uint32_t* d_tabs,
+               uint32_t* d_page_crc, uint32_t* d_chunk_crc, void* stream);
+// device CRC table blob layout (uint32 offsets)
+constexpr uint32_t kCrcPageLevels = 20;
+constexpr uint32_t kTabS4 = 0;
+constexpr uint32_t kTabLane = 4 * 256;
+constexpr uint32_t kTabPage = kTabLane + 5 * 1024;
+constexpr uint32_t kTabWords = kTabPage + kCrcPageLevels * 1024;
 
 // ---------------------------------------------------------------------------
 // CRC-32 helpers (crc32.cpp)
@@ -166,5 +172,7 @@ uint32_t gf_x8n(uint64_t n);                      // x^(8n) mod P
 uint32_t crc_raw_update(uint32_t c, const uint8_t* p, uint64_t n);
 uint32_t crc_zeros(uint64_t n);                   // standard CRC-32 of n zero bytes
 const uint32_t* crc_tables8();                    // 8 x 256 slicing tables, contiguous
+// the kTabWords-word blob fp_crc_pages / fp_crc_fold read (layout: pack.cu)
+std::vector<uint32_t> crc_device_tables();
 
 }  // namespace fp

@@ -221,7 +221,7 @@ int fp_ctx::save_shard_gds(int fd, uint32_t* shard_raw) {
   const uint64_t G = std::max<uint64_t>(1, P / S);  // chunks per group
   const uint64_t NG = (C + G - 1) / G;
   const bool want_crc = !(cfg.flags & FP_CFG_NO_CRC);
-  const bool gpu_crc = want_crc && S % 4096 == 0 && d_crc_tab8;
+  const bool gpu_crc = want_crc && S % 4096 == 0 && d_crc_tabs;
   const uint64_t piece = std::max<uint64_t>(cfg.sqe_bytes, 4ull << 20);
   int status = 0;
   uint32_t raw = 0;
@@ -238,8 +238,8 @@ int fp_ctx::save_shard_gds(int fd, uint32_t* shard_raw) {
     CK(cudaEventRecord(gds_ev[3 * h + 1], stream));
     st.kernel_launches += 1;
     if (gpu_crc) {
-      rr = crc_launch(slab, round_up(gbytes, 4096), S, d_crc_tab8, d_lane_k, d_x4k, d_page_crc,
-                      d_chunk_crc, stream);
+      rr = crc_launch(slab, round_up(gbytes, 4096), S, d_crc_tabs, d_page_crc, d_chunk_crc,
+                      stream);
       if (rr) return rr;
       CK(cudaMemcpyAsync(h_gds_crc + (size_t)h * (G + 1), d_chunk_crc, (c1 - c0) * 4,
                          cudaMemcpyDeviceToHost, stream));

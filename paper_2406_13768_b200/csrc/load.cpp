@@ -731,7 +731,7 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
     uint8_t* slot = ra.slot_of(j);
     uint64_t foff = 0;
     const uint64_t mylen = my_span(j, &foff);
-    const bool gpu_crc = check_crc && dev && mylen % 4096 == 0 && c->d_crc_tab8;
+    const bool gpu_crc = check_crc && dev && mylen % 4096 == 0 && c->d_crc_tabs;
     uint8_t* sbuf = use_gds ? send + (j & 1) * CH : send;
     if (use_gds) {
       // the unpack of chunk j-2 read this half: wait for it, then read into it
@@ -762,8 +762,7 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
         cudaEventRecord(c->ev_d2h[s], st);
       }
       if (gpu_crc && mylen &&
-          (crc_launch(sbuf, mylen, mylen, c->d_crc_tab8, c->d_lane_k, c->d_x4k, c->d_page_crc,
-                      c->d_chunk_crc, st) ||
+          (crc_launch(sbuf, mylen, mylen, c->d_crc_tabs, c->d_page_crc, c->d_chunk_crc, st) ||
            cudaMemcpyAsync(&chunk_crc[j], c->d_chunk_crc, 4, cudaMemcpyDeviceToHost, st) !=
                cudaSuccess))
         status = status ? status : FP_ECUDA;

@@ -230,94 +230,103 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
 
 // ---------------------------------------------------------------------------
 // CRC-32 of the packed bytes, raw form (init 0, no xorout; see
-// crc32.cpp): fp_crc_pages gives one raw CRC per 4 KiB page (warp per page,
-// lane l owns bytes [128 l, 128 l + 128), slicing-by-8 from shared-memory
-// tables, lanes combined with x^(8*128*(31-l)) and a warp XOR), then
-// fp_crc_chunks folds the pages of each ring chunk into one raw CRC (Horner
-// over x^(8*4096) per thread, then x^(8*4096*pages_after) and a block XOR).
+// crc32.cpp). Two kernels, both table-driven (no bit-serial GF(2) products):
+//
+//  fp_crc_pages : one raw CRC per 4 KiB page. Warp per page, lane l owns bytes
+//                 [128 l, 128 l + 128): 8 x 16-B loads, then 32 slicing-by-4
+//                 steps whose lookups go to a per-lane copy of the tables
+//                 (entry e of table k at word (k*256 + e)*32 + lane, i.e. in
+//                 bank `lane`: conflict-free, 128 KiB), then the 32 lane CRCs
+//                 are combined in a shuffle tree, R(A||B) = R(A)*x^(8|B|) ^ R(B),
+//                 the constant product of level v (|B| = 128*2^v bytes) done
+//                 with four 256-entry tables.
+//  fp_crc_fold  : one raw CRC per chunk from its page CRCs. A block folds the
+//                 chunk padded at the FRONT to 1024*r pages (leading zeros are
+//                 invisible to a raw CRC): thread t runs Horner over r pages
+//                 (x^(8*4096) tables), then a 10-level tree over the block
+//                 (x^(8*4096*r*2^m) tables).
+//
+// Device table blob (uint32, built by crc_device_tables on the host):
+//   [kTabS4 .. +1024)   slicing-by-4 tables t[k][b] (b followed by k bytes)
+//   [kTabLane + 1024 v) product by x^(8*128*2^v),  v = 0..4
+//   [kTabPage + 1024 j) product by x^(8*4096*2^j), j = 0..19
+// each product table is four 256-entry tables: M[i][b] = K * (b << 8i).
 // ---------------------------------------------------------------------------
-constexpr uint32_t kCrcPoly = 0xEDB88320u;
+constexpr int kCrcThreads = 1024;
+constexpr size_t kCrcPagesSmem = (4 * 256 * 32 + 5 * 1024) * sizeof(uint32_t);  // 148 KiB
 
-__device__ __forceinline__ uint32_t gf_mul_d(uint32_t a, uint32_t b) {
-  uint32_t p = 0;
-#pragma unroll 1
-  for (int i = 31; i >= 0 && a; --i) {
-    if (a & (1u << i)) {
-      p ^= b;
-      a &= ~(1u << i);
-    }
-    b = (b & 1) ? (b >> 1) ^ kCrcPoly : b >> 1;
-  }
-  return p;
+__device__ __forceinline__ uint32_t mul_tab(const uint32_t* __restrict__ m, uint32_t a) {
+  return m[a & 255] ^ m[256 + ((a >> 8) & 255)] ^ m[512 + ((a >> 16) & 255)] ^ m[768 + (a >> 24)];
 }
 
-__global__ void __launch_bounds__(256) fp_crc_pages(const uint8_t* __restrict__ buf,
-                                                    uint32_t n_pages,
-                                                    const uint32_t* __restrict__ tab8,
-                                                    const uint32_t* __restrict__ lane_k,
-                                                    uint32_t* __restrict__ out) {
-  __shared__ uint32_t t[8][256];
-  __shared__ uint32_t kl[32];
-  for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) t[i >> 8][i & 255] = tab8[i];
-  if (threadIdx.x < 32) kl[threadIdx.x] = lane_k[threadIdx.x];
+__global__ void __launch_bounds__(kCrcThreads, 1)
+    fp_crc_pages(const uint8_t* __restrict__ buf, uint32_t n_pages,
+                 const uint32_t* __restrict__ tabs, uint32_t* __restrict__ out) {
+  extern __shared__ __align__(16) uint32_t crc_smem[];
+  uint32_t* rep = crc_smem;                    // [4][256][32] per-lane copies
+  uint32_t* lvl = crc_smem + 4 * 256 * 32;     // [5][4][256]
+  for (int i = threadIdx.x; i < 4 * 256 * 32; i += blockDim.x) rep[i] = tabs[kTabS4 + (i >> 5)];
+  for (int i = threadIdx.x; i < 5 * 1024; i += blockDim.x) lvl[i] = tabs[kTabLane + i];
   __syncthreads();
   const int lane = threadIdx.x & 31;
+  const uint32_t* r0 = rep + lane;                   // table 0, entry e at r0[e*32]
+  const uint32_t* r1 = rep + 256 * 32 + lane;
+  const uint32_t* r2 = rep + 2 * 256 * 32 + lane;
+  const uint32_t* r3 = rep + 3 * 256 * 32 + lane;
   const uint32_t wpb = blockDim.x >> 5;
   for (uint32_t pg = blockIdx.x * wpb + (threadIdx.x >> 5); pg < n_pages; pg += gridDim.x * wpb) {
     const uint4* src = reinterpret_cast<const uint4*>(buf + (size_t)pg * 4096 + lane * 128);
     uint4 v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = src[u];
+    for (int u = 0; u < 8; ++u) v[u] = __ldg(src + u);
     uint32_t c = 0;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      uint32_t lo = v[u].x ^ c, hi = v[u].y;
-      c = t[7][lo & 255] ^ t[6][(lo >> 8) & 255] ^ t[5][(lo >> 16) & 255] ^ t[4][lo >> 24] ^
-          t[3][hi & 255] ^ t[2][(hi >> 8) & 255] ^ t[1][(hi >> 16) & 255] ^ t[0][hi >> 24];
-      lo = v[u].z ^ c;
-      hi = v[u].w;
-      c = t[7][lo & 255] ^ t[6][(lo >> 8) & 255] ^ t[5][(lo >> 16) & 255] ^ t[4][lo >> 24] ^
-          t[3][hi & 255] ^ t[2][(hi >> 8) & 255] ^ t[1][(hi >> 16) & 255] ^ t[0][hi >> 24];
-    }
-    c = gf_mul_d(kl[lane], c);
+      const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
 #pragma unroll
-    for (int o = 16; o; o >>= 1) c ^= __shfl_xor_sync(0xffffffffu, c, o);
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t x = c ^ w[q];
+        c = r3[(x & 255) << 5] ^ r2[((x >> 8) & 255) << 5] ^ r1[((x >> 16) & 255) << 5] ^
+            r0[(x >> 24) << 5];
+      }
+    }
+#pragma unroll
+    for (int v2 = 0; v2 < 5; ++v2) {
+      const uint32_t o = __shfl_down_sync(0xffffffffu, c, 1 << v2);
+      if ((lane & ((2 << v2) - 1)) == 0) c = mul_tab(lvl + 1024 * v2, c) ^ o;
+    }
     if (lane == 0) out[pg] = c;
   }
 }
 
-// x^(8*4096*n) mod P from the table x4k[i] = x^(8*4096*2^i)
-__device__ __forceinline__ uint32_t x4k_pow(const uint32_t* x4k, uint32_t n) {
-  uint32_t p = 1u << 31;
-  for (int i = 0; n; ++i, n >>= 1)
-    if (n & 1) p = gf_mul_d(x4k[i], p);
-  return p;
-}
-
-__global__ void __launch_bounds__(256) fp_crc_chunks(const uint32_t* __restrict__ page_crc,
-                                                     uint32_t pages_per_chunk, uint32_t n_pages,
-                                                     const uint32_t* __restrict__ x4k_g,
-                                                     uint32_t* __restrict__ out) {
-  __shared__ uint32_t x4k[32];
-  __shared__ uint32_t red[8];
-  if (threadIdx.x < 32) x4k[threadIdx.x] = x4k_g[threadIdx.x];
+__global__ void __launch_bounds__(kCrcThreads)
+    fp_crc_fold(const uint32_t* __restrict__ page_crc, uint32_t pages_per_chunk, uint32_t n_pages,
+                uint32_t log2r, const uint32_t* __restrict__ tabs, uint32_t* __restrict__ out) {
+  __shared__ uint32_t k0[1024];        // x^(8*4096)
+  __shared__ uint32_t km[10][1024];    // x^(8*4096*2^(log2r+m))
+  __shared__ uint32_t red[kCrcThreads];
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) k0[i] = tabs[kTabPage + i];
+  for (int i = threadIdx.x; i < 10 * 1024; i += blockDim.x)
+    km[i >> 10][i & 1023] = tabs[kTabPage + 1024 * (log2r + (i >> 10)) + (i & 1023)];
   __syncthreads();
   const uint32_t p0 = blockIdx.x * pages_per_chunk;
-  const uint32_t p1 = min(p0 + pages_per_chunk, n_pages);
-  const uint32_t np = p1 - p0, per = (np + blockDim.x - 1) / blockDim.x;
-  const uint32_t b0 = min(np, threadIdx.x * per), b1 = min(np, b0 + per);
+  const uint32_t np = min(pages_per_chunk, n_pages - p0);
+  const uint32_t r = 1u << log2r;
+  const int64_t pad = (int64_t)kCrcThreads * r - np;  // zero pages in front
   uint32_t acc = 0;
-  for (uint32_t i = b0; i < b1; ++i) acc = gf_mul_d(x4k[0], acc) ^ page_crc[p0 + i];
-  if (b1 > b0 && b1 < np) acc = gf_mul_d(x4k_pow(x4k, np - b1), acc);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) acc ^= __shfl_xor_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t r = 0;
-    for (uint32_t w = 0; w < (blockDim.x >> 5); ++w) r ^= red[w];
-    out[blockIdx.x] = r;
+  for (uint32_t i = 0; i < r; ++i) {
+    const int64_t idx = (int64_t)threadIdx.x * r + i - pad;
+    acc = mul_tab(k0, acc) ^ (idx >= 0 ? page_crc[p0 + idx] : 0u);
   }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int m = 0; (1 << m) < kCrcThreads; ++m) {
+    const int step = 1 << m;
+    if ((threadIdx.x & (2 * step - 1)) == 0)
+      red[threadIdx.x] = mul_tab(km[m], red[threadIdx.x]) ^ red[threadIdx.x + step];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = red[0];
 }
 
 // ---------------------------------------------------------------------------
@@ -385,18 +394,29 @@ int flag_wait_launch(const uint32_t* d_flag, uint32_t value, uint64_t max_ns,
   return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
 }
 
-int crc_launch(const uint8_t* d_buf, uint64_t bytes, uint64_t chunk_bytes, const uint32_t* d_tab8,
-               const uint32_t* d_lane_k, const uint32_t* d_x4k, uint32_t* d_page_crc,
-               uint32_t* d_chunk_crc, void* stream) {
+int crc_launch(const uint8_t* d_buf, uint64_t bytes, uint64_t chunk_bytes, const uint32_t* d_tabs,
+               uint32_t* d_page_crc, uint32_t* d_chunk_crc, void* stream) {
   if (!bytes) return 0;
   if (bytes % 4096 || chunk_bytes % 4096) return -EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(fp_crc_pages, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kCrcPagesSmem) != cudaSuccess)
+      return FP_ECUDA;
+    attr_set = true;
+  }
   const uint32_t n_pages = (uint32_t)(bytes / 4096);
   const uint32_t ppc = (uint32_t)(chunk_bytes / 4096);
-  const int grid_p = (int)std::min<uint32_t>((n_pages + 7) / 8, (uint32_t)sm_count(-1) * 8);
-  fp_crc_pages<<<grid_p, 256, 0, st>>>(d_buf, n_pages, d_tab8, d_lane_k, d_page_crc);
+  const int grid_p = (int)std::min<uint32_t>((n_pages + 31) / 32, (uint32_t)sm_count(-1));
+  fp_crc_pages<<<grid_p, kCrcThreads, kCrcPagesSmem, st>>>(d_buf, n_pages, d_tabs, d_page_crc);
   const uint32_t n_chunks = (n_pages + ppc - 1) / ppc;
-  fp_crc_chunks<<<n_chunks, 256, 0, st>>>(d_page_crc, ppc, n_pages, d_x4k, d_chunk_crc);
+  const uint32_t per = std::min(ppc, n_pages);
+  uint32_t log2r = 0;
+  while (((uint64_t)kCrcThreads << log2r) < per) ++log2r;
+  if (log2r + 10 > kCrcPageLevels) return -EINVAL;
+  fp_crc_fold<<<n_chunks, kCrcThreads, 0, st>>>(d_page_crc, ppc, n_pages, log2r, d_tabs,
+                                                d_chunk_crc);
   return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
 }
 

@@ -182,7 +182,7 @@ int fp_ctx::save_shard() {
   // CRC: raw CRC per chunk (GPU: from the packed slab; otherwise the CPU over
   // the ring slot), folded in file order: R = R * x^(8 len) ^ R_chunk
   const bool want_crc = !(cfg.flags & FP_CFG_NO_CRC);
-  const bool gpu_crc = want_crc && !host && !slabless && S % 4096 == 0 && d_crc_tab8;
+  const bool gpu_crc = want_crc && !host && !slabless && S % 4096 == 0 && d_crc_tabs;
   uint32_t shard_raw = 0;
   auto stage = [&](uint64_t c) -> int {
     const uint32_t s = (uint32_t)(c % R);
@@ -251,8 +251,8 @@ int fp_ctx::save_shard() {
                         pack_ctas, stream);
       if (!r && cudaEventRecord(ev_p1[s], stream) != cudaSuccess) r = FP_ECUDA;
       if (!r && gpu_crc)
-        r = crc_launch(d_slab, round_up(gbytes, 4096), S, d_crc_tab8, d_lane_k, d_x4k,
-                       d_page_crc, d_chunk_crc, stream);
+        r = crc_launch(d_slab, round_up(gbytes, 4096), S, d_crc_tabs, d_page_crc, d_chunk_crc,
+                       stream);
       if (gated) __atomic_store_n(&h_sig[0], ++gate_seq, __ATOMIC_RELEASE);  // open the gate
       if (r) return r;
       has_pack[s] = 1;
@@ -780,23 +780,18 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
       // gate kernel to its timeout before the host could open it
       c->gate_on = !getenv("FP_NO_GATE") && !getenv("CUDA_INJECTION64_PATH");
     }
-    // CRC tables + scratch: slicing tables, lane multipliers x^(8*128*(31-l)),
-    // x^(8*4096*2^i), page CRCs of one pack group, chunk CRCs
+    // CRC tables (slicing + constant-product tables, crc_device_tables) and
+    // scratch: page CRCs of one pack group, chunk CRCs
     {
-      std::vector<uint32_t> k32(64);
-      for (int l = 0; l < 32; ++l) k32[l] = gf_x8n(128ull * (31 - l));
-      for (int i = 0; i < 32; ++i) k32[32 + i] = gf_x8n(4096ull << i);
+      const std::vector<uint32_t> tabs = crc_device_tables();
       const uint64_t pages = cfg.pack_bytes / 4096 + 1, chunks = cfg.pack_bytes / cfg.slot_bytes + 1;
-      if (cudaMalloc(&c->d_crc_tab8, 8 * 256 * 4 + 64 * 4) != cudaSuccess ||
+      if (cudaMalloc(&c->d_crc_tabs, tabs.size() * 4) != cudaSuccess ||
           cudaMalloc(&c->d_page_crc, pages * 4) != cudaSuccess ||
           cudaMalloc(&c->d_chunk_crc, chunks * 4) != cudaSuccess ||
           cudaHostAlloc(&c->h_crc, cfg.ring_slots * 4, cudaHostAllocPortable) != cudaSuccess)
         return fail(-ENOMEM);
-      c->d_lane_k = c->d_crc_tab8 + 8 * 256;
-      c->d_x4k = c->d_lane_k + 32;
-      if (cudaMemcpy(c->d_crc_tab8, crc_tables8(), 8 * 256 * 4, cudaMemcpyHostToDevice) !=
-              cudaSuccess ||
-          cudaMemcpy(c->d_lane_k, k32.data(), 64 * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+      if (cudaMemcpy(c->d_crc_tabs, tabs.data(), tabs.size() * 4, cudaMemcpyHostToDevice) !=
+          cudaSuccess)
         return fail(FP_ECUDA);
     }
     c->pack_ctas = cfg.pack_ctas ? (int)cfg.pack_ctas
@@ -953,7 +948,7 @@ void fp_ckpt_destroy(fp_ctx* c) {
     if (c->gds_slab_registered) gds_buf_deregister(c->d_slab);
     if (c->d_slab) cudaFree(c->d_slab);
     if (c->d_items) cudaFree(c->d_items);
-    if (c->d_crc_tab8) cudaFree(c->d_crc_tab8);
+    if (c->d_crc_tabs) cudaFree(c->d_crc_tabs);
     if (c->d_page_crc) cudaFree(c->d_page_crc);
     if (c->d_chunk_crc) cudaFree(c->d_chunk_crc);
     if (c->h_crc) cudaFreeHost(c->h_crc);
