@@ -42,7 +42,7 @@ std::string shard_file(int r, int k);
 // GPUDirect Storage (gds.cpp): libcufile loaded at run time
 class GdsPool;
 int gds_available(bool* p2p);  // 0 or -ENOSYS; *p2p: NVMe P2P (not compat mode)
-GdsPool* gds_pool_new(uint32_t threads);
+GdsPool* gds_pool_new(uint32_t threads, int device);
 void gds_pool_delete(GdsPool* p);
 int gds_buf_register(void* d, uint64_t bytes);
 void gds_buf_deregister(void* d);
@@ -120,6 +120,10 @@ struct fp_ctx {
   std::vector<uint32_t> run_lo;
   Item* d_items = nullptr;
   size_t d_items_cap = 0;
+  std::vector<uint32_t> tile_lo;          // fused pack + CRC: tiles of each pack group
+  std::vector<uint64_t> group_tile_off;
+  uint32_t* d_tiles = nullptr;
+  size_t d_tiles_cap = 0;
   uint8_t* d_hdr = nullptr;
   size_t d_hdr_cap = 0;
   std::vector<uint8_t> h_hdr;

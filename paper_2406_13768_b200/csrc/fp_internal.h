@@ -113,6 +113,13 @@ void plan_items(const Plan& p, uint64_t slot_bytes, uint64_t group_bytes,
                 std::vector<Item>* items, std::vector<uint32_t>* item_lo,
                 uint64_t max_item = kTile);
 
+// Per pack group: tile_lo[off_g + t] = first item (relative to the group's
+// first item) of 32 KiB slab tile t, t = 0..n_tiles_g (n_tiles_g + 1 entries
+// per group, groups concatenated; group_tile_off[g] = off_g).
+void plan_tiles(const std::vector<Item>& items, const std::vector<uint32_t>& item_lo,
+                uint64_t shard_bytes, uint64_t slot_bytes, uint64_t group_bytes,
+                std::vector<uint32_t>* tile_lo, std::vector<uint64_t>* group_tile_off);
+
 // ---------------------------------------------------------------------------
 // I/O engines
 // ---------------------------------------------------------------------------
@@ -157,6 +164,15 @@ int flag_wait_launch(const uint32_t* d_flag, uint32_t value, uint64_t max_ns,
 // scratch; d_tabs: the blob of crc_device_tables; chunk <= 2^29 pages / 1024)
 int crc_launch(const uint8_t* d_buf, uint64_t bytes, uint64_t chunk_bytes, const uint32_t* d_tabs,
                uint32_t* d_page_crc, uint32_t* d_chunk_crc, void* stream);
+// fused pack + page CRCs (fp_pack_crc): items of n_tiles 32 KiB slab tiles
+// (tile t = items [d_tile_lo[t], d_tile_lo[t+1]), none crossing a tile
+// boundary) -> d_slab, raw CRC of each of the first n_pages pages ->
+// d_page_crc; then crc_fold_launch folds them per chunk_bytes chunk
+int pack_crc_launch(const Item* d_items, const uint32_t* d_tile_lo, uint32_t n_tiles,
+                    uint8_t* d_slab, uint32_t n_pages, const uint32_t* d_tabs,
+                    uint32_t* d_page_crc, int ctas, void* stream);
+int crc_fold_launch(const uint32_t* d_page_crc, uint64_t bytes, uint64_t chunk_bytes,
+                    const uint32_t* d_tabs, uint32_t* d_chunk_crc, void* stream);
 // device CRC table blob layout (uint32 offsets)
 constexpr uint32_t kCrcPageLevels = 20;
 constexpr uint32_t kTabS4 = 0;

@@ -47,8 +47,18 @@ struct CuFileApi {
 
 CuFileApi g_api;
 std::once_flag g_once;
+bool g_dbg = getenv("FP_DEBUG_GDS") != nullptr;
+#define GDS_DBG(...)                                  \
+  do {                                                \
+    if (g_dbg) {                                      \
+      fprintf(stderr, "[fp gds %.6f] ", now_s());     \
+      fprintf(stderr, __VA_ARGS__);                   \
+      fputc('\n', stderr);                            \
+    }                                                 \
+  } while (0)
 
 void load_api() {
+  GDS_DBG("dlopen libcufile");
   void* h = dlopen("libcufile.so.0", RTLD_NOW | RTLD_GLOBAL);
   if (!h) h = dlopen("libcufile.so", RTLD_NOW | RTLD_GLOBAL);
   if (!h) return;
@@ -65,7 +75,9 @@ void load_api() {
   FP_SYM(Write, "cuFileWrite");
   FP_SYM(Read, "cuFileRead");
 #undef FP_SYM
+  GDS_DBG("cuFileDriverOpen");
   CUfileError_t e = g_api.DriverOpen();
+  GDS_DBG("cuFileDriverOpen -> %d", (int)e.err);
   if (e.err != CU_FILE_SUCCESS) {
     fprintf(stderr, "fastpersist: cuFileDriverOpen failed (%d)\n", (int)e.err);
     return;
@@ -74,6 +86,8 @@ void load_api() {
   memset(&props, 0, sizeof(props));
   if (g_api.DriverGetProperties(&props).err == CU_FILE_SUCCESS)
     g_api.p2p = (props.nvfs.dstatusflags & (1u << CU_FILE_NVME_SUPPORTED)) != 0;
+  GDS_DBG("props: nvfs %u.%u dstatus 0x%x dcontrol 0x%x p2p %d", props.nvfs.major_version,
+          props.nvfs.minor_version, props.nvfs.dstatusflags, props.nvfs.dcontrolflags, (int)g_api.p2p);
   g_api.ok = true;
 }
 
@@ -89,8 +103,12 @@ class GdsPool {
     void* base;
     uint64_t buf_off, file_off, len;
   };
-  explicit GdsPool(uint32_t n) {
-    for (uint32_t i = 0; i < std::max<uint32_t>(1, n); ++i) th_.emplace_back([this] { run(); });
+  GdsPool(uint32_t n, int device) {
+    for (uint32_t i = 0; i < std::max<uint32_t>(1, n); ++i)
+      th_.emplace_back([this, device] {
+        cudaSetDevice(device);  // libcufile stages through the calling thread's context
+        run();
+      });
   }
   ~GdsPool() {
     {
@@ -132,6 +150,8 @@ class GdsPool {
       }
       int e = 0;
       uint64_t done = 0;
+      GDS_DBG("%s fo=%llu len=%llu", j.write ? "write" : "read", (unsigned long long)j.file_off,
+              (unsigned long long)j.len);
       while (done < j.len && !e) {
         const ssize_t n = j.write ? g_api.Write(j.fh, j.base, j.len - done, (off_t)(j.file_off + done),
                                                 (off_t)(j.buf_off + done))
@@ -167,12 +187,15 @@ int gds_available(bool* p2p) {
   return g_api.ok ? 0 : -ENOSYS;
 }
 
-GdsPool* gds_pool_new(uint32_t threads) { return new GdsPool(threads); }
+GdsPool* gds_pool_new(uint32_t threads, int device) { return new GdsPool(threads, device); }
 void gds_pool_delete(GdsPool* p) { delete p; }
 
 int gds_buf_register(void* d, uint64_t bytes) {
   if (!g_api.ok) return -ENOSYS;
-  return g_api.BufRegister(d, bytes, 0).err == CU_FILE_SUCCESS ? 0 : -EIO;
+  GDS_DBG("cuFileBufRegister %p %llu", d, (unsigned long long)bytes);
+  const int r = g_api.BufRegister(d, bytes, 0).err == CU_FILE_SUCCESS ? 0 : -EIO;
+  GDS_DBG("cuFileBufRegister -> %d", r);
+  return r;
 }
 void gds_buf_deregister(void* d) {
   if (g_api.ok) g_api.BufDeregister(d);
@@ -185,7 +208,9 @@ int gds_handle_open(int fd, void** fh_out) {
   d.type = CU_FILE_HANDLE_TYPE_OPAQUE_FD;
   d.handle.fd = fd;
   CUfileHandle_t fh = nullptr;
+  GDS_DBG("cuFileHandleRegister fd=%d", fd);
   CUfileError_t e = g_api.HandleRegister(&fh, &d);
+  GDS_DBG("cuFileHandleRegister -> %d", (int)e.err);
   if (e.err != CU_FILE_SUCCESS) {
     fprintf(stderr, "fastpersist: cuFileHandleRegister failed (%d)\n", (int)e.err);
     return -EIO;
@@ -232,18 +257,27 @@ int fp_ctx::save_shard_gds(int fd, uint32_t* shard_raw) {
     uint8_t* slab = d_slab + (size_t)h * P;
     if (g == 0) CK(cudaStreamWaitEvent(stream, ev_producer, 0));
     CK(cudaEventRecord(gds_ev[3 * h], stream));
-    int rr = pack_launch(cfg.pack_impl == FP_PACK_BULK ? FP_PACK_BULK : FP_PACK_V4,
-                         d_items + item_lo[c0], item_lo[c1] - item_lo[c0], slab, pack_ctas, stream);
+    const bool fused = gpu_crc && cfg.pack_impl == FP_PACK_V4 && !getenv("FP_CRC_SEPARATE") &&
+                       !group_tile_off.empty();
+    int rr = fused ? pack_crc_launch(d_items + item_lo[c0], d_tiles + group_tile_off[g],
+                                     (uint32_t)((gbytes + kTile - 1) / kTile), slab,
+                                     (uint32_t)(round_up(gbytes, 4096) / 4096), d_crc_tabs,
+                                     d_page_crc, (int)cfg.pack_ctas, stream)
+                   : pack_launch(cfg.pack_impl == FP_PACK_BULK ? FP_PACK_BULK : FP_PACK_V4,
+                                 d_items + item_lo[c0], item_lo[c1] - item_lo[c0], slab,
+                                 pack_ctas, stream);
     if (rr) return rr;
     CK(cudaEventRecord(gds_ev[3 * h + 1], stream));
     st.kernel_launches += 1;
     if (gpu_crc) {
-      rr = crc_launch(slab, round_up(gbytes, 4096), S, d_crc_tabs, d_page_crc, d_chunk_crc,
-                      stream);
+      rr = fused ? crc_fold_launch(d_page_crc, round_up(gbytes, 4096), S, d_crc_tabs, d_chunk_crc,
+                                   stream)
+                 : crc_launch(slab, round_up(gbytes, 4096), S, d_crc_tabs, d_page_crc, d_chunk_crc,
+                              stream);
       if (rr) return rr;
       CK(cudaMemcpyAsync(h_gds_crc + (size_t)h * (G + 1), d_chunk_crc, (c1 - c0) * 4,
                          cudaMemcpyDeviceToHost, stream));
-      st.kernel_launches += 2;
+      st.kernel_launches += fused ? 1 : 2;
     }
     CK(cudaEventRecord(gds_ev[3 * h + 2], stream));
     ++st.pack_launches;
@@ -259,6 +293,7 @@ int fp_ctx::save_shard_gds(int fd, uint32_t* shard_raw) {
       status = enqueue(g + 1);
       if (status) break;
     }
+    GDS_DBG("group %llu/%llu: wait pack", (unsigned long long)g, (unsigned long long)NG);
     if (cudaEventSynchronize(gds_ev[3 * h + 2]) != cudaSuccess) {
       status = FP_ECUDA;
       break;
@@ -291,6 +326,7 @@ int fp_ctx::save_shard_gds(int fd, uint32_t* shard_raw) {
     st.io_requests += (gbytes + piece - 1) / piece;
     st.chunks += c1 - c0;
     status = gds_wait(gds_pool, &st.t_io_stall);
+    GDS_DBG("group %llu written: %d", (unsigned long long)g, status);
   }
   cudaStreamSynchronize(stream);  // never leave a pack writing into the slab
   gds_handle_close(fh);

@@ -302,8 +302,11 @@ void plan_items(const Plan& p, uint64_t slot_bytes, uint64_t group_bytes,
         ++chunk;
       }
       const uint64_t cend = (chunk + 1) * slot_bytes;
-      const uint64_t n = std::min<uint64_t>({left, max_item, cend - fo});
       const uint64_t gbase = chunk / per_group * per_group * slot_bytes;
+      uint64_t n = std::min<uint64_t>({left, max_item, cend - fo});
+      // tile-sized items never cross a kTile boundary of their group (the
+      // fused pack + CRC kernel works on whole tiles)
+      if (max_item <= kTile) n = std::min<uint64_t>(n, kTile - (fo - gbase) % kTile);
       items->push_back({src, (uint32_t)(fo - gbase), (uint32_t)n});
       fo += n;
       left -= n;
@@ -311,6 +314,27 @@ void plan_items(const Plan& p, uint64_t slot_bytes, uint64_t group_bytes,
     }
   }
   while (item_lo->size() < n_chunks + 1) item_lo->push_back((uint32_t)items->size());
+}
+
+void plan_tiles(const std::vector<Item>& items, const std::vector<uint32_t>& item_lo,
+                uint64_t shard_bytes, uint64_t slot_bytes, uint64_t group_bytes,
+                std::vector<uint32_t>* tile_lo, std::vector<uint64_t>* group_tile_off) {
+  const uint64_t per_group = std::max<uint64_t>(1, group_bytes / slot_bytes);
+  const uint64_t n_chunks = item_lo.size() - 1;
+  tile_lo->clear();
+  group_tile_off->clear();
+  for (uint64_t c0 = 0; c0 < n_chunks; c0 += per_group) {
+    const uint64_t c1 = std::min(c0 + per_group, n_chunks);
+    const uint64_t gbytes = std::min(c1 * slot_bytes, shard_bytes) - c0 * slot_bytes;
+    const uint64_t nt = (gbytes + kTile - 1) / kTile;
+    group_tile_off->push_back(tile_lo->size());
+    const uint32_t i0 = item_lo[c0], i1 = item_lo[c1];
+    uint32_t i = i0;
+    for (uint64_t t = 0; t <= nt; ++t) {  // first item whose dst >= t * kTile
+      while (i < i1 && items[i].dst < t * kTile) ++i;
+      tile_lo->push_back(i - i0);
+    }
+  }
 }
 
 }  // namespace fp

@@ -330,6 +330,166 @@ __global__ void __launch_bounds__(kCrcThreads)
 }
 
 // ---------------------------------------------------------------------------
+// fp_pack_crc: the pack and the page CRCs in ONE pass over the data (the
+// separate fp_crc_pages re-reads the whole slab from HBM). Work unit: one
+// 32 KiB tile of the slab (8 pages); items never cross a tile boundary and
+// tile_lo[t] is the first item of tile t. Warp-specialised CTA of 512
+// threads, one per SM (the per-lane CRC tables take 148 KiB of shared memory):
+//   warps 0-7  (producers): gather the tile's items src -> slab exactly as
+//              fp_pack_v4 does, and store the same bytes into a shared-memory
+//              staging tile (double buffered, 16-B chunks XOR-swizzled so both
+//              the producers' coalesced stores and the consumers' per-lane
+//              128-B reads are free of bank conflicts);
+//   warps 8-15 (consumers): CRC of page w of the staged tile from shared
+//              memory, as fp_crc_pages computes it from global memory.
+// Hand-off through named barriers: FULL[b] (producers arrive, consumers sync)
+// and EMPTY[b] (consumers arrive, producers sync before refilling b).
+// ---------------------------------------------------------------------------
+constexpr int kPcThreads = 512;
+constexpr int kPcProducers = 256;
+constexpr size_t kPcTabWords = 4 * 256 * 32 + 5 * 1024;
+constexpr size_t kPcSmem = kPcTabWords * 4 + 2 * (size_t)kTile;  // 212 KiB
+
+__device__ __forceinline__ uint32_t stage_off(uint32_t off) {  // swizzled byte offset
+  const uint32_t c = off >> 4;
+  return ((c ^ ((c >> 3) & 7)) << 4) | (off & 15);
+}
+__device__ __forceinline__ void bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// copy_bytes + the same bytes into the staging tile at `soff` (tile offset)
+__device__ __forceinline__ void copy_stage(uint8_t* __restrict__ dst,
+                                           const uint8_t* __restrict__ src, uint32_t len,
+                                           uint8_t* __restrict__ stage, uint32_t soff, int t,
+                                           int nthr) {
+  const uint32_t phase = (uint32_t)((uintptr_t)dst & 15);
+  const bool coaligned = !src || (((uintptr_t)src & 15) == phase) ;
+  if (!coaligned || ((soff ^ phase) & 15)) {
+    for (uint32_t i = t; i < len; i += nthr) {
+      const uint8_t b = src[i];
+      dst[i] = b;
+      stage[stage_off(soff + i)] = b;
+    }
+    return;
+  }
+  uint32_t head = (16 - phase) & 15;
+  if (head > len) head = len;
+  if ((uint32_t)t < head) {
+    const uint8_t b = src ? src[t] : 0;
+    dst[t] = b;
+    stage[stage_off(soff + t)] = b;
+  }
+  const uint32_t n16 = (len - head) >> 4;
+  uint4* d16 = reinterpret_cast<uint4*>(dst + head);
+  const uint32_t s0 = soff + head;  // 16-B aligned
+  if (src) {
+    const uint4* s16 = reinterpret_cast<const uint4*>(src + head);
+    for (uint32_t base = 0; base < n16; base += (uint32_t)nthr * kV4Unroll) {
+      uint4 v[kV4Unroll];
+#pragma unroll
+      for (int u = 0; u < kV4Unroll; ++u) {
+        const uint32_t j = base + (uint32_t)u * nthr + t;
+        if (j < n16) v[u] = ld_stream(s16 + j);
+      }
+#pragma unroll
+      for (int u = 0; u < kV4Unroll; ++u) {
+        const uint32_t j = base + (uint32_t)u * nthr + t;
+        if (j < n16) {
+          st_v4(d16 + j, v[u]);
+          *reinterpret_cast<uint4*>(stage + stage_off(s0 + 16 * j)) = v[u];
+        }
+      }
+    }
+  } else {
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    for (uint32_t j = t; j < n16; j += nthr) {
+      st_v4(d16 + j, z);
+      *reinterpret_cast<uint4*>(stage + stage_off(s0 + 16 * j)) = z;
+    }
+  }
+  const uint32_t done = head + (n16 << 4);
+  const uint32_t tail = len - done;
+  if ((uint32_t)t < tail) {
+    const uint8_t b = src ? src[done + t] : 0;
+    dst[done + t] = b;
+    stage[stage_off(soff + done + t)] = b;
+  }
+}
+
+__global__ void __launch_bounds__(kPcThreads, 1)
+    fp_pack_crc(const Item* __restrict__ items, const uint32_t* __restrict__ tile_lo,
+                uint32_t n_tiles, uint8_t* __restrict__ slab, uint32_t n_pages,
+                const uint32_t* __restrict__ tabs, uint32_t* __restrict__ page_crc) {
+  extern __shared__ __align__(16) uint32_t pc_smem[];
+  uint32_t* rep = pc_smem;                    // [4][256][32] per-lane copies
+  uint32_t* lvl = pc_smem + 4 * 256 * 32;     // [5][4][256]
+  uint8_t* stage0 = reinterpret_cast<uint8_t*>(pc_smem + kPcTabWords);
+  for (int i = threadIdx.x; i < 4 * 256 * 32; i += blockDim.x) rep[i] = tabs[kTabS4 + (i >> 5)];
+  for (int i = threadIdx.x; i < 5 * 1024; i += blockDim.x) lvl[i] = tabs[kTabLane + i];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < kPcProducers / 32) {
+    const int t = threadIdx.x;
+    uint32_t k = 0;
+    for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
+      const int b = (int)(k & 1);
+      if (k >= 2) bar_sync(3 + b, kPcThreads);  // EMPTY[b]
+      uint8_t* stage = stage0 + (size_t)b * kTile;
+      const uint32_t base = tile * kTile;
+      for (uint32_t i = tile_lo[tile]; i < tile_lo[tile + 1]; ++i) {
+        const Item it = items[i];
+        copy_stage(slab + it.dst, reinterpret_cast<const uint8_t*>(it.src), it.len, stage,
+                   it.dst - base, t, kPcProducers);
+      }
+      bar_arrive(1 + b, kPcThreads);  // FULL[b]
+    }
+    // consume the consumers' last EMPTY arrivals (barrier state must balance)
+    for (uint32_t j = (k >= 2 ? k - 2 : 0); j < k; ++j) bar_sync(3 + (int)(j & 1), kPcThreads);
+  } else {
+    const int w = warp - kPcProducers / 32;  // page of the tile
+    const uint32_t* r0 = rep + lane;
+    const uint32_t* r1 = rep + 256 * 32 + lane;
+    const uint32_t* r2 = rep + 2 * 256 * 32 + lane;
+    const uint32_t* r3 = rep + 3 * 256 * 32 + lane;
+    uint32_t k = 0;
+    for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
+      const int b = (int)(k & 1);
+      bar_sync(1 + b, kPcThreads);  // FULL[b]
+      const uint8_t* stage = stage0 + (size_t)b * kTile;
+      const uint32_t pg = tile * (kTile / 4096) + (uint32_t)w;
+      uint32_t c = 0;
+      if (pg < n_pages) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint4 v = *reinterpret_cast<const uint4*>(
+              stage + stage_off((uint32_t)w * 4096 + (uint32_t)lane * 128 + 16 * u));
+          const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t x = c ^ wd[q];
+            c = r3[(x & 255) << 5] ^ r2[((x >> 8) & 255) << 5] ^ r1[((x >> 16) & 255) << 5] ^
+                r0[(x >> 24) << 5];
+          }
+        }
+      }
+      bar_arrive(3 + b, kPcThreads);  // EMPTY[b]: staging read, registers hold the rest
+      if (pg < n_pages) {
+#pragma unroll
+        for (int v2 = 0; v2 < 5; ++v2) {
+          const uint32_t o = __shfl_down_sync(0xffffffffu, c, 1 << v2);
+          if ((lane & ((2 << v2) - 1)) == 0) c = mul_tab(lvl + 1024 * v2, c) ^ o;
+        }
+        if (lane == 0) page_crc[pg] = c;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host -> GPU signal: one warp spins (acquire loads at system scope, so the
 // host's store to the mapped pinned word is observed) until the word reaches
 // `value` (cyclic >=); gives up after max_ns and then sets *timed_out.
@@ -417,6 +577,41 @@ int crc_launch(const uint8_t* d_buf, uint64_t bytes, uint64_t chunk_bytes, const
   if (log2r + 10 > kCrcPageLevels) return -EINVAL;
   fp_crc_fold<<<n_chunks, kCrcThreads, 0, st>>>(d_page_crc, ppc, n_pages, log2r, d_tabs,
                                                 d_chunk_crc);
+  return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
+}
+
+int pack_crc_launch(const Item* d_items, const uint32_t* d_tile_lo, uint32_t n_tiles,
+                    uint8_t* d_slab, uint32_t n_pages, const uint32_t* d_tabs,
+                    uint32_t* d_page_crc, int ctas, void* stream) {
+  if (!n_tiles) return 0;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(fp_pack_crc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kPcSmem) != cudaSuccess)
+      return FP_ECUDA;
+    attr_set = true;
+  }
+  const int sms = sm_count(-1);
+  const int grid = (int)std::min<uint32_t>(n_tiles, (uint32_t)std::min(ctas > 0 ? ctas : sms, sms));
+  fp_pack_crc<<<grid, kPcThreads, kPcSmem, (cudaStream_t)stream>>>(d_items, d_tile_lo, n_tiles,
+                                                                  d_slab, n_pages, d_tabs,
+                                                                  d_page_crc);
+  return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
+}
+
+int crc_fold_launch(const uint32_t* d_page_crc, uint64_t bytes, uint64_t chunk_bytes,
+                    const uint32_t* d_tabs, uint32_t* d_chunk_crc, void* stream) {
+  if (!bytes) return 0;
+  if (bytes % 4096 || chunk_bytes % 4096) return -EINVAL;
+  const uint32_t n_pages = (uint32_t)(bytes / 4096);
+  const uint32_t ppc = (uint32_t)(chunk_bytes / 4096);
+  const uint32_t n_chunks = (n_pages + ppc - 1) / ppc;
+  const uint32_t per = std::min(ppc, n_pages);
+  uint32_t log2r = 0;
+  while (((uint64_t)kCrcThreads << log2r) < per) ++log2r;
+  if (log2r + 10 > kCrcPageLevels) return -EINVAL;
+  fp_crc_fold<<<n_chunks, kCrcThreads, 0, (cudaStream_t)stream>>>(d_page_crc, ppc, n_pages, log2r,
+                                                                  d_tabs, d_chunk_crc);
   return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
 }
 

@@ -184,6 +184,10 @@ int fp_ctx::save_shard() {
   const bool want_crc = !(cfg.flags & FP_CFG_NO_CRC);
   const bool gpu_crc = want_crc && !host && !slabless && S % 4096 == 0 && d_crc_tabs;
   uint32_t shard_raw = 0;
+  // default: the CRC pages are computed inside the pack (fp_pack_crc);
+  // FP_CRC_SEPARATE=1 keeps fp_pack_v4 + fp_crc_pages (ablation)
+  const bool fused = gpu_crc && cfg.pack_impl == FP_PACK_V4 && !getenv("FP_CRC_SEPARATE") &&
+                     !group_tile_off.empty();
   auto stage = [&](uint64_t c) -> int {
     const uint32_t s = (uint32_t)(c % R);
     const uint64_t len = std::min<uint64_t>(S, plan.shard_bytes - c * S);
@@ -242,17 +246,24 @@ int fp_ctx::save_shard() {
         gate_on = gated = false;  // could not launch the gate: run ungated from now on
         cudaGetLastError();
       }
-      st.kernel_launches += (gated ? 1 : 0) + 1 + (gpu_crc ? 2 : 0);
+      st.kernel_launches += (gated ? 1 : 0) + 1 + (gpu_crc ? (fused ? 1 : 2) : 0);
       // the gate is opened on every path out of this block: a stream left
       // waiting on it would never drain
       int r = cudaEventRecord(ev_p0[s], stream) == cudaSuccess ? 0 : FP_ECUDA;
-      if (!r)
+      if (!r && fused)  // pack + page CRCs in one pass over the data
+        r = pack_crc_launch(d_items + item_lo[c], d_tiles + group_tile_off[c / G],
+                            (uint32_t)((gbytes + kTile - 1) / kTile), d_slab,
+                            (uint32_t)(round_up(gbytes, 4096) / 4096), d_crc_tabs, d_page_crc,
+                            (int)cfg.pack_ctas, stream);
+      else if (!r)
         r = pack_launch(cfg.pack_impl, d_items + item_lo[c], item_lo[c1] - item_lo[c], d_slab,
                         pack_ctas, stream);
       if (!r && cudaEventRecord(ev_p1[s], stream) != cudaSuccess) r = FP_ECUDA;
       if (!r && gpu_crc)
-        r = crc_launch(d_slab, round_up(gbytes, 4096), S, d_crc_tabs, d_page_crc, d_chunk_crc,
-                       stream);
+        r = fused ? crc_fold_launch(d_page_crc, round_up(gbytes, 4096), S, d_crc_tabs,
+                                    d_chunk_crc, stream)
+                  : crc_launch(d_slab, round_up(gbytes, 4096), S, d_crc_tabs, d_page_crc,
+                               d_chunk_crc, stream);
       if (gated) __atomic_store_n(&h_sig[0], ++gate_seq, __ATOMIC_RELEASE);  // open the gate
       if (r) return r;
       has_pack[s] = 1;
@@ -559,10 +570,27 @@ int fp::build_items(fp_ctx* c, bool for_save) {
     plan_items(c->plan, c->cfg.slot_bytes, c->cfg.slot_bytes, &c->runs, &c->run_lo,
                c->cfg.slot_bytes);
   }
+  c->tile_lo.clear();
+  c->group_tile_off.clear();
+  if (!c->host && c->dev >= 0 && !slabless && !c->items.empty()) {
+    // 32 KiB slab tiles of each pack group for the fused pack + CRC kernel
+    plan_tiles(c->items, c->item_lo, c->plan.shard_bytes, c->cfg.slot_bytes, c->cfg.pack_bytes,
+               &c->tile_lo, &c->group_tile_off);
+    const size_t need = c->tile_lo.size() * sizeof(uint32_t);
+    if (c->d_tiles_cap < need) {
+      if (c->d_tiles) cudaFree(c->d_tiles);
+      c->d_tiles = nullptr;
+      c->d_tiles_cap = 0;
+      CK(cudaMalloc(&c->d_tiles, need));
+      c->d_tiles_cap = need;
+    }
+    CK(cudaMemcpyAsync(c->d_tiles, c->tile_lo.data(), need, cudaMemcpyHostToDevice, c->stream));
+  }
   if (!c->host && c->dev >= 0 && !c->items.empty()) {
     const size_t need = c->items.size() * sizeof(Item);
     if (c->d_items_cap < need) {
       if (c->d_items) cudaFree(c->d_items);
+    if (c->d_tiles) cudaFree(c->d_tiles);
       c->d_items = nullptr;
       c->d_items_cap = 0;
       CK(cudaMalloc(&c->d_items, need));
@@ -735,7 +763,7 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
     if (cudaMalloc(&c->d_slab, slab_bytes) != cudaSuccess) return fail(-ENOMEM);
     if (c->gds) {
       c->gds_slab_registered = gds_buf_register(c->d_slab, slab_bytes) == 0;  // best effort
-      c->gds_pool = gds_pool_new(std::min<uint32_t>(cfg.io_depth, 16));
+      c->gds_pool = gds_pool_new(std::min<uint32_t>(cfg.io_depth, 16), cuda_device);
       const uint64_t G = cfg.pack_bytes / cfg.slot_bytes;
       if (cudaHostAlloc(&c->h_gds_crc, 2 * (G + 1) * 4, cudaHostAllocPortable) != cudaSuccess)
         return fail(-ENOMEM);
@@ -948,6 +976,7 @@ void fp_ckpt_destroy(fp_ctx* c) {
     if (c->gds_slab_registered) gds_buf_deregister(c->d_slab);
     if (c->d_slab) cudaFree(c->d_slab);
     if (c->d_items) cudaFree(c->d_items);
+    if (c->d_tiles) cudaFree(c->d_tiles);
     if (c->d_crc_tabs) cudaFree(c->d_crc_tabs);
     if (c->d_page_crc) cudaFree(c->d_page_crc);
     if (c->d_chunk_crc) cudaFree(c->d_chunk_crc);
