@@ -532,7 +532,11 @@ def our_arm(a):
 
     if rank == 0:
         hbm = float(peaks["hbm_gbs"])
-        kname = {"v4": "fp_pack_v4", "bulk": "fp_pack_bulk"}.get(a.pack)
+        # v4 with the shard CRC (default) runs the fused pack + page-CRC kernel
+        fused = a.pack == "v4" and not os.environ.get("FP_CRC_SEPARATE") \
+            and not os.environ.get("FP_NO_CRC")
+        kname = {"v4": "fp_pack_crc" if fused else "fp_pack_v4",
+                 "bulk": "fp_pack_bulk", "host": "fp_pack_v4 (to mapped host)"}.get(a.pack)
         traffic = a.traffic
         try:   # ncu-measured DRAM bytes per launch of this launch shape (profiles/)
             with open(os.path.join(ROOT, "profiles", "pack_traffic.json")) as f:
@@ -559,8 +563,7 @@ def our_arm(a):
                        "dir": root},
             "latency_s": {"median": round(statistics.median(lat_max), 4),
                           "min": round(min(lat_max), 4), "max": round(max(lat_max), 4)},
-            "roofline": {"bound": "hbm", "kernel": {"v4": "fp_pack_v4", "bulk": "fp_pack_bulk",
-                                    "host": "fp_pack_v4 (to mapped host)", "ce": None}[a.pack],
+            "roofline": {"bound": "hbm", "kernel": kname,
                          "achieved": round(pack_gbs, 1), "peak": hbm, "unit": "GB/s",
                          "frac": round(pack_gbs / hbm, 4), "traffic": traffic,
                          "peak_source": peak_src, "launch_avg_ms": round(launch_avg_ms, 5),

@@ -590,7 +590,6 @@ int fp::build_items(fp_ctx* c, bool for_save) {
     const size_t need = c->items.size() * sizeof(Item);
     if (c->d_items_cap < need) {
       if (c->d_items) cudaFree(c->d_items);
-    if (c->d_tiles) cudaFree(c->d_tiles);
       c->d_items = nullptr;
       c->d_items_cap = 0;
       CK(cudaMalloc(&c->d_items, need));
