@@ -7,6 +7,10 @@ import faulthandler; faulthandler.dump_traceback_later(120, exit=True)
 import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke10.log 2>&1
 rc=$?; echo "smoke exit $rc" >> gpurun_out/smoke10.log
 if [ $rc -ne 0 ]; then cat gpurun_out/smoke10.log; exit 1; fi
+FP_NO_GATE=1 timeout 600 compute-sanitizer --tool racecheck --print-limit 10 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/racecheck10.log 2>&1
+echo "racecheck exit $?" >> gpurun_out/racecheck10.log
+FP_NO_GATE=1 timeout 600 compute-sanitizer --tool synccheck --print-limit 10 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/synccheck10.log 2>&1
+echo "synccheck exit $?" >> gpurun_out/synccheck10.log
 timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider -k "not gds" > gpurun_out/pytest_gpu10.log 2>&1
 echo "pytest exit $?" >> gpurun_out/pytest_gpu10.log
 FP_DEBUG_GDS=1 CUFILE_ENV_PATH_JSON=$PWD/tools/diag/cufile_trace.json timeout -s KILL 120 python tools/diag/gds_diag.py > gpurun_out/gds_diag10.log 2>&1
@@ -22,5 +26,5 @@ FP_NO_GATE=1 timeout 400 ncu --set full --clock-control none --import-source on 
    -o gpurun_out/pc10 -f python tools/ncu_pack.py > gpurun_out/ncu_pc10.log 2>&1
 timeout 900 python bench.py --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench10.json 2> gpurun_out/bench10.err
 echo "bench exit $?" >> gpurun_out/bench10.err
-tail -5 gpurun_out/pytest_gpu10.log; cat gpurun_out/smoke10.log; tail -25 gpurun_out/gds_diag10.log; tail -12 gpurun_out/gds_diag10_compat.log
+tail -4 gpurun_out/racecheck10.log gpurun_out/synccheck10.log; tail -5 gpurun_out/pytest_gpu10.log; cat gpurun_out/smoke10.log; tail -25 gpurun_out/gds_diag10.log; tail -12 gpurun_out/gds_diag10_compat.log
 cat gpurun_out/bench10.json; tail -3 gpurun_out/bench10.err gpurun_out/ncu_bench10.log gpurun_out/ncu_pc10.log
