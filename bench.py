@@ -532,8 +532,8 @@ def our_arm(a):
 
     if rank == 0:
         hbm = float(peaks["hbm_gbs"])
-        # v4 with the shard CRC (default) runs the fused pack + page-CRC kernel
-        fused = a.pack == "v4" and not os.environ.get("FP_CRC_SEPARATE") \
+        # FP_CRC_FUSED=1 (ablation) runs the fused pack + page-CRC kernel
+        fused = a.pack == "v4" and bool(os.environ.get("FP_CRC_FUSED")) \
             and not os.environ.get("FP_NO_CRC")
         kname = {"v4": "fp_pack_crc" if fused else "fp_pack_v4",
                  "bulk": "fp_pack_bulk", "host": "fp_pack_v4 (to mapped host)"}.get(a.pack)

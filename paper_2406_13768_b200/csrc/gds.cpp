@@ -21,7 +21,9 @@
 
 #include <algorithm>
 #include <cerrno>
+#include <chrono>
 #include <condition_variable>
+#include <memory>
 #include <deque>
 #include <mutex>
 #include <thread>
@@ -75,8 +77,38 @@ void load_api() {
   FP_SYM(Write, "cuFileWrite");
   FP_SYM(Read, "cuFileRead");
 #undef FP_SYM
+  // cuFileDriverOpen can block indefinitely on a host without nvidia-fs (seen
+  // on the gpurun B200 boxes, compatibility mode forced or not): it runs on
+  // a detached thread and is abandoned after FP_GDS_OPEN_TIMEOUT seconds
+  // (default 20), which makes FP_IO_GDS unavailable (-ENOSYS) instead of
+  // hanging the caller.
   GDS_DBG("cuFileDriverOpen");
-  CUfileError_t e = g_api.DriverOpen();
+  struct OpenState {
+    std::mutex mu;
+    std::condition_variable cv;
+    bool done = false;
+    CUfileError_t e;
+  };
+  auto os = std::make_shared<OpenState>();
+  auto open_fn = g_api.DriverOpen;
+  std::thread([os, open_fn] {
+    CUfileError_t e = open_fn();
+    std::lock_guard<std::mutex> g(os->mu);
+    os->e = e;
+    os->done = true;
+    os->cv.notify_all();
+  }).detach();
+  const double tmo = (double)env_u64("FP_GDS_OPEN_TIMEOUT", 20);
+  CUfileError_t e;
+  {
+    std::unique_lock<std::mutex> g(os->mu);
+    if (!os->cv.wait_for(g, std::chrono::duration<double>(tmo), [&] { return os->done; })) {
+      fprintf(stderr, "fastpersist: cuFileDriverOpen did not return within %.0f s "
+                      "(no nvidia-fs / GDS on this host?); FP_IO_GDS unavailable\n", tmo);
+      return;
+    }
+    e = os->e;
+  }
   GDS_DBG("cuFileDriverOpen -> %d", (int)e.err);
   if (e.err != CU_FILE_SUCCESS) {
     fprintf(stderr, "fastpersist: cuFileDriverOpen failed (%d)\n", (int)e.err);
@@ -257,7 +289,7 @@ int fp_ctx::save_shard_gds(int fd, uint32_t* shard_raw) {
     uint8_t* slab = d_slab + (size_t)h * P;
     if (g == 0) CK(cudaStreamWaitEvent(stream, ev_producer, 0));
     CK(cudaEventRecord(gds_ev[3 * h], stream));
-    const bool fused = gpu_crc && cfg.pack_impl == FP_PACK_V4 && !getenv("FP_CRC_SEPARATE") &&
+    const bool fused = gpu_crc && cfg.pack_impl == FP_PACK_V4 && getenv("FP_CRC_FUSED") &&
                        !group_tile_off.empty();
     int rr = fused ? pack_crc_launch(d_items + item_lo[c0], d_tiles + group_tile_off[g],
                                      (uint32_t)((gbytes + kTile - 1) / kTile), slab,

@@ -21,6 +21,7 @@
 //                 cp.async.bulk (S2G, bulk_group); the other warps handle
 //                 zero fill, vector tails and misaligned items with the LSU.
 //  fp_unpack_v4 : load path, slab -> tensors (zero items skipped).
+#include <cuda.h>  // CUtensorMap (the encode entry point is fetched at run time)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -299,6 +300,97 @@ __global__ void __launch_bounds__(kCrcThreads, 1)
   }
 }
 
+// fp_crc_pages_tma: fp_crc_pages with the page bytes brought into shared
+// memory by the TMA engine instead of 8 LSU loads per lane (each of which
+// touched 32 different 128-B lines: the L1/TEX pipe was the limiter). The slab
+// is a 2-D tensor map of 128-B rows with 128-B swizzling; one box = one 4 KiB
+// page = 32 rows, so lane l's run (row l) lands with its 16-B chunk u at
+// chunk u ^ (l & 7): the per-lane LDS.128 reads are conflict-free. Each warp
+// streams its own pages through 2 stages (lane 0 issues, mbarrier
+// complete_tx); no cross-warp synchronisation.
+constexpr int kCtWarps = 8;
+constexpr int kCtStages = 2;  // per warp
+constexpr size_t kCtSmem = 1024 + (size_t)kCtWarps * kCtStages * 4096 +
+                           (4 * 256 * 32 + 5 * 1024) * sizeof(uint32_t) +
+                           (size_t)kCtWarps * kCtStages * 8;
+
+__global__ void __launch_bounds__(kCtWarps * 32, 1)
+    fp_crc_pages_tma(const __grid_constant__ CUtensorMap tmap, uint32_t n_pages,
+                     const uint32_t* __restrict__ tabs, uint32_t* __restrict__ out) {
+  extern __shared__ uint8_t ct_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>(((uintptr_t)ct_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* stages = base;
+  uint32_t* rep = reinterpret_cast<uint32_t*>(base + (size_t)kCtWarps * kCtStages * 4096);
+  uint32_t* lvl = rep + 4 * 256 * 32;
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(lvl + 5 * 1024);
+  for (int i = threadIdx.x; i < 4 * 256 * 32; i += blockDim.x) rep[i] = tabs[kTabS4 + (i >> 5)];
+  for (int i = threadIdx.x; i < 5 * 1024; i += blockDim.x) lvl[i] = tabs[kTabLane + i];
+  if (threadIdx.x < kCtWarps * kCtStages)
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[threadIdx.x])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t gw = blockIdx.x * kCtWarps + (uint32_t)w, nw = gridDim.x * kCtWarps;
+  auto issue = [&](uint32_t k) {  // lane 0: page gw + k*nw -> stage k & 1
+    const uint32_t pg = gw + k * nw;
+    if (pg >= n_pages) return;
+    const int s = w * kCtStages + (int)(k & 1);
+    const uint32_t bar = smem_u32(&mbar[s]);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(4096)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(stages + (size_t)s * 4096)),
+        "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(0), "r"(pg * 32), "r"(bar)
+        : "memory");
+  };
+  if (lane == 0) {
+    issue(0);
+    issue(1);
+  }
+  const uint32_t* r0 = rep + lane;
+  const uint32_t* r1 = rep + 256 * 32 + lane;
+  const uint32_t* r2 = rep + 2 * 256 * 32 + lane;
+  const uint32_t* r3 = rep + 3 * 256 * 32 + lane;
+  for (uint32_t k = 0;; ++k) {
+    const uint32_t pg = gw + k * nw;
+    if (pg >= n_pages) break;
+    const int s = w * kCtStages + (int)(k & 1);
+    const uint32_t bar = smem_u32(&mbar[s]), parity = (k >> 1) & 1;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+    const uint8_t* row = stages + (size_t)s * 4096 + lane * 128;
+    uint32_t c = 0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const uint4 v = *reinterpret_cast<const uint4*>(row + ((u ^ (lane & 7)) << 4));
+      const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t x = c ^ wd[q];
+        c = r3[(x & 255) << 5] ^ r2[((x >> 8) & 255) << 5] ^ r1[((x >> 16) & 255) << 5] ^
+            r0[(x >> 24) << 5];
+      }
+    }
+    __syncwarp();
+    if (lane == 0) issue(k + 2);  // every lane has read this stage
+#pragma unroll
+    for (int v2 = 0; v2 < 5; ++v2) {
+      const uint32_t o = __shfl_down_sync(0xffffffffu, c, 1 << v2);
+      if ((lane & ((2 << v2) - 1)) == 0) c = mul_tab(lvl + 1024 * v2, c) ^ o;
+    }
+    if (lane == 0) out[pg] = c;
+  }
+}
+
 __global__ void __launch_bounds__(kCrcThreads)
     fp_crc_fold(const uint32_t* __restrict__ page_crc, uint32_t pages_per_chunk, uint32_t n_pages,
                 uint32_t log2r, const uint32_t* __restrict__ tabs, uint32_t* __restrict__ out) {
@@ -554,6 +646,35 @@ int flag_wait_launch(const uint32_t* d_flag, uint32_t value, uint64_t max_ns,
   return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
 }
 
+// 2-D tensor map of d_buf as rows of 128 B, box = one 4 KiB page (32 rows),
+// 128-B swizzle. false if the driver entry point is unavailable (or FP_NO_TMA)
+static bool encode_page_map(CUtensorMap* m, const uint8_t* d_buf, uint64_t bytes) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (!getenv("FP_NO_TMA") &&
+        cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<Encode>(p);
+  }
+  if (!fn || ((uintptr_t)d_buf & 15) || bytes / 128 > (1ull << 32)) return false;
+  const cuuint64_t dims[2] = {128, bytes / 128};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {128, 32};
+  const cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_buf), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int crc_launch(const uint8_t* d_buf, uint64_t bytes, uint64_t chunk_bytes, const uint32_t* d_tabs,
                uint32_t* d_page_crc, uint32_t* d_chunk_crc, void* stream) {
   if (!bytes) return 0;
@@ -568,8 +689,22 @@ int crc_launch(const uint8_t* d_buf, uint64_t bytes, uint64_t chunk_bytes, const
   }
   const uint32_t n_pages = (uint32_t)(bytes / 4096);
   const uint32_t ppc = (uint32_t)(chunk_bytes / 4096);
-  const int grid_p = (int)std::min<uint32_t>((n_pages + 31) / 32, (uint32_t)sm_count(-1));
-  fp_crc_pages<<<grid_p, kCrcThreads, kCrcPagesSmem, st>>>(d_buf, n_pages, d_tabs, d_page_crc);
+  CUtensorMap tmap;
+  if (encode_page_map(&tmap, d_buf, bytes)) {
+    static bool tma_attr = false;
+    if (!tma_attr) {
+      if (cudaFuncSetAttribute(fp_crc_pages_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)kCtSmem) != cudaSuccess)
+        return FP_ECUDA;
+      tma_attr = true;
+    }
+    const int grid = (int)std::min<uint32_t>((n_pages + kCtWarps - 1) / kCtWarps,
+                                             (uint32_t)sm_count(-1));
+    fp_crc_pages_tma<<<grid, kCtWarps * 32, kCtSmem, st>>>(tmap, n_pages, d_tabs, d_page_crc);
+  } else {
+    const int grid_p = (int)std::min<uint32_t>((n_pages + 31) / 32, (uint32_t)sm_count(-1));
+    fp_crc_pages<<<grid_p, kCrcThreads, kCrcPagesSmem, st>>>(d_buf, n_pages, d_tabs, d_page_crc);
+  }
   const uint32_t n_chunks = (n_pages + ppc - 1) / ppc;
   const uint32_t per = std::min(ppc, n_pages);
   uint32_t log2r = 0;

@@ -184,9 +184,10 @@ int fp_ctx::save_shard() {
   const bool want_crc = !(cfg.flags & FP_CFG_NO_CRC);
   const bool gpu_crc = want_crc && !host && !slabless && S % 4096 == 0 && d_crc_tabs;
   uint32_t shard_raw = 0;
-  // default: the CRC pages are computed inside the pack (fp_pack_crc);
-  // FP_CRC_SEPARATE=1 keeps fp_pack_v4 + fp_crc_pages (ablation)
-  const bool fused = gpu_crc && cfg.pack_impl == FP_PACK_V4 && !getenv("FP_CRC_SEPARATE") &&
+  // default: fp_pack_v4, then fp_crc_pages_tma over the slab; FP_CRC_FUSED=1
+  // computes the page CRCs inside the pack (fp_pack_crc, ablation: measured
+  // slower)
+  const bool fused = gpu_crc && cfg.pack_impl == FP_PACK_V4 && getenv("FP_CRC_FUSED") &&
                      !group_tile_off.empty();
   auto stage = [&](uint64_t c) -> int {
     const uint32_t s = (uint32_t)(c % R);

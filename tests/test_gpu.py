@@ -314,7 +314,14 @@ cfg, slot, pack_bytes, pack, d = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
 dev = torch.device("cuda", 0)
 st = make_state(config_specs(cfg), dev)
 lay = oracle_layout([st], 1)
-with fp.Checkpointer(dev, io_engine="gds", slot_bytes=slot, pack_bytes=pack_bytes, pack=pack) as ck:
+try:
+    ck = fp.Checkpointer(dev, io_engine="gds", slot_bytes=slot, pack_bytes=pack_bytes, pack=pack)
+except fp.FastPersistError as e:
+    if e.code == -38:                     # -ENOSYS: no usable libcufile on this host
+        print("GDS_UNAVAILABLE", flush=True)
+        os._exit(0)                       # skip atexit hooks of a stuck libcufile thread
+    raise
+with ck:
     for _ in range(2):
         s = ck.save(entries(st), d)
     assert s["engine"] == 4 and s["pack_launches"] > 0 and s["fallback"] in (0, 2), s
@@ -347,16 +354,41 @@ def test_gds_engine_parity(tmp_path, cfg, slot, pack_bytes, pack):
     except subprocess.TimeoutExpired:
         pytest.fail("GDS checkpoint did not finish within 240 s")
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    if "GDS_UNAVAILABLE" in r.stdout:
+        pytest.skip("cuFile driver unavailable on this host (no nvidia-fs): " + r.stderr[-300:])
     assert "gds ok" in r.stdout
 
 
-def test_crc_separate_kernels_parity(tmp_path, monkeypatch):
-    """FP_CRC_SEPARATE=1 (ablation): fp_pack_v4 then fp_crc_pages over the slab
-    instead of the fused fp_pack_crc; same shard bytes, same CRC-32."""
-    monkeypatch.setenv("FP_CRC_SEPARATE", "1")
+@pytest.mark.parametrize("slot,pack_bytes", [(1 << 20, 3 << 20), (4096, 8192), (64 << 20, 256 << 20)])
+def test_crc_fused_kernel_parity(tmp_path, monkeypatch, slot, pack_bytes):
+    """FP_CRC_FUSED=1 (ablation): page CRCs computed inside the pack
+    (fp_pack_crc) instead of fp_crc_pages_tma over the slab; same shard bytes,
+    same CRC-32."""
+    monkeypatch.setenv("FP_CRC_FUSED", "1")
     st = _state("gpt3_odd")
     lay = oracle_layout([st], 1)
-    with fp.Checkpointer(DEV, slot_bytes=1 << 20, pack_bytes=3 << 20) as ck:
+    with fp.Checkpointer(DEV, slot_bytes=slot, pack_bytes=pack_bytes) as ck:
         s = ck.save(entries(st), str(tmp_path))
     assert s["crc_valid"]
     _check_rank_files(str(tmp_path), lay, 1)
+
+
+def test_crc_pages_without_tma_parity(tmp_path, monkeypatch):
+    """FP_NO_TMA=1: the LSU fp_crc_pages kernel (used when no tensor map can be
+    encoded) gives the same CRC-32 as the TMA kernel and zlib. Runs in a child
+    process (the tensor-map entry point is resolved once per process)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import os,sys,torch; sys.path.insert(0, os.environ['FP_ROOT']);"
+            "import paper_2406_13768_b200 as fp;"
+            "from tests._util import entries, oracle_layout;"
+            "from tests.test_gpu import _check_rank_files, _state;"
+            "st=_state('gpt3_odd'); lay=oracle_layout([st],1); d=sys.argv[1];"
+            "ck=fp.Checkpointer(torch.device('cuda',0), slot_bytes=1<<20, pack_bytes=3<<20);"
+            "s=ck.save(entries(st), d); ck.close(); assert s['crc_valid'];"
+            "_check_rank_files(d, lay, 1); print('ok')")
+    env = dict(os.environ, FP_ROOT=root, PYTHONPATH=root, FP_NO_TMA="1")
+    r = subprocess.run([sys.executable, "-c", code, str(tmp_path)], capture_output=True, text=True,
+                       env=env, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
