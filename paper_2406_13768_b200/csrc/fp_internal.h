@@ -177,7 +177,8 @@ int crc_fold_launch(const uint32_t* d_page_crc, uint64_t bytes, uint64_t chunk_b
 constexpr uint32_t kCrcPageLevels = 20;
 constexpr uint32_t kTabS4 = 0;
 constexpr uint32_t kTabLane = 4 * 256;
-constexpr uint32_t kTabPage = kTabLane + 5 * 1024;
+constexpr uint32_t kLaneLevels = 7;  // products by x^(8*32*2^v), v = 0..6
+constexpr uint32_t kTabPage = kTabLane + kLaneLevels * 1024;
 constexpr uint32_t kTabWords = kTabPage + kCrcPageLevels * 1024;
 
 // ---------------------------------------------------------------------------

@@ -249,15 +249,53 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
 //
 // Device table blob (uint32, built by crc_device_tables on the host):
 //   [kTabS4 .. +1024)   slicing-by-4 tables t[k][b] (b followed by k bytes)
-//   [kTabLane + 1024 v) product by x^(8*128*2^v),  v = 0..4
+//   [kTabLane + 1024 v) product by x^(8*32*2^v),   v = 0..6
 //   [kTabPage + 1024 j) product by x^(8*4096*2^j), j = 0..19
 // each product table is four 256-entry tables: M[i][b] = K * (b << 8i).
 // ---------------------------------------------------------------------------
 constexpr int kCrcThreads = 1024;
-constexpr size_t kCrcPagesSmem = (4 * 256 * 32 + 5 * 1024) * sizeof(uint32_t);  // 148 KiB
+constexpr size_t kCrcTabWords = 4 * 256 * 32 + kLaneLevels * 1024;  // per-lane + level tables
+constexpr size_t kCrcPagesSmem = kCrcTabWords * sizeof(uint32_t);      // 156 KiB
 
 __device__ __forceinline__ uint32_t mul_tab(const uint32_t* __restrict__ m, uint32_t a) {
   return m[a & 255] ^ m[256 + ((a >> 8) & 255)] ^ m[512 + ((a >> 16) & 255)] ^ m[768 + (a >> 24)];
+}
+
+// Raw CRC of one 4 KiB page held by a warp, lane l owning bytes
+// [128 l, 128 l + 128) as v[0..7]; the result is valid in lane 0. Each lane
+// runs four independent 32-B slicing-by-4 chains (ILP: the chains' table
+// lookups overlap instead of waiting on each other), combines them with the
+// products by x^(8*32) and x^(8*64), then the lanes are combined in a
+// 5-level shuffle tree (x^(8*128*2^v)). rep = per-lane copies of the 4
+// slicing tables (entry e of table k at (k*256 + e)*32 + lane), lvl = the
+// kLaneLevels constant-product tables.
+__device__ __forceinline__ uint32_t page_crc_warp(const uint4 (&v)[8], const uint32_t* rep,
+                                                  const uint32_t* lvl, int lane) {
+  const uint32_t* r0 = rep + lane;
+  const uint32_t* r1 = rep + 256 * 32 + lane;
+  const uint32_t* r2 = rep + 2 * 256 * 32 + lane;
+  const uint32_t* r3 = rep + 3 * 256 * 32 + lane;
+  uint32_t c[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint4& vv = v[2 * j + (q >> 2)];
+      const uint32_t w = (q & 3) == 0 ? vv.x : (q & 3) == 1 ? vv.y : (q & 3) == 2 ? vv.z : vv.w;
+      const uint32_t x = c[j] ^ w;
+      c[j] = r3[(x & 255) << 5] ^ r2[((x >> 8) & 255) << 5] ^ r1[((x >> 16) & 255) << 5] ^
+             r0[(x >> 24) << 5];
+    }
+  }
+  const uint32_t ab = mul_tab(lvl, c[0]) ^ c[1];
+  const uint32_t cd = mul_tab(lvl, c[2]) ^ c[3];
+  uint32_t cl = mul_tab(lvl + 1024, ab) ^ cd;
+#pragma unroll
+  for (int v2 = 0; v2 < 5; ++v2) {
+    const uint32_t o = __shfl_down_sync(0xffffffffu, cl, 1 << v2);
+    if ((lane & ((2 << v2) - 1)) == 0) cl = mul_tab(lvl + 1024 * (2 + v2), cl) ^ o;
+  }
+  return cl;
 }
 
 __global__ void __launch_bounds__(kCrcThreads, 1)
@@ -265,37 +303,18 @@ __global__ void __launch_bounds__(kCrcThreads, 1)
                  const uint32_t* __restrict__ tabs, uint32_t* __restrict__ out) {
   extern __shared__ __align__(16) uint32_t crc_smem[];
   uint32_t* rep = crc_smem;                    // [4][256][32] per-lane copies
-  uint32_t* lvl = crc_smem + 4 * 256 * 32;     // [5][4][256]
+  uint32_t* lvl = crc_smem + 4 * 256 * 32;     // [kLaneLevels][4][256]
   for (int i = threadIdx.x; i < 4 * 256 * 32; i += blockDim.x) rep[i] = tabs[kTabS4 + (i >> 5)];
-  for (int i = threadIdx.x; i < 5 * 1024; i += blockDim.x) lvl[i] = tabs[kTabLane + i];
+  for (int i = threadIdx.x; i < (int)kLaneLevels * 1024; i += blockDim.x) lvl[i] = tabs[kTabLane + i];
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const uint32_t* r0 = rep + lane;                   // table 0, entry e at r0[e*32]
-  const uint32_t* r1 = rep + 256 * 32 + lane;
-  const uint32_t* r2 = rep + 2 * 256 * 32 + lane;
-  const uint32_t* r3 = rep + 3 * 256 * 32 + lane;
   const uint32_t wpb = blockDim.x >> 5;
   for (uint32_t pg = blockIdx.x * wpb + (threadIdx.x >> 5); pg < n_pages; pg += gridDim.x * wpb) {
     const uint4* src = reinterpret_cast<const uint4*>(buf + (size_t)pg * 4096 + lane * 128);
     uint4 v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) v[u] = __ldg(src + u);
-    uint32_t c = 0;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t x = c ^ w[q];
-        c = r3[(x & 255) << 5] ^ r2[((x >> 8) & 255) << 5] ^ r1[((x >> 16) & 255) << 5] ^
-            r0[(x >> 24) << 5];
-      }
-    }
-#pragma unroll
-    for (int v2 = 0; v2 < 5; ++v2) {
-      const uint32_t o = __shfl_down_sync(0xffffffffu, c, 1 << v2);
-      if ((lane & ((2 << v2) - 1)) == 0) c = mul_tab(lvl + 1024 * v2, c) ^ o;
-    }
+    const uint32_t c = page_crc_warp(v, rep, lvl, lane);
     if (lane == 0) out[pg] = c;
   }
 }
@@ -311,8 +330,7 @@ __global__ void __launch_bounds__(kCrcThreads, 1)
 constexpr int kCtWarps = 8;
 constexpr int kCtStages = 2;  // per warp
 constexpr size_t kCtSmem = 1024 + (size_t)kCtWarps * kCtStages * 4096 +
-                           (4 * 256 * 32 + 5 * 1024) * sizeof(uint32_t) +
-                           (size_t)kCtWarps * kCtStages * 8;
+                           kCrcTabWords * sizeof(uint32_t) + (size_t)kCtWarps * kCtStages * 8;
 
 __global__ void __launch_bounds__(kCtWarps * 32, 1)
     fp_crc_pages_tma(const __grid_constant__ CUtensorMap tmap, uint32_t n_pages,
@@ -322,9 +340,9 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
   uint8_t* stages = base;
   uint32_t* rep = reinterpret_cast<uint32_t*>(base + (size_t)kCtWarps * kCtStages * 4096);
   uint32_t* lvl = rep + 4 * 256 * 32;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(lvl + 5 * 1024);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(lvl + kLaneLevels * 1024);
   for (int i = threadIdx.x; i < 4 * 256 * 32; i += blockDim.x) rep[i] = tabs[kTabS4 + (i >> 5)];
-  for (int i = threadIdx.x; i < 5 * 1024; i += blockDim.x) lvl[i] = tabs[kTabLane + i];
+  for (int i = threadIdx.x; i < (int)kLaneLevels * 1024; i += blockDim.x) lvl[i] = tabs[kTabLane + i];
   if (threadIdx.x < kCtWarps * kCtStages)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[threadIdx.x])));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -349,10 +367,6 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
     issue(0);
     issue(1);
   }
-  const uint32_t* r0 = rep + lane;
-  const uint32_t* r1 = rep + 256 * 32 + lane;
-  const uint32_t* r2 = rep + 2 * 256 * 32 + lane;
-  const uint32_t* r3 = rep + 3 * 256 * 32 + lane;
   for (uint32_t k = 0;; ++k) {
     const uint32_t pg = gw + k * nw;
     if (pg >= n_pages) break;
@@ -368,25 +382,13 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
         "r"(parity)
         : "memory");
     const uint8_t* row = stages + (size_t)s * 4096 + lane * 128;
-    uint32_t c = 0;
+    uint4 v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const uint4 v = *reinterpret_cast<const uint4*>(row + ((u ^ (lane & 7)) << 4));
-      const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint32_t x = c ^ wd[q];
-        c = r3[(x & 255) << 5] ^ r2[((x >> 8) & 255) << 5] ^ r1[((x >> 16) & 255) << 5] ^
-            r0[(x >> 24) << 5];
-      }
-    }
+    for (int u = 0; u < 8; ++u)
+      v[u] = *reinterpret_cast<const uint4*>(row + ((u ^ (lane & 7)) << 4));
     __syncwarp();
-    if (lane == 0) issue(k + 2);  // every lane has read this stage
-#pragma unroll
-    for (int v2 = 0; v2 < 5; ++v2) {
-      const uint32_t o = __shfl_down_sync(0xffffffffu, c, 1 << v2);
-      if ((lane & ((2 << v2) - 1)) == 0) c = mul_tab(lvl + 1024 * v2, c) ^ o;
-    }
+    if (lane == 0) issue(k + 2);  // every lane has its copy of this stage
+    const uint32_t c = page_crc_warp(v, rep, lvl, lane);
     if (lane == 0) out[pg] = c;
   }
 }
@@ -439,8 +441,8 @@ __global__ void __launch_bounds__(kCrcThreads)
 // ---------------------------------------------------------------------------
 constexpr int kPcThreads = 512;
 constexpr int kPcProducers = 256;
-constexpr size_t kPcTabWords = 4 * 256 * 32 + 5 * 1024;
-constexpr size_t kPcSmem = kPcTabWords * 4 + 2 * (size_t)kTile;  // 212 KiB
+constexpr size_t kPcTabWords = kCrcTabWords;
+constexpr size_t kPcSmem = kPcTabWords * 4 + 2 * (size_t)kTile;  // 220 KiB
 
 __device__ __forceinline__ uint32_t stage_off(uint32_t off) {  // swizzled byte offset
   const uint32_t c = off >> 4;
@@ -521,7 +523,7 @@ __global__ void __launch_bounds__(kPcThreads, 1)
   uint32_t* lvl = pc_smem + 4 * 256 * 32;     // [5][4][256]
   uint8_t* stage0 = reinterpret_cast<uint8_t*>(pc_smem + kPcTabWords);
   for (int i = threadIdx.x; i < 4 * 256 * 32; i += blockDim.x) rep[i] = tabs[kTabS4 + (i >> 5)];
-  for (int i = threadIdx.x; i < 5 * 1024; i += blockDim.x) lvl[i] = tabs[kTabLane + i];
+  for (int i = threadIdx.x; i < (int)kLaneLevels * 1024; i += blockDim.x) lvl[i] = tabs[kTabLane + i];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp < kPcProducers / 32) {
@@ -543,38 +545,20 @@ __global__ void __launch_bounds__(kPcThreads, 1)
     for (uint32_t j = (k >= 2 ? k - 2 : 0); j < k; ++j) bar_sync(3 + (int)(j & 1), kPcThreads);
   } else {
     const int w = warp - kPcProducers / 32;  // page of the tile
-    const uint32_t* r0 = rep + lane;
-    const uint32_t* r1 = rep + 256 * 32 + lane;
-    const uint32_t* r2 = rep + 2 * 256 * 32 + lane;
-    const uint32_t* r3 = rep + 3 * 256 * 32 + lane;
     uint32_t k = 0;
     for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
       const int b = (int)(k & 1);
       bar_sync(1 + b, kPcThreads);  // FULL[b]
       const uint8_t* stage = stage0 + (size_t)b * kTile;
       const uint32_t pg = tile * (kTile / 4096) + (uint32_t)w;
-      uint32_t c = 0;
+      uint4 v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        v[u] = *reinterpret_cast<const uint4*>(
+            stage + stage_off((uint32_t)w * 4096 + (uint32_t)lane * 128 + 16 * u));
+      bar_arrive(3 + b, kPcThreads);  // EMPTY[b]: the page is in registers
       if (pg < n_pages) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint4 v = *reinterpret_cast<const uint4*>(
-              stage + stage_off((uint32_t)w * 4096 + (uint32_t)lane * 128 + 16 * u));
-          const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const uint32_t x = c ^ wd[q];
-            c = r3[(x & 255) << 5] ^ r2[((x >> 8) & 255) << 5] ^ r1[((x >> 16) & 255) << 5] ^
-                r0[(x >> 24) << 5];
-          }
-        }
-      }
-      bar_arrive(3 + b, kPcThreads);  // EMPTY[b]: staging read, registers hold the rest
-      if (pg < n_pages) {
-#pragma unroll
-        for (int v2 = 0; v2 < 5; ++v2) {
-          const uint32_t o = __shfl_down_sync(0xffffffffu, c, 1 << v2);
-          if ((lane & ((2 << v2) - 1)) == 0) c = mul_tab(lvl + 1024 * v2, c) ^ o;
-        }
+        const uint32_t c = page_crc_warp(v, rep, lvl, lane);
         if (lane == 0) page_crc[pg] = c;
       }
     }

@@ -1,0 +1,55 @@
+// Host emulation of the device CRC-32 scheme (pack.cu: page_crc_warp as used
+// by fp_crc_pages / fp_crc_pages_tma / fp_pack_crc, and fp_crc_fold): the same
+// table blob (crc_device_tables), the same chain split, lane tree and
+// front-padded fold, compared with the plain slicing CRC (crc_raw_update) on
+// random pages, for several page and chunk counts. Built and run by
+// tests/test_crc_scheme_cpu.py (no GPU needed).
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+#include "fp_internal.h"
+using namespace fp;
+static uint32_t mul_tab(const uint32_t* m, uint32_t a) {
+  return m[a & 255] ^ m[256 + ((a >> 8) & 255)] ^ m[512 + ((a >> 16) & 255)] ^ m[768 + (a >> 24)];
+}
+int main() {
+  auto T = crc_device_tables();
+  const uint32_t* t0 = &T[kTabS4], *t1 = t0 + 256, *t2 = t0 + 512, *t3 = t0 + 768;
+  for (uint32_t n_pages : {1u, 2u, 3u, 37u, 1024u, 1500u, 2049u}) for (uint32_t ppc : {1u, 3u, 16u, 1024u, 2048u}) {
+    std::vector<uint8_t> buf((size_t)n_pages * 4096);
+    for (auto& b : buf) b = rand() & 255;
+    std::vector<uint32_t> pc(n_pages);
+    for (uint32_t pg = 0; pg < n_pages; ++pg) {
+      uint32_t lc[32];
+      for (int lane = 0; lane < 32; ++lane) {
+        const uint32_t* w = (const uint32_t*)(buf.data() + (size_t)pg * 4096 + lane * 128);
+        uint32_t c[4] = {0,0,0,0};
+        for (int q = 0; q < 8; ++q) for (int j = 0; j < 4; ++j) { uint32_t x = c[j] ^ w[8*j + q]; c[j] = t3[x & 255] ^ t2[(x >> 8) & 255] ^ t1[(x >> 16) & 255] ^ t0[x >> 24]; }
+        uint32_t ab = mul_tab(&T[kTabLane], c[0]) ^ c[1], cd = mul_tab(&T[kTabLane], c[2]) ^ c[3];
+        lc[lane] = mul_tab(&T[kTabLane + 1024], ab) ^ cd;
+      }
+      for (int v = 0; v < 5; ++v) {
+        uint32_t nc[32];
+        for (int l = 0; l < 32; ++l) { uint32_t o = l + (1 << v) < 32 ? lc[l + (1 << v)] : lc[l];
+          nc[l] = ((l & ((2 << v) - 1)) == 0) ? mul_tab(&T[kTabLane + 1024 * (2 + v)], lc[l]) ^ o : lc[l]; }
+        for (int l = 0; l < 32; ++l) lc[l] = nc[l];
+      }
+      pc[pg] = lc[0];
+      if (pc[pg] != crc_raw_update(0, buf.data() + (size_t)pg * 4096, 4096)) { printf("page mismatch\n"); return 1; }
+    }
+    const uint32_t n_chunks = (n_pages + ppc - 1) / ppc, per = std::min(ppc, n_pages);
+    uint32_t log2r = 0; while ((1024ull << log2r) < per) ++log2r;
+    for (uint32_t ch = 0; ch < n_chunks; ++ch) {
+      const uint32_t p0 = ch * ppc, np = std::min(ppc, n_pages - p0), r = 1u << log2r;
+      const int64_t pad = 1024ll * r - np;
+      std::vector<uint32_t> red(1024);
+      for (int t = 0; t < 1024; ++t) { uint32_t acc = 0;
+        for (uint32_t i = 0; i < r; ++i) { int64_t idx = (int64_t)t * r + i - pad; acc = mul_tab(&T[kTabPage], acc) ^ (idx >= 0 ? pc[p0 + idx] : 0u); }
+        red[t] = acc; }
+      for (int m = 0; (1 << m) < 1024; ++m) { int step = 1 << m;
+        for (int t = 0; t < 1024; t += 2 * step) red[t] = mul_tab(&T[kTabPage + 1024 * (log2r + m)], red[t]) ^ red[t + step]; }
+      if (red[0] != crc_raw_update(0, buf.data() + (size_t)p0 * 4096, (size_t)np * 4096)) { printf("chunk mismatch n=%u ppc=%u ch=%u\n", n_pages, ppc, ch); return 1; }
+    }
+  }
+  printf("emulation ok\n");
+}
