@@ -422,6 +422,7 @@ def our_arm(a):
     pk_launches = sum(s["pack_launches"] for s in stats)
     pack_gbs = 2 * pk_bytes / (pk_ms / 1e3) / 1e9 if pk_ms > 0 else None
     d2h_ms = sum(s["d2h_ms"] for s in stats)
+    crc_ms = sum(s.get("crc_ms", 0.0) for s in stats)
     pack_gbs = pack_gbs or 0.0                       # this rank's own GPU (rank 0 reports)
     launches_all = allreduce_sum(sum(s["kernel_launches"] for s in stats), dev)
 
@@ -568,6 +569,16 @@ def our_arm(a):
                          "frac": round(pack_gbs / hbm, 4), "traffic": traffic,
                          "peak_source": peak_src, "launch_avg_ms": round(launch_avg_ms, 5),
                          "bytes_per_launch": int(2 * pk_bytes / max(1, pk_launches))},
+            # the second library kernel pair of a step: page CRCs + fold over
+            # each packed group (1 B read per slab byte; issue-bound on table
+            # lookups) — reported, not the roofline kernel
+            "crc_kernels": None if crc_ms <= 0 else {
+                "kernels": "fp_crc_pages + fp_crc_fold" if not os.environ.get("FP_CRC_TMA")
+                else "fp_crc_pages_tma + fp_crc_fold",
+                "us_per_launch": round(1e3 * crc_ms / max(1, pk_launches), 2),
+                "read_gbs": round(pk_bytes / (crc_ms / 1e3) / 1e9, 1),
+                "frac_of_hbm": round(pk_bytes / (crc_ms / 1e3) / 1e9 / hbm, 4),
+                "share_of_library_gpu_time": round(crc_ms / (crc_ms + pk_ms), 3)},
             "nvme": {"measured_gbs": round(nvme_gbs, 3), "frac": round(gbs / nvme_gbs, 4),
                      "before_gbs": round(nvme_before, 3), "after_gbs": round(nvme_after, 3),
                      "how": f"built-in fp_io_bench (fio absent): O_DIRECT io_uring seq "

@@ -180,6 +180,8 @@ typedef struct fp_stats {
                               (host tensors: on the CPU); also in the manifest  */
   uint32_t crc_valid;      /* 1 if shard_crc32 was computed                       */
   uint64_t kernel_launches;/* all library kernels launched (pack, CRC, gate)      */
+  double   crc_ms;         /* sum of CUDA-event durations of the CRC kernels
+                              (page CRCs + per-chunk fold) after each pack       */
 } fp_stats;
 
 typedef struct fp_ctx fp_ctx;

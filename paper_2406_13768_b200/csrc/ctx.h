@@ -75,7 +75,7 @@ struct fp_ctx {
   uint8_t* d_slab = nullptr;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_producer = nullptr;
-  std::vector<cudaEvent_t> ev_p0, ev_p1, ev_d0, ev_d2h;
+  std::vector<cudaEvent_t> ev_p0, ev_p1, ev_c1, ev_d0, ev_d2h;  // pack, CRC end, D2H
   std::vector<uint8_t> has_pack;  // per ring slot: its chunk led a pack launch
   // Host -> GPU signals live in one mapped pinned page, read on the GPU by
   // fp_wait_flag (a 1-warp kernel spinning with ld.acquire.sys; stream

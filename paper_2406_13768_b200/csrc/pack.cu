@@ -269,27 +269,36 @@ __device__ __forceinline__ uint32_t mul_tab(const uint32_t* __restrict__ m, uint
 // 5-level shuffle tree (x^(8*128*2^v)). rep = per-lane copies of the 4
 // slicing tables (entry e of table k at (k*256 + e)*32 + lane), lvl = the
 // kLaneLevels constant-product tables.
+template <int kChains>
 __device__ __forceinline__ uint32_t page_crc_warp(const uint4 (&v)[8], const uint32_t* rep,
                                                   const uint32_t* lvl, int lane) {
+  static_assert(kChains == 1 || kChains == 4, "1 chain of 128 B or 4 chains of 32 B");
   const uint32_t* r0 = rep + lane;
   const uint32_t* r1 = rep + 256 * 32 + lane;
   const uint32_t* r2 = rep + 2 * 256 * 32 + lane;
   const uint32_t* r3 = rep + 3 * 256 * 32 + lane;
-  uint32_t c[4] = {0, 0, 0, 0};
+  constexpr int kWords = 32 / kChains;  // words per chain
+  uint32_t c[kChains];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
+  for (int j = 0; j < kChains; ++j) c[j] = 0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint4& vv = v[2 * j + (q >> 2)];
-      const uint32_t w = (q & 3) == 0 ? vv.x : (q & 3) == 1 ? vv.y : (q & 3) == 2 ? vv.z : vv.w;
+  for (int q = 0; q < kWords; ++q) {
+#pragma unroll
+    for (int j = 0; j < kChains; ++j) {
+      const int wi = j * kWords + q;  // word index in the lane's 128 B
+      const uint4& vv = v[wi >> 2];
+      const uint32_t w = (wi & 3) == 0 ? vv.x : (wi & 3) == 1 ? vv.y : (wi & 3) == 2 ? vv.z : vv.w;
       const uint32_t x = c[j] ^ w;
       c[j] = r3[(x & 255) << 5] ^ r2[((x >> 8) & 255) << 5] ^ r1[((x >> 16) & 255) << 5] ^
              r0[(x >> 24) << 5];
     }
   }
-  const uint32_t ab = mul_tab(lvl, c[0]) ^ c[1];
-  const uint32_t cd = mul_tab(lvl, c[2]) ^ c[3];
-  uint32_t cl = mul_tab(lvl + 1024, ab) ^ cd;
+  uint32_t cl = c[0];
+  if (kChains == 4) {
+    const uint32_t ab = mul_tab(lvl, c[0]) ^ c[1];
+    const uint32_t cd = mul_tab(lvl, c[kChains > 2 ? 2 : 0]) ^ c[kChains > 3 ? 3 : 0];
+    cl = mul_tab(lvl + 1024, ab) ^ cd;
+  }
 #pragma unroll
   for (int v2 = 0; v2 < 5; ++v2) {
     const uint32_t o = __shfl_down_sync(0xffffffffu, cl, 1 << v2);
@@ -314,7 +323,7 @@ __global__ void __launch_bounds__(kCrcThreads, 1)
     uint4 v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) v[u] = __ldg(src + u);
-    const uint32_t c = page_crc_warp(v, rep, lvl, lane);
+    const uint32_t c = page_crc_warp<1>(v, rep, lvl, lane);
     if (lane == 0) out[pg] = c;
   }
 }
@@ -388,7 +397,7 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
       v[u] = *reinterpret_cast<const uint4*>(row + ((u ^ (lane & 7)) << 4));
     __syncwarp();
     if (lane == 0) issue(k + 2);  // every lane has its copy of this stage
-    const uint32_t c = page_crc_warp(v, rep, lvl, lane);
+    const uint32_t c = page_crc_warp<4>(v, rep, lvl, lane);
     if (lane == 0) out[pg] = c;
   }
 }
@@ -558,7 +567,7 @@ __global__ void __launch_bounds__(kPcThreads, 1)
             stage + stage_off((uint32_t)w * 4096 + (uint32_t)lane * 128 + 16 * u));
       bar_arrive(3 + b, kPcThreads);  // EMPTY[b]: the page is in registers
       if (pg < n_pages) {
-        const uint32_t c = page_crc_warp(v, rep, lvl, lane);
+        const uint32_t c = page_crc_warp<4>(v, rep, lvl, lane);
         if (lane == 0) page_crc[pg] = c;
       }
     }
@@ -631,7 +640,8 @@ int flag_wait_launch(const uint32_t* d_flag, uint32_t value, uint64_t max_ns,
 }
 
 // 2-D tensor map of d_buf as rows of 128 B, box = one 4 KiB page (32 rows),
-// 128-B swizzle. false if the driver entry point is unavailable (or FP_NO_TMA)
+// 128-B swizzle. false unless FP_CRC_TMA=1 (ablation: measured slower than the
+// LSU kernel) and the driver entry point is available
 static bool encode_page_map(CUtensorMap* m, const uint8_t* d_buf, uint64_t bytes) {
   using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -643,7 +653,7 @@ static bool encode_page_map(CUtensorMap* m, const uint8_t* d_buf, uint64_t bytes
     tried = true;
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
-    if (!getenv("FP_NO_TMA") &&
+    if (getenv("FP_CRC_TMA") &&
         cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
             cudaSuccess &&
         q == cudaDriverEntryPointSuccess)

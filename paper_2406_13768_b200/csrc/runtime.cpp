@@ -265,6 +265,7 @@ int fp_ctx::save_shard() {
                                     d_chunk_crc, stream)
                   : crc_launch(d_slab, round_up(gbytes, 4096), S, d_crc_tabs, d_page_crc,
                                d_chunk_crc, stream);
+      if (!r && gpu_crc && cudaEventRecord(ev_c1[s], stream) != cudaSuccess) r = FP_ECUDA;
       if (gated) __atomic_store_n(&h_sig[0], ++gate_seq, __ATOMIC_RELEASE);  // open the gate
       if (r) return r;
       has_pack[s] = 1;
@@ -287,6 +288,9 @@ int fp_ctx::save_shard() {
       float a = 0, b = 0;
       if (has_pack[s] && cudaEventElapsedTime(&a, ev_p0[s], ev_p1[s]) == cudaSuccess)
         st.pack_ms += a;
+      float cm = 0;
+      if (has_pack[s] && gpu_crc && cudaEventElapsedTime(&cm, ev_p1[s], ev_c1[s]) == cudaSuccess)
+        st.crc_ms += cm;
       if (cudaEventElapsedTime(&b, ev_d0[s], ev_d2h[s]) == cudaSuccess) st.d2h_ms += b;
     }
     uint8_t* slot = ring + (size_t)s * S;
@@ -783,12 +787,14 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
       return fail(FP_ECUDA);
     c->ev_p0.resize(cfg.ring_slots);
     c->ev_p1.resize(cfg.ring_slots);
+    c->ev_c1.resize(cfg.ring_slots);
     c->ev_d0.resize(cfg.ring_slots);
     c->ev_d2h.resize(cfg.ring_slots);
     c->has_pack.assign(cfg.ring_slots, 0);
     for (uint32_t s = 0; s < cfg.ring_slots; ++s) {
       if (cudaEventCreate(&c->ev_p0[s]) != cudaSuccess ||
           cudaEventCreate(&c->ev_p1[s]) != cudaSuccess ||
+          cudaEventCreate(&c->ev_c1[s]) != cudaSuccess ||
           cudaEventCreate(&c->ev_d0[s]) != cudaSuccess ||
           cudaEventCreateWithFlags(&c->ev_d2h[s], cudaEventBlockingSync) != cudaSuccess)
         return fail(FP_ECUDA);
@@ -964,7 +970,7 @@ void fp_ckpt_destroy(fp_ctx* c) {
   }
   if (c->dev >= 0) {
     if (c->stream) cudaStreamSynchronize(c->stream);
-    for (auto* v : {&c->ev_p0, &c->ev_p1, &c->ev_d0, &c->ev_d2h})
+    for (auto* v : {&c->ev_p0, &c->ev_p1, &c->ev_c1, &c->ev_d0, &c->ev_d2h})
       for (cudaEvent_t e : *v)
         if (e) cudaEventDestroy(e);
     if (c->ev_producer) cudaEventDestroy(c->ev_producer);

@@ -21,12 +21,18 @@ int main() {
     std::vector<uint32_t> pc(n_pages);
     for (uint32_t pg = 0; pg < n_pages; ++pg) {
       uint32_t lc[32];
+      const int chains = (pg & 1) ? 4 : 1;  // both variants of page_crc_warp
       for (int lane = 0; lane < 32; ++lane) {
         const uint32_t* w = (const uint32_t*)(buf.data() + (size_t)pg * 4096 + lane * 128);
         uint32_t c[4] = {0,0,0,0};
-        for (int q = 0; q < 8; ++q) for (int j = 0; j < 4; ++j) { uint32_t x = c[j] ^ w[8*j + q]; c[j] = t3[x & 255] ^ t2[(x >> 8) & 255] ^ t1[(x >> 16) & 255] ^ t0[x >> 24]; }
-        uint32_t ab = mul_tab(&T[kTabLane], c[0]) ^ c[1], cd = mul_tab(&T[kTabLane], c[2]) ^ c[3];
-        lc[lane] = mul_tab(&T[kTabLane + 1024], ab) ^ cd;
+        const int kw = 32 / chains;
+        for (int q = 0; q < kw; ++q) for (int j = 0; j < chains; ++j) { uint32_t x = c[j] ^ w[kw*j + q]; c[j] = t3[x & 255] ^ t2[(x >> 8) & 255] ^ t1[(x >> 16) & 255] ^ t0[x >> 24]; }
+        if (chains == 4) {
+          uint32_t ab = mul_tab(&T[kTabLane], c[0]) ^ c[1], cd = mul_tab(&T[kTabLane], c[2]) ^ c[3];
+          lc[lane] = mul_tab(&T[kTabLane + 1024], ab) ^ cd;
+        } else {
+          lc[lane] = c[0];
+        }
       }
       for (int v = 0; v < 5; ++v) {
         uint32_t nc[32];
