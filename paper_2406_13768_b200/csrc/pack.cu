@@ -333,54 +333,63 @@ __global__ void __launch_bounds__(kCrcThreads, 1)
 // touched 32 different 128-B lines: the L1/TEX pipe was the limiter). The slab
 // is a 2-D tensor map of 128-B rows with 128-B swizzling; one box = one 4 KiB
 // page = 32 rows, so lane l's run (row l) lands with its 16-B chunk u at
-// chunk u ^ (l & 7): the per-lane LDS.128 reads are conflict-free. Each warp
-// streams its own pages through 2 stages (lane 0 issues, mbarrier
-// complete_tx); no cross-warp synchronisation.
-constexpr int kCtWarps = 8;
-constexpr int kCtStages = 2;  // per warp
-constexpr size_t kCtSmem = 1024 + (size_t)kCtWarps * kCtStages * 4096 +
-                           kCrcTabWords * sizeof(uint32_t) + (size_t)kCtWarps * kCtStages * 8;
+// chunk u ^ (l & 7): the per-lane LDS.128 reads are conflict-free. Each of
+// the 16 warps streams its own pages through one stage (the page is copied
+// to registers, then the next page's TMA is issued into the same stage while
+// the warp computes). Table lookups are one PRMT + one LDS: the per-lane
+// copies are laid out in pairs of tables so that entry e of table k for lane
+// l sits at byte (k>>1)*64K + e*256 + (k&1)*128 + l*4; one byte_perm builds
+// (e << 8) | (l*4) from the data word and the constant offset is an
+// immediate of the load.
+constexpr int kCtWarps = 16;
+constexpr size_t kCtTabBytes = 4 * 256 * 32 * 4;  // paired per-lane tables
+constexpr size_t kCtSmem = kCtTabBytes + kLaneLevels * 1024 * 4 + 256 + 1024 +
+                           (size_t)kCtWarps * 4096;
 
 __global__ void __launch_bounds__(kCtWarps * 32, 1)
     fp_crc_pages_tma(const __grid_constant__ CUtensorMap tmap, uint32_t n_pages,
                      const uint32_t* __restrict__ tabs, uint32_t* __restrict__ out) {
-  extern __shared__ uint8_t ct_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>(((uintptr_t)ct_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* stages = base;
-  uint32_t* rep = reinterpret_cast<uint32_t*>(base + (size_t)kCtWarps * kCtStages * 4096);
-  uint32_t* lvl = rep + 4 * 256 * 32;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(lvl + kLaneLevels * 1024);
-  for (int i = threadIdx.x; i < 4 * 256 * 32; i += blockDim.x) rep[i] = tabs[kTabS4 + (i >> 5)];
+  extern __shared__ __align__(16) uint8_t ct_raw[];
+  uint32_t* lvl = reinterpret_cast<uint32_t*>(ct_raw + kCtTabBytes);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(ct_raw + kCtTabBytes + kLaneLevels * 1024 * 4);
+  uint8_t* stages = reinterpret_cast<uint8_t*>(
+      ((uintptr_t)(ct_raw + kCtTabBytes + kLaneLevels * 1024 * 4 + 256) + 1023) & ~(uintptr_t)1023);
+  for (int i = threadIdx.x; i < 4 * 256 * 32; i += blockDim.x) {
+    const int k = i >> 13, e = (i >> 5) & 255, l = i & 31;
+    *reinterpret_cast<uint32_t*>(ct_raw + (k >> 1) * 65536 + e * 256 + (k & 1) * 128 + l * 4) =
+        tabs[kTabS4 + k * 256 + e];
+  }
   for (int i = threadIdx.x; i < (int)kLaneLevels * 1024; i += blockDim.x) lvl[i] = tabs[kTabLane + i];
-  if (threadIdx.x < kCtWarps * kCtStages)
+  if (threadIdx.x < kCtWarps)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[threadIdx.x])));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t lane4 = (uint32_t)lane * 4;
   const uint32_t gw = blockIdx.x * kCtWarps + (uint32_t)w, nw = gridDim.x * kCtWarps;
-  auto issue = [&](uint32_t k) {  // lane 0: page gw + k*nw -> stage k & 1
+  uint8_t* stage = stages + (size_t)w * 4096;
+  const uint32_t bar = smem_u32(&mbar[w]);
+  auto issue = [&](uint32_t k) {  // lane 0: page gw + k*nw -> this warp's stage
     const uint32_t pg = gw + k * nw;
     if (pg >= n_pages) return;
-    const int s = w * kCtStages + (int)(k & 1);
-    const uint32_t bar = smem_u32(&mbar[s]);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(4096)
                  : "memory");
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(stages + (size_t)s * 4096)),
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(stage)),
         "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(0), "r"(pg * 32), "r"(bar)
         : "memory");
   };
-  if (lane == 0) {
-    issue(0);
-    issue(1);
-  }
+  // T_t[byte b of x] for this lane: one byte_perm + one LDS with an immediate
+  auto lk = [&](uint32_t x, const int b, const int t) -> uint32_t {
+    const uint32_t r = __byte_perm(x, lane4, 4u | ((uint32_t)b << 4) | (5u << 8) | (5u << 12));
+    return *reinterpret_cast<const uint32_t*>(ct_raw + r + ((t >> 1) * 65536 + (t & 1) * 128));
+  };
+  if (lane == 0) issue(0);
   for (uint32_t k = 0;; ++k) {
     const uint32_t pg = gw + k * nw;
     if (pg >= n_pages) break;
-    const int s = w * kCtStages + (int)(k & 1);
-    const uint32_t bar = smem_u32(&mbar[s]), parity = (k >> 1) & 1;
     asm volatile(
         "{\n"
         ".reg .pred p;\n"
@@ -388,17 +397,36 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
         "@!p bra WAIT_%=;\n"
         "}\n" ::"r"(bar),
-        "r"(parity)
+        "r"(k & 1)
         : "memory");
-    const uint8_t* row = stages + (size_t)s * 4096 + lane * 128;
+    const uint8_t* row = stage + lane * 128;
     uint4 v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u)
       v[u] = *reinterpret_cast<const uint4*>(row + ((u ^ (lane & 7)) << 4));
     __syncwarp();
-    if (lane == 0) issue(k + 2);  // every lane has its copy of this stage
-    const uint32_t c = page_crc_warp<4>(v, rep, lvl, lane);
-    if (lane == 0) out[pg] = c;
+    if (lane == 0) issue(k + 1);  // every lane has its copy of this page
+    uint32_t c[4] = {0, 0, 0, 0};  // four 32-B chains (ILP)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int wi = j * 8 + q;
+        const uint4& vv = v[wi >> 2];
+        const uint32_t wd = (wi & 3) == 0 ? vv.x : (wi & 3) == 1 ? vv.y : (wi & 3) == 2 ? vv.z : vv.w;
+        const uint32_t x = c[j] ^ wd;
+        c[j] = lk(x, 0, 3) ^ lk(x, 1, 2) ^ lk(x, 2, 1) ^ lk(x, 3, 0);
+      }
+    }
+    const uint32_t ab = mul_tab(lvl, c[0]) ^ c[1];
+    const uint32_t cd = mul_tab(lvl, c[2]) ^ c[3];
+    uint32_t cl = mul_tab(lvl + 1024, ab) ^ cd;
+#pragma unroll
+    for (int v2 = 0; v2 < 5; ++v2) {
+      const uint32_t o = __shfl_down_sync(0xffffffffu, cl, 1 << v2);
+      if ((lane & ((2 << v2) - 1)) == 0) cl = mul_tab(lvl + 1024 * (2 + v2), cl) ^ o;
+    }
+    if (lane == 0) out[pg] = cl;
   }
 }
 
