@@ -373,6 +373,12 @@ def our_arm(a):
     # on the box): the image's per-rank share, capped
     img_total = int(allreduce_sum(shard_bytes, dev))
     nv_bytes = min(-(-img_total // world), int(a.nvme_bytes))
+    # the roofline file sits beside two checkpoint generations: keep it within
+    # what the file system can hold (all ranks share one box)
+    fs = os.statvfs(root)
+    free_now = fs.f_bavail * fs.f_frsize
+    room = (free_now - 2.2 * img_total) / world
+    nv_bytes = int(max(2e9, min(nv_bytes, room * 0.8))) // 4096 * 4096
     barrier()
     os.sync()                                 # settle writeback of earlier runs first
 
@@ -573,8 +579,8 @@ def our_arm(a):
             # each packed group (1 B read per slab byte; issue-bound on table
             # lookups) — reported, not the roofline kernel
             "crc_kernels": None if crc_ms <= 0 else {
-                "kernels": "fp_crc_pages + fp_crc_fold" if not os.environ.get("FP_CRC_TMA")
-                else "fp_crc_pages_tma + fp_crc_fold",
+                "kernels": "fp_crc_pages_tma + fp_crc_fold" if not os.environ.get("FP_NO_TMA")
+                else "fp_crc_pages + fp_crc_fold",
                 "us_per_launch": round(1e3 * crc_ms / max(1, pk_launches), 2),
                 "read_gbs": round(pk_bytes / (crc_ms / 1e3) / 1e9, 1),
                 "frac_of_hbm": round(pk_bytes / (crc_ms / 1e3) / 1e9 / hbm, 4),
@@ -621,7 +627,8 @@ def main():
     ap.add_argument("--ring-slots", type=int, default=4)
     ap.add_argument("--qd", type=int, default=64)
     ap.add_argument("--sqe-kib", type=int, default=1024)
-    ap.add_argument("--nvme-bytes", type=float, default=16e9)
+    ap.add_argument("--nvme-bytes", type=float, default=24e9,
+                    help="cap on the roofline file per rank (default covers a whole C2 shard)")
     ap.add_argument("--oracle-bytes", type=float, default=1.5e9)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--overhead-iters", type=int, default=4)

@@ -668,8 +668,8 @@ int flag_wait_launch(const uint32_t* d_flag, uint32_t value, uint64_t max_ns,
 }
 
 // 2-D tensor map of d_buf as rows of 128 B, box = one 4 KiB page (32 rows),
-// 128-B swizzle. false unless FP_CRC_TMA=1 (ablation: measured slower than the
-// LSU kernel) and the driver entry point is available
+// 128-B swizzle. false if the driver entry point is unavailable or FP_NO_TMA=1
+// (then the LSU kernel fp_crc_pages runs: 1.6x slower)
 static bool encode_page_map(CUtensorMap* m, const uint8_t* d_buf, uint64_t bytes) {
   using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -681,7 +681,7 @@ static bool encode_page_map(CUtensorMap* m, const uint8_t* d_buf, uint64_t bytes
     tried = true;
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
-    if (getenv("FP_CRC_TMA") &&
+    if (!getenv("FP_NO_TMA") &&
         cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
             cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
