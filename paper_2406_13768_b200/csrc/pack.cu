@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cerrno>
 #include <cstdint>
 
@@ -636,6 +637,22 @@ int sm_count(int device) {
 
 }  // namespace
 
+// The dynamic shared-memory opt-in is a per-device function attribute: set it
+// once per (kernel, device), thread-safely. Slot: one per kernel.
+template <int Slot, typename K>
+static bool smem_opt_in(K kernel, size_t bytes) {
+  static std::atomic<uint64_t> done{0};  // bit d: set on device d
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) return false;
+  const uint64_t bit = 1ull << (d & 63);
+  if (done.load(std::memory_order_acquire) & bit) return true;
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
+      cudaSuccess)
+    return false;
+  done.fetch_or(bit, std::memory_order_acq_rel);
+  return true;
+}
+
 int pack_default_ctas(int impl, int device) {
   const int sms = sm_count(device);
   return impl == FP_PACK_BULK ? sms : sms * 4;
@@ -647,13 +664,7 @@ int pack_launch(int impl, const Item* d_items, uint32_t n_items, uint8_t* d_slab
   cudaStream_t st = (cudaStream_t)stream;
   const int grid = (int)((uint32_t)ctas < n_items ? (uint32_t)ctas : n_items);
   if (impl == FP_PACK_BULK) {
-    static bool attr_set = false;
-    if (!attr_set) {
-      if (cudaFuncSetAttribute(fp_pack_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)kBulkSmem) != cudaSuccess)
-        return FP_ECUDA;
-      attr_set = true;
-    }
+    if (!smem_opt_in<0>(fp_pack_bulk, kBulkSmem)) return FP_ECUDA;
     fp_pack_bulk<<<grid, kBulkThreads, kBulkSmem, st>>>(d_items, n_items, d_slab);
   } else {
     fp_pack_v4<<<grid, kV4Threads, 0, st>>>(d_items, n_items, d_slab);
@@ -702,24 +713,12 @@ int crc_launch(const uint8_t* d_buf, uint64_t bytes, uint64_t chunk_bytes, const
   if (!bytes) return 0;
   if (bytes % 4096 || chunk_bytes % 4096) return -EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(fp_crc_pages, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kCrcPagesSmem) != cudaSuccess)
-      return FP_ECUDA;
-    attr_set = true;
-  }
+  if (!smem_opt_in<1>(fp_crc_pages, kCrcPagesSmem)) return FP_ECUDA;
   const uint32_t n_pages = (uint32_t)(bytes / 4096);
   const uint32_t ppc = (uint32_t)(chunk_bytes / 4096);
   CUtensorMap tmap;
   if (encode_page_map(&tmap, d_buf, bytes)) {
-    static bool tma_attr = false;
-    if (!tma_attr) {
-      if (cudaFuncSetAttribute(fp_crc_pages_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)kCtSmem) != cudaSuccess)
-        return FP_ECUDA;
-      tma_attr = true;
-    }
+    if (!smem_opt_in<2>(fp_crc_pages_tma, kCtSmem)) return FP_ECUDA;
     const int grid = (int)std::min<uint32_t>((n_pages + kCtWarps - 1) / kCtWarps,
                                              (uint32_t)sm_count(-1));
     fp_crc_pages_tma<<<grid, kCtWarps * 32, kCtSmem, st>>>(tmap, n_pages, d_tabs, d_page_crc);
@@ -741,13 +740,7 @@ int pack_crc_launch(const Item* d_items, const uint32_t* d_tile_lo, uint32_t n_t
                     uint8_t* d_slab, uint32_t n_pages, const uint32_t* d_tabs,
                     uint32_t* d_page_crc, int ctas, void* stream) {
   if (!n_tiles) return 0;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(fp_pack_crc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kPcSmem) != cudaSuccess)
-      return FP_ECUDA;
-    attr_set = true;
-  }
+  if (!smem_opt_in<3>(fp_pack_crc, kPcSmem)) return FP_ECUDA;
   const int sms = sm_count(-1);
   const int grid = (int)std::min<uint32_t>(n_tiles, (uint32_t)std::min(ctas > 0 ? ctas : sms, sms));
   fp_pack_crc<<<grid, kPcThreads, kPcSmem, (cudaStream_t)stream>>>(d_items, d_tile_lo, n_tiles,
