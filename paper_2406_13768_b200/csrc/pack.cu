@@ -28,6 +28,7 @@
 #include <atomic>
 #include <cerrno>
 #include <cstdint>
+#include <mutex>
 
 #include "fp_internal.h"
 
@@ -687,9 +688,8 @@ static bool encode_page_map(CUtensorMap* m, const uint8_t* d_buf, uint64_t bytes
                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                               CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
   static Encode fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  static std::once_flag once;
+  std::call_once(once, [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (!getenv("FP_NO_TMA") &&
@@ -697,7 +697,7 @@ static bool encode_page_map(CUtensorMap* m, const uint8_t* d_buf, uint64_t bytes
             cudaSuccess &&
         q == cudaDriverEntryPointSuccess)
       fn = reinterpret_cast<Encode>(p);
-  }
+  });
   if (!fn || ((uintptr_t)d_buf & 15) || bytes / 128 > (1ull << 32)) return false;
   const cuuint64_t dims[2] = {128, bytes / 128};
   const cuuint64_t strides[1] = {128};
