@@ -446,10 +446,19 @@ __global__ void __launch_bounds__(kCrcThreads)
   const uint32_t np = min(pages_per_chunk, n_pages - p0);
   const uint32_t r = 1u << log2r;
   const int64_t pad = (int64_t)kCrcThreads * r - np;  // zero pages in front
+  // Horner over this thread's r pages; the page CRCs of each block of 16 are
+  // loaded first (independent loads in flight), not one load per step
   uint32_t acc = 0;
-  for (uint32_t i = 0; i < r; ++i) {
-    const int64_t idx = (int64_t)threadIdx.x * r + i - pad;
-    acc = mul_tab(k0, acc) ^ (idx >= 0 ? page_crc[p0 + idx] : 0u);
+  for (uint32_t i0 = 0; i0 < r; i0 += 16) {
+    uint32_t pv[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int64_t idx = (int64_t)threadIdx.x * r + i0 + i - pad;
+      pv[i] = (i0 + i < r && idx >= 0) ? page_crc[p0 + idx] : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (i0 + i < r) acc = mul_tab(k0, acc) ^ pv[i];
   }
   red[threadIdx.x] = acc;
   __syncthreads();
