@@ -656,14 +656,9 @@ static bool smem_opt_in(K kernel, size_t bytes) {
   if (cudaGetDevice(&d) != cudaSuccess) return false;
   const uint64_t bit = 1ull << (d & 63);
   if (done.load(std::memory_order_acquire) & bit) return true;
-  if (bytes && cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)bytes) != cudaSuccess)
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
+      cudaSuccess)
     return false;
-  // every library kernel prefers the largest shared-memory carveout, so
-  // back-to-back pack / CRC / fold launches never wait for an L1 <-> shared
-  // reconfiguration of the SMs (the pack streams past L1 anyway)
-  cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                       (int)cudaSharedmemCarveoutMaxShared);
   done.fetch_or(bit, std::memory_order_acq_rel);
   return true;
 }
@@ -682,7 +677,6 @@ int pack_launch(int impl, const Item* d_items, uint32_t n_items, uint8_t* d_slab
     if (!smem_opt_in<0>(fp_pack_bulk, kBulkSmem)) return FP_ECUDA;
     fp_pack_bulk<<<grid, kBulkThreads, kBulkSmem, st>>>(d_items, n_items, d_slab);
   } else {
-    if (!smem_opt_in<4>(fp_pack_v4, 0)) return FP_ECUDA;
     fp_pack_v4<<<grid, kV4Threads, 0, st>>>(d_items, n_items, d_slab);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
@@ -746,7 +740,6 @@ int crc_launch(const uint8_t* d_buf, uint64_t bytes, uint64_t chunk_bytes, const
   uint32_t log2r = 0;
   while (((uint64_t)kCrcThreads << log2r) < per) ++log2r;
   if (log2r + 10 > kCrcPageLevels) return -EINVAL;
-  if (!smem_opt_in<5>(fp_crc_fold, 0)) return FP_ECUDA;
   fp_crc_fold<<<n_chunks, kCrcThreads, 0, st>>>(d_page_crc, ppc, n_pages, log2r, d_tabs,
                                                 d_chunk_crc);
   return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
@@ -776,7 +769,6 @@ int crc_fold_launch(const uint32_t* d_page_crc, uint64_t bytes, uint64_t chunk_b
   uint32_t log2r = 0;
   while (((uint64_t)kCrcThreads << log2r) < per) ++log2r;
   if (log2r + 10 > kCrcPageLevels) return -EINVAL;
-  if (!smem_opt_in<5>(fp_crc_fold, 0)) return FP_ECUDA;
   fp_crc_fold<<<n_chunks, kCrcThreads, 0, (cudaStream_t)stream>>>(d_page_crc, ppc, n_pages, log2r,
                                                                   d_tabs, d_chunk_crc);
   return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
