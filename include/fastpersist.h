@@ -188,7 +188,13 @@ typedef struct fp_ctx fp_ctx;
 
 /* Fill *cfg with the defaults above (env overrides: FP_RING_SLOTS,
  * FP_SLOT_BYTES, FP_SQE_BYTES, FP_QD, FP_IO_ENGINE=uring|pwrite|buffered|null|gds,
- * FP_PACK=v4|bulk|host|ce, FP_PACK_PRIO=low, FP_PACK_CTAS, FP_ALIGN, FP_PACK_BYTES). Returns 0.         */
+ * FP_PACK=v4|bulk|host|ce, FP_PACK_PRIO=low, FP_PACK_CTAS, FP_ALIGN, FP_PACK_BYTES,
+ * FP_WRITER_STRIDE, FP_CKPT_DIRS, FP_NO_CRC). Returns 0.
+ * Read at run time (not part of fp_config): FP_NO_TMA=1 (LSU page-CRC kernel
+ * instead of the TMA-staged one), FP_CRC_FUSED=1 (page CRCs inside the pack
+ * kernel, ablation), FP_NO_GATE=1 (no launch gate; automatic when a profiler
+ * is injected), FP_GDS_OPEN_TIMEOUT (s, default 20), FP_DEBUG_GDS=1,
+ * FP_FAULT_EIO_AT=<n>[@rank] (tests).                                          */
 int fp_config_default(fp_config *cfg);
 
 /* Create a context bound to CUDA device `cuda_device` (-1: host tensors only).
@@ -246,7 +252,8 @@ int fp_ckpt_load(fp_ctx *ctx, const fp_tensor *t, size_t n, const char *path,
 /* Parallel restore, the paper's two-step load (§4.2: each rank "(i)
  * loads its checkpoint partition, if any, into GPU memory, and (ii) performs
  * an allgather"): rank r reads ONLY its own shard file, in slot_bytes chunks
- * (O_DIRECT through the pinned ring, then H2D); every chunk of the replicated
+ * (O_DIRECT through the pinned ring, ring_slots chunks ahead, then H2D; with
+ * FP_IO_GDS, cuFileRead into device memory instead); every chunk of the replicated
  * partitions is exchanged with one comm->allgather_bytes call (bytes =
  * slot_bytes per rank; ranks whose partition is shorter send padding) and the
  * unpack kernel scatters the gathered bytes into t[i] on `stream`; the rank's
