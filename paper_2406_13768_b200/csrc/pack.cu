@@ -432,26 +432,23 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
   }
 }
 
-constexpr int kFoldThreads = 256;
-constexpr int kFoldLevels = 8;  // log2(kFoldThreads)
-
-__global__ void __launch_bounds__(kFoldThreads)
+__global__ void __launch_bounds__(kCrcThreads)
     fp_crc_fold(const uint32_t* __restrict__ page_crc, uint32_t pages_per_chunk, uint32_t n_pages,
                 uint32_t log2r, const uint32_t* __restrict__ tabs, uint32_t* __restrict__ out) {
-  __shared__ uint32_t k0[1024];                // x^(8*4096)
-  __shared__ uint32_t km[kFoldLevels][1024];   // x^(8*4096*2^(log2r+m))
-  __shared__ uint32_t wred[kFoldThreads / 32];
+  __shared__ uint32_t k0[1024];        // x^(8*4096)
+  __shared__ uint32_t km[10][1024];    // x^(8*4096*2^(log2r+m))
+  __shared__ uint32_t red[kCrcThreads];
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) k0[i] = tabs[kTabPage + i];
-  for (int i = threadIdx.x; i < kFoldLevels * 1024; i += blockDim.x)
+  for (int i = threadIdx.x; i < 10 * 1024; i += blockDim.x)
     km[i >> 10][i & 1023] = tabs[kTabPage + 1024 * (log2r + (i >> 10)) + (i & 1023)];
+  __syncthreads();
   const uint32_t p0 = blockIdx.x * pages_per_chunk;
   const uint32_t np = min(pages_per_chunk, n_pages - p0);
   const uint32_t r = 1u << log2r;
-  const int64_t pad = (int64_t)kFoldThreads * r - np;  // zero pages in front
-  // this thread's r pages: loaded 16 at a time (independent loads in flight)
-  // while the tables land, then Horner with the product by x^(8*4096)
+  const int64_t pad = (int64_t)kCrcThreads * r - np;  // zero pages in front
+  // Horner over this thread's r pages; the page CRCs of each block of 16 are
+  // loaded first (independent loads in flight), not one load per step
   uint32_t acc = 0;
-  bool first = true;
   for (uint32_t i0 = 0; i0 < r; i0 += 16) {
     uint32_t pv[16];
 #pragma unroll
@@ -459,32 +456,19 @@ __global__ void __launch_bounds__(kFoldThreads)
       const int64_t idx = (int64_t)threadIdx.x * r + i0 + i - pad;
       pv[i] = (i0 + i < r && idx >= 0) ? page_crc[p0 + idx] : 0u;
     }
-    if (first) {
-      __syncthreads();  // tables in shared memory
-      first = false;
-    }
 #pragma unroll
     for (int i = 0; i < 16; ++i)
       if (i0 + i < r) acc = mul_tab(k0, acc) ^ pv[i];
   }
-  // tree: 5 levels inside the warp (shuffles), 3 across the 8 warps
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-  for (int m = 0; m < 5; ++m) {
-    const uint32_t o = __shfl_down_sync(0xffffffffu, acc, 1 << m);
-    if ((lane & ((2 << m) - 1)) == 0) acc = mul_tab(km[m], acc) ^ o;
-  }
-  if (lane == 0) wred[w] = acc;
+  red[threadIdx.x] = acc;
   __syncthreads();
-  if (w == 0) {
-    acc = lane < kFoldThreads / 32 ? wred[lane] : 0u;
-#pragma unroll
-    for (int m = 5; m < kFoldLevels; ++m) {
-      const uint32_t o = __shfl_down_sync(0xffffffffu, acc, 1 << (m - 5));
-      if ((lane & ((2 << (m - 5)) - 1)) == 0) acc = mul_tab(km[m], acc) ^ o;
-    }
-    if (lane == 0) out[blockIdx.x] = acc;
+  for (int m = 0; (1 << m) < kCrcThreads; ++m) {
+    const int step = 1 << m;
+    if ((threadIdx.x & (2 * step - 1)) == 0)
+      red[threadIdx.x] = mul_tab(km[m], red[threadIdx.x]) ^ red[threadIdx.x + step];
+    __syncthreads();
   }
+  if (threadIdx.x == 0) out[blockIdx.x] = red[0];
 }
 
 // ---------------------------------------------------------------------------
@@ -754,9 +738,9 @@ int crc_launch(const uint8_t* d_buf, uint64_t bytes, uint64_t chunk_bytes, const
   const uint32_t n_chunks = (n_pages + ppc - 1) / ppc;
   const uint32_t per = std::min(ppc, n_pages);
   uint32_t log2r = 0;
-  while (((uint64_t)kFoldThreads << log2r) < per) ++log2r;
-  if (log2r + kFoldLevels > kCrcPageLevels) return -EINVAL;
-  fp_crc_fold<<<n_chunks, kFoldThreads, 0, st>>>(d_page_crc, ppc, n_pages, log2r, d_tabs,
+  while (((uint64_t)kCrcThreads << log2r) < per) ++log2r;
+  if (log2r + 10 > kCrcPageLevels) return -EINVAL;
+  fp_crc_fold<<<n_chunks, kCrcThreads, 0, st>>>(d_page_crc, ppc, n_pages, log2r, d_tabs,
                                                 d_chunk_crc);
   return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
 }
@@ -783,9 +767,9 @@ int crc_fold_launch(const uint32_t* d_page_crc, uint64_t bytes, uint64_t chunk_b
   const uint32_t n_chunks = (n_pages + ppc - 1) / ppc;
   const uint32_t per = std::min(ppc, n_pages);
   uint32_t log2r = 0;
-  while (((uint64_t)kFoldThreads << log2r) < per) ++log2r;
-  if (log2r + kFoldLevels > kCrcPageLevels) return -EINVAL;
-  fp_crc_fold<<<n_chunks, kFoldThreads, 0, (cudaStream_t)stream>>>(d_page_crc, ppc, n_pages, log2r,
+  while (((uint64_t)kCrcThreads << log2r) < per) ++log2r;
+  if (log2r + 10 > kCrcPageLevels) return -EINVAL;
+  fp_crc_fold<<<n_chunks, kCrcThreads, 0, (cudaStream_t)stream>>>(d_page_crc, ppc, n_pages, log2r,
                                                                   d_tabs, d_chunk_crc);
   return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
 }

@@ -44,17 +44,16 @@ int main() {
       if (pc[pg] != crc_raw_update(0, buf.data() + (size_t)pg * 4096, 4096)) { printf("page mismatch\n"); return 1; }
     }
     const uint32_t n_chunks = (n_pages + ppc - 1) / ppc, per = std::min(ppc, n_pages);
-    const int FT = 256;  // fp_crc_fold threads
-    uint32_t log2r = 0; while (((uint64_t)FT << log2r) < per) ++log2r;
+    uint32_t log2r = 0; while ((1024ull << log2r) < per) ++log2r;
     for (uint32_t ch = 0; ch < n_chunks; ++ch) {
       const uint32_t p0 = ch * ppc, np = std::min(ppc, n_pages - p0), r = 1u << log2r;
-      const int64_t pad = (int64_t)FT * r - np;
-      std::vector<uint32_t> red(FT);
-      for (int t = 0; t < FT; ++t) { uint32_t acc = 0;
+      const int64_t pad = 1024ll * r - np;
+      std::vector<uint32_t> red(1024);
+      for (int t = 0; t < 1024; ++t) { uint32_t acc = 0;
         for (uint32_t i = 0; i < r; ++i) { int64_t idx = (int64_t)t * r + i - pad; acc = mul_tab(&T[kTabPage], acc) ^ (idx >= 0 ? pc[p0 + idx] : 0u); }
         red[t] = acc; }
-      for (int m = 0; (1 << m) < FT; ++m) { int step = 1 << m;
-        for (int t = 0; t < FT; t += 2 * step) red[t] = mul_tab(&T[kTabPage + 1024 * (log2r + m)], red[t]) ^ red[t + step]; }
+      for (int m = 0; (1 << m) < 1024; ++m) { int step = 1 << m;
+        for (int t = 0; t < 1024; t += 2 * step) red[t] = mul_tab(&T[kTabPage + 1024 * (log2r + m)], red[t]) ^ red[t + step]; }
       if (red[0] != crc_raw_update(0, buf.data() + (size_t)p0 * 4096, (size_t)np * 4096)) { printf("chunk mismatch n=%u ppc=%u ch=%u\n", n_pages, ppc, ch); return 1; }
     }
   }
