@@ -418,7 +418,11 @@ def our_arm(a):
     # the drive is shared and its rate drifts (virtio disk on the gpurun box):
     # measure the roofline again right after the timed region; the roofline
     # is the best the device did in this run
-    nvme_after = nvme_roofline()
+    try:
+        nvme_after = nvme_roofline()
+    except Exception as e:  # noqa: BLE001 - the re-measure must not lose the line
+        print(f"bench: NVMe roofline after the steps failed: {e}", file=sys.stderr)
+        nvme_after = 0.0
     nvme_gbs = max(nvme_before, nvme_after)
 
     # pack kernel roofline: algorithmic bytes = 1 B read + 1 B written per slab
@@ -437,105 +441,122 @@ def our_arm(a):
     # tensors (identical bytes); vs the same-run O_DIRECT read roofline
     restore = None
     if not a.no_restore:
-        last = os.path.join(root, f"gen{(a.warmup + a.steps - 1) % 2}")
-        gr = fp.io_bench(root, nv_bytes, tag=rank, read=True, io_depth=a.qd,
-                         sqe_bytes=a.sqe_kib << 10, ring_slots=a.ring_slots,
-                         slot_bytes=a.slot_mib << 20)
-        nvme_read = allreduce_sum(gr, dev)
-        rl = []
-        for _ in range(a.restore_steps):
-            barrier()
-            torch.cuda.synchronize(dev)
-            t0 = time.perf_counter()
-            ck.load_parallel(ents, last, stream=stream)   # synchronous; checks the CRC
-            torch.cuda.synchronize(dev)
-            rl.append(allreduce_max(time.perf_counter() - t0, dev))
-        rt = statistics.median(rl)
-        restore = {"value": round(image_bytes / rt / 1e9, 4), "unit": "GB/s",
-                   "latency_s": round(rt, 4), "steps": len(rl),
-                   "nvme_read_gbs": round(nvme_read, 3),
-                   "frac": round(image_bytes / rt / 1e9 / nvme_read, 4),
-                   "call": "fp_ckpt_load_parallel (own shard O_DIRECT read-ahead over the "
-                           "pinned ring -> H2D -> all-gather -> unpack kernel, CRC-32 checked)",
-                   "roofline_how": f"fp_io_bench_read: O_DIRECT io_uring seq read, {a.qd} x "
-                                   f"{a.sqe_kib} KiB in flight, best of 2, {world} concurrent "
-                                   f"readers x {nv_bytes} B, same dir, same run"}
+        try:
+            last = os.path.join(root, f"gen{(a.warmup + a.steps - 1) % 2}")
+            gr = fp.io_bench(root, nv_bytes, tag=rank, read=True, io_depth=a.qd,
+                             sqe_bytes=a.sqe_kib << 10, ring_slots=a.ring_slots,
+                             slot_bytes=a.slot_mib << 20)
+            nvme_read = allreduce_sum(gr, dev)
+            rl = []
+            for _ in range(a.restore_steps):
+                barrier()
+                torch.cuda.synchronize(dev)
+                t0 = time.perf_counter()
+                ck.load_parallel(ents, last, stream=stream)   # synchronous; checks the CRC
+                torch.cuda.synchronize(dev)
+                rl.append(allreduce_max(time.perf_counter() - t0, dev))
+            rt = statistics.median(rl)
+            restore = {"value": round(image_bytes / rt / 1e9, 4), "unit": "GB/s",
+                       "latency_s": round(rt, 4), "steps": len(rl),
+                       "nvme_read_gbs": round(nvme_read, 3),
+                       "frac": round(image_bytes / rt / 1e9 / nvme_read, 4),
+                       "call": "fp_ckpt_load_parallel (own shard O_DIRECT read-ahead over the "
+                               "pinned ring -> H2D -> all-gather -> unpack kernel, CRC-32 checked)",
+                       "roofline_how": f"fp_io_bench_read: O_DIRECT io_uring seq read, {a.qd} x "
+                                       f"{a.sqe_kib} KiB in flight, best of 2, {world} concurrent "
+                                       f"readers x {nv_bytes} B, same dir, same run"}
+        except Exception as e:  # noqa: BLE001 - an optional measurement must not lose the line
+            print(f"bench: restore failed: {type(e).__name__}: {e}", file=sys.stderr)
+            restore = {"error": f"{type(e).__name__}: {e}"}
 
     # ---- e2e: public API with the state sourced from pinned HOST memory ------
     e2e = None
     if not a.no_e2e:
-        # this rank sources its share of the state from pinned host memory:
-        # tensors are dealt to ranks by the position of their middle byte in
-        # the state (rank r takes [r/N, (r+1)/N)), so across ranks every state
-        # byte crosses PCIe H2D exactly once per step and each rank pins ~1/N
-        mine, cum = [], 0
-        for _, t in state:
-            nb = t.numel() * t.element_size()
-            if int((cum + nb / 2) * world // state_bytes) == rank:
-                mine.append(t)
-            cum += nb
-        host = [torch.empty_like(t, device="cpu").pin_memory() for t in mine]
-        for h, t in zip(host, mine):
-            h.copy_(t)
-        my_h2d = sum(t.numel() * t.element_size() for t in mine)
-        torch.cuda.synchronize(dev)
-        ke = max(1, min(a.steps, a.e2e_steps))
-        barrier()
-        torch.cuda.synchronize(dev)
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        f0.record(stream)
-        for i in range(ke):
+        try:
+            # this rank sources its share of the state from pinned host memory:
+            # tensors are dealt to ranks by the position of their middle byte in
+            # the state (rank r takes [r/N, (r+1)/N)), so across ranks every state
+            # byte crosses PCIe H2D exactly once per step and each rank pins ~1/N
+            mine, cum = [], 0
+            for _, t in state:
+                nb = t.numel() * t.element_size()
+                if int((cum + nb / 2) * world // state_bytes) == rank:
+                    mine.append(t)
+                cum += nb
+            host = [torch.empty_like(t, device="cpu").pin_memory() for t in mine]
             for h, t in zip(host, mine):
-                t.copy_(h, non_blocking=True)          # H2D of this step's inputs
-            ck.begin(ents, os.path.join(root, f"gen{i % 2}"), stream=stream)
-            st = ck.wait()                             # result: durable status (host)
-        f1.record(stream)
-        torch.cuda.synchronize(dev)
-        barrier()
-        e_el = allreduce_max(f0.elapsed_time(f1) / 1e3, dev)
-        e2e = {"value": round(st["image_bytes"] * ke / e_el / 1e9, 4), "unit": "GB/s",
-               "h2d_bytes_per_step": int(allreduce_sum(my_h2d, dev)),
-               "d2h_bytes_per_step": int(st["image_bytes"]), "steps": ke,
-               "note": "timed: H2D of the whole state from pinned host memory, then "
-                       "begin/wait through the Python API (D2H of the image via the ring)"}
-        del host
+                h.copy_(t)
+            my_h2d = sum(t.numel() * t.element_size() for t in mine)
+            torch.cuda.synchronize(dev)
+            ke = max(1, min(a.steps, a.e2e_steps))
+            barrier()
+            torch.cuda.synchronize(dev)
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
+            for i in range(ke):
+                for h, t in zip(host, mine):
+                    t.copy_(h, non_blocking=True)          # H2D of this step's inputs
+                ck.begin(ents, os.path.join(root, f"gen{i % 2}"), stream=stream)
+                st = ck.wait()                             # result: durable status (host)
+            f1.record(stream)
+            torch.cuda.synchronize(dev)
+            barrier()
+            e_el = allreduce_max(f0.elapsed_time(f1) / 1e3, dev)
+            e2e = {"value": round(st["image_bytes"] * ke / e_el / 1e9, 4), "unit": "GB/s",
+                   "h2d_bytes_per_step": int(allreduce_sum(my_h2d, dev)),
+                   "d2h_bytes_per_step": int(st["image_bytes"]), "steps": ke,
+                   "note": "timed: H2D of the whole state from pinned host memory, then "
+                           "begin/wait through the Python API (D2H of the image via the ring)"}
+            del host
+        except Exception as e:  # noqa: BLE001 - an optional measurement must not lose the line
+            print(f"bench: e2e failed: {type(e).__name__}: {e}", file=sys.stderr)
+            e2e = {"error": f"{type(e).__name__}: {e}"}
 
     overhead = None
     if not a.no_overhead:
-        ovcfg = dict(cfg)
-        ovcfg["pack_ctas"] = a.overlap_ctas
-        with fp.Checkpointer(dev, **ovcfg) as cko:
-            overhead = synthetic_overhead(a, cko, ents, state, dev, rank, world, root,
-                                          shard_bytes / 1e9)
+        try:
+            ovcfg = dict(cfg)
+            ovcfg["pack_ctas"] = a.overlap_ctas
+            with fp.Checkpointer(dev, **ovcfg) as cko:
+                overhead = synthetic_overhead(a, cko, ents, state, dev, rank, world, root,
+                                              shard_bytes / 1e9)
+        except Exception as e:  # noqa: BLE001 - an optional measurement must not lose the line
+            print(f"bench: overhead failed: {type(e).__name__}: {e}", file=sys.stderr)
+            overhead = {"error": f"{type(e).__name__}: {e}"}
+
     ck.close()
     if rank == 0:
         shutil.rmtree(root, ignore_errors=True)
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        sample, _ = oracle_sample_tensors(specs, int(a.oracle_bytes))
-        croot = os.path.join(out_root(), "oracle")
-        os.makedirs(croot, exist_ok=True)
-        cg, ct, cimg = run_oracle_steps(sample, 1, croot)
-        # the paper's baseline: torch.save of the same tensors (host
-        # state dict) + fsync, as context for "speedup vs torch.save"
-        tsd = {s.name: t for s, t in sample}
-        fpath = os.path.join(croot, "torch_save.pt")
-        t0 = time.perf_counter()
-        with open(fpath, "wb") as f:
-            torch.save(tsd, f)
-            f.flush()
-            os.fsync(f.fileno())
-        ts_dt = time.perf_counter() - t0
-        ts_bytes = os.path.getsize(fpath)
-        shutil.rmtree(croot, ignore_errors=True)
-        cpu = {"value": round(cg, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
-               "sample": f"first {len(sample)} tensors of {CFG} ({cimg} image bytes), "
-                         "host-resident, buffered write()+fsync, 1 step",
-               "host_cores_available": cpu_cores(),
-               "torch_save_gbs": round(ts_bytes / ts_dt / 1e9, 4),
-               "torch_save_note": "context only: torch.save(state dict of the same sample) "
-                                  "+ fsync on the same file system (PAPER.md P:259 baseline)"}
+        try:
+            sample, _ = oracle_sample_tensors(specs, int(a.oracle_bytes))
+            croot = os.path.join(out_root(), "oracle")
+            os.makedirs(croot, exist_ok=True)
+            cg, ct, cimg = run_oracle_steps(sample, 1, croot)
+            # the paper's baseline: torch.save of the same tensors (host
+            # state dict) + fsync, as context for "speedup vs torch.save"
+            tsd = {s.name: t for s, t in sample}
+            fpath = os.path.join(croot, "torch_save.pt")
+            t0 = time.perf_counter()
+            with open(fpath, "wb") as f:
+                torch.save(tsd, f)
+                f.flush()
+                os.fsync(f.fileno())
+            ts_dt = time.perf_counter() - t0
+            ts_bytes = os.path.getsize(fpath)
+            shutil.rmtree(croot, ignore_errors=True)
+            cpu = {"value": round(cg, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                   "sample": f"first {len(sample)} tensors of {CFG} ({cimg} image bytes), "
+                             "host-resident, buffered write()+fsync, 1 step",
+                   "host_cores_available": cpu_cores(),
+                   "torch_save_gbs": round(ts_bytes / ts_dt / 1e9, 4),
+                   "torch_save_note": "context only: torch.save(state dict of the same sample) "
+                                      "+ fsync on the same file system (PAPER.md P:259 baseline)"}
+        except Exception as e:  # noqa: BLE001 - an optional measurement must not lose the line
+            print(f"bench: cpu_baseline failed: {type(e).__name__}: {e}", file=sys.stderr)
+            cpu = {"error": f"{type(e).__name__}: {e}"}
 
     if rank == 0:
         hbm = float(peaks["hbm_gbs"])
