@@ -38,7 +38,9 @@ if ROOT not in sys.path:
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
-CFG = "c2_gpt3_1.3b"
+# the workload BASELINE.json's metric is quoted on (configs[1]); FP_BENCH_CFG
+# exists only so the GPU test suite can exercise the full JSON line quickly
+CFG = os.environ.get("FP_BENCH_CFG", "c2_gpt3_1.3b")
 # test hook: all ranks on cuda:0 over gloo (exercises the N>1 code path on a
 # 1-GPU box; NCCL refuses two ranks on one device). Never used for numbers.
 SHARE_GPU = os.environ.get("FP_BENCH_SHARE_GPU") == "1"
@@ -378,7 +380,7 @@ def our_arm(a):
     fs = os.statvfs(root)
     free_now = fs.f_bavail * fs.f_frsize
     room = (free_now - 2.2 * img_total) / world
-    nv_bytes = int(max(2e9, min(nv_bytes, room * 0.8))) // 4096 * 4096
+    nv_bytes = int(min(nv_bytes, max(2e9, room * 0.8))) // 4096 * 4096
     barrier()
     os.sync()                                 # settle writeback of earlier runs first
 

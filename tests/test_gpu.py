@@ -398,3 +398,36 @@ def test_crc_pages_lsu_fallback_parity(tmp_path, monkeypatch):
     r = subprocess.run([sys.executable, "-c", code, str(tmp_path)], capture_output=True, text=True,
                        env=env, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
+
+
+def test_bench_json_line_contract(tmp_path):
+    """bench.py's own arm end to end on the GPU (small workload): one JSON line
+    with every key of the driver contract and the roofline / cpu_baseline /
+    e2e / restore objects this tier asks for."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, FP_BENCH_CFG="c1_tiny", FP_BENCH_DIR=str(tmp_path))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--steps", "2", "--warmup", "3",
+                        "--no-overhead", "--nvme-bytes", "2e8", "--oracle-bytes", "2e7"],
+                       capture_output=True, text=True, env=env, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks", "restore"):
+        assert k in d, k
+    assert d["value"] > 0 and d["steps"] == 2 and d["gpu_launches"] > 0
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in d["roofline"], k
+    assert d["roofline"]["achieved"] > 0
+    for k in ("value", "unit", "cores", "kind", "sample"):
+        assert k in d["cpu_baseline"], k
+    for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
+        assert k in d["e2e"], k
+    assert d["restore"]["value"] > 0, d["restore"]
+    for k in ("sm_mhz", "sm_max_mhz", "reasons"):
+        assert k in d["clocks"], k
