@@ -5,9 +5,13 @@
 // linear in the data: R(A||B) = R(A)*x^(8|B|) xor R(B) (mod P), zero bytes
 // contribute nothing and leading zeros are invisible. A standard CRC is
 // recovered as crc(M) = R(M) xor crc(0^|M|). Polynomial products are done in
-// the reflected bit order (bit 31 = x^0), as in zlib's crc32_combine.
+// the reflected bit order (bit 31 = x^0). gf_mul and gf_x8n are the standard
+// GF(2) routines zlib uses for crc32_combine (zlib's crc32.c multmodp and
+// x2nmodp, permissive zlib license), restated here.
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <mutex>
 
 #include "fp_internal.h"
 
@@ -29,14 +33,14 @@ uint32_t gf_mul(uint32_t a, uint32_t b) {
 }
 
 static uint32_t x2n[32];  // x^(2^k) mod P
-static bool x2n_ready = false;
+static std::once_flag x2n_once;
 
 static void init_x2n() {
-  if (x2n_ready) return;
-  uint32_t p = 1u << 30;  // x^1
-  x2n[0] = p;
-  for (int k = 1; k < 32; ++k) x2n[k] = p = gf_mul(p, p);
-  x2n_ready = true;
+  std::call_once(x2n_once, [] {
+    uint32_t p = 1u << 30;  // x^1
+    x2n[0] = p;
+    for (int k = 1; k < 32; ++k) x2n[k] = p = gf_mul(p, p);
+  });
 }
 
 uint32_t gf_x8n(uint64_t n) {  // x^(8n) mod P
@@ -52,18 +56,18 @@ uint32_t gf_x8n(uint64_t n) {  // x^(8n) mod P
 }
 
 static uint32_t tab[8][256];
-static bool tab_ready = false;
+static std::once_flag tab_once;
 
 static void init_tab() {
-  if (tab_ready) return;
-  for (uint32_t b = 0; b < 256; ++b) {
-    uint32_t c = b;
-    for (int i = 0; i < 8; ++i) c = (c & 1) ? (c >> 1) ^ kPoly : c >> 1;
-    tab[0][b] = c;
-  }
-  for (int t = 1; t < 8; ++t)
-    for (uint32_t b = 0; b < 256; ++b) tab[t][b] = (tab[t - 1][b] >> 8) ^ tab[0][tab[t - 1][b] & 0xFF];
-  tab_ready = true;
+  std::call_once(tab_once, [] {
+    for (uint32_t b = 0; b < 256; ++b) {
+      uint32_t c = b;
+      for (int i = 0; i < 8; ++i) c = (c & 1) ? (c >> 1) ^ kPoly : c >> 1;
+      tab[0][b] = c;
+    }
+    for (int t = 1; t < 8; ++t)
+      for (uint32_t b = 0; b < 256; ++b) tab[t][b] = (tab[t - 1][b] >> 8) ^ tab[0][tab[t - 1][b] & 0xFF];
+  });
 }
 
 const uint32_t* crc_tables8() {
@@ -103,12 +107,97 @@ std::vector<uint32_t> crc_device_tables() {
   std::vector<uint32_t> t(kTabWords, 0);
   for (int k = 0; k < 4; ++k) memcpy(&t[kTabS4 + 256 * k], tab[k], 256 * 4);
   for (uint32_t v = 0; v < kLaneLevels; ++v) mul_tables(gf_x8n(32ull << v), &t[kTabLane + 1024 * v]);
-  for (uint32_t j = 0; j < kCrcPageLevels; ++j) mul_tables(gf_x8n(4096ull << j), &t[kTabPage + 1024 * j]);
   return t;
 }
 
 uint32_t crc_zeros(uint64_t n) {  // standard CRC-32 of n zero bytes
   return gf_mul(gf_x8n(n), 0xFFFFFFFFu) ^ 0xFFFFFFFFu;
+}
+
+// ---------------------------------------------------------------------------
+// ExtentCrc
+// ---------------------------------------------------------------------------
+static uint32_t page_tab[1024];  // product by x^(8*4096), four 256-entry tables
+static std::once_flag page_tab_once;
+
+static inline uint32_t mul_page(uint32_t a) {
+  return page_tab[a & 255] ^ page_tab[256 + ((a >> 8) & 255)] ^ page_tab[512 + ((a >> 16) & 255)] ^
+         page_tab[768 + (a >> 24)];
+}
+
+void ExtentCrc::reset(const std::vector<Extent>& ext) {
+  std::call_once(page_tab_once, [] { mul_tables(gf_x8n(4096), page_tab); });
+  beg_.clear();
+  len_.clear();
+  for (const Extent& e : ext) {
+    beg_.push_back(e.file_off);
+    len_.push_back(e.len);
+  }
+  done_.assign(beg_.size(), 0);
+  raw_.assign(beg_.size(), 0);
+  cur_ = 0;
+  ok_ = true;
+}
+
+size_t ExtentCrc::find(uint64_t fo) {
+  if (cur_ >= beg_.size() || fo < beg_[cur_]) cur_ = 0;
+  while (cur_ < beg_.size() && fo >= beg_[cur_] + len_[cur_]) ++cur_;
+  return cur_;
+}
+
+bool ExtentCrc::pages_ok(uint64_t fo, uint64_t n) const {
+  if (fo % 4096 || n % 4096) return false;
+  for (size_t i = 0; i < beg_.size(); ++i) {
+    const uint64_t b = beg_[i], e = beg_[i] + len_[i];
+    if ((b > fo && b < fo + n && b % 4096) || (e > fo && e < fo + n && e % 4096)) return false;
+  }
+  return true;
+}
+
+void ExtentCrc::add_pages(uint64_t fo, const uint32_t* pc, uint64_t n_pages) {
+  for (uint64_t p = 0; p < n_pages; ++p, fo += 4096) {
+    const size_t i = find(fo);
+    if (i >= beg_.size() || fo != beg_[i] + done_[i] || done_[i] + 4096 > len_[i]) {
+      ok_ = false;
+      return;
+    }
+    raw_[i] = mul_page(raw_[i]) ^ pc[p];
+    done_[i] += 4096;
+  }
+}
+
+void ExtentCrc::add_bytes(uint64_t fo, const uint8_t* p, uint64_t n) {
+  while (n) {
+    const size_t i = find(fo);
+    if (i >= beg_.size() || fo != beg_[i] + done_[i]) {
+      ok_ = false;
+      return;
+    }
+    const uint64_t m = std::min<uint64_t>(n, len_[i] - done_[i]);
+    raw_[i] = crc_raw_update(raw_[i], p, m);
+    done_[i] += m;
+    fo += m;
+    p += m;
+    n -= m;
+  }
+}
+
+bool ExtentCrc::complete() const {
+  for (size_t i = 0; i < beg_.size(); ++i)
+    if (done_[i] != len_[i]) return false;
+  return ok_;
+}
+
+uint32_t ExtentCrc::extent_crc(size_t i) const { return raw_[i] ^ crc_zeros(len_[i]); }
+
+uint32_t ExtentCrc::file_crc() const {
+  uint32_t r = 0;
+  uint64_t tot = 0;
+  for (size_t i = 0; i < beg_.size(); ++i) {
+    r = gf_mul(gf_x8n(len_[i]), r) ^ raw_[i];
+    tot += len_[i];
+  }
+  return r ^ crc_zeros(tot);
 }
 
 }  // namespace fp

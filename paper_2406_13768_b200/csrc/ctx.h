@@ -98,7 +98,11 @@ struct fp_ctx {
   int fault_rank = -1;
   // CRC-32 of the shard
   uint32_t* d_crc_tabs = nullptr;  // crc_device_tables() blob
-  uint32_t *d_page_crc = nullptr, *d_chunk_crc = nullptr, *h_crc = nullptr;
+  uint32_t* d_page_crc = nullptr;  // page CRCs of one pack group (device)
+  uint32_t* h_pcrc = nullptr;      // pinned: page CRCs of each ring slot's chunk
+  fp::ExtentCrc xcrc;              // this rank's shard, per extent, file order
+  uint32_t ext_crc[2] = {0, 0};    // per-extent CRC-32 of the last checkpoint
+  uint32_t n_ext_crc = 0;
   IoEngine* io = nullptr;
   int pack_ctas = 0;
   // GPUDirect Storage (FP_IO_GDS): writer pool, per-half events
@@ -106,7 +110,7 @@ struct fp_ctx {
   bool gds = false, gds_p2p = false, gds_slab_registered = false;
   fp::GdsPool* gds_pool = nullptr;
   cudaEvent_t gds_ev[6] = {};
-  uint32_t* h_gds_crc = nullptr;
+  uint32_t* h_gds_pcrc = nullptr;  // pinned page CRCs of both slab halves
   // plan cache
   bool planned = false;
   uint64_t sig_meta = 0, sig_ptr = 0;
@@ -128,7 +132,9 @@ struct fp_ctx {
   size_t d_hdr_cap = 0;
   std::vector<uint8_t> h_hdr;
   std::vector<std::vector<Extent>> all_extents;
-  std::vector<uint64_t> shard_crcs;  // per rank: bit 32 = valid, low 32 = CRC-32
+  // per rank, 3 words: whole shard, extent 0, extent 1 (bit 32 = valid,
+  // low 32 = CRC-32)
+  std::vector<uint64_t> shard_crcs;
   // request
   std::string shard_dir, manifest_dir;
   int rank = 0, k = 1;
@@ -143,8 +149,8 @@ struct fp_ctx {
   double t_begin = 0;
 
   int save_shard();
-  int save_shard_gds(int fd, uint32_t* shard_raw);
-  int finish_shard(int fd, int status, uint32_t shard_raw, double t0);
+  int save_shard_gds(int fd);
+  int finish_shard(int fd, int status, double t0);
   void helper();
   int write_manifest();
 };

@@ -159,27 +159,22 @@ int pack_default_ctas(int impl, int device);
 // reaches `value` (or max_ns passes; then *d_timed_out = 1 if non-null)
 int flag_wait_launch(const uint32_t* d_flag, uint32_t value, uint64_t max_ns,
                      uint32_t* d_timed_out, void* stream);
-// raw CRC-32 of d_buf[0, bytes) per chunk_bytes chunk -> d_chunk_crc[]
-// (bytes, chunk_bytes: multiples of 4096; d_page_crc: bytes/4096 entries of
-// scratch; d_tabs: the blob of crc_device_tables; chunk <= 2^29 pages / 1024)
-int crc_launch(const uint8_t* d_buf, uint64_t bytes, uint64_t chunk_bytes, const uint32_t* d_tabs,
-               uint32_t* d_page_crc, uint32_t* d_chunk_crc, void* stream);
-// fused pack + page CRCs (fp_pack_crc): items of n_tiles 32 KiB slab tiles
-// (tile t = items [d_tile_lo[t], d_tile_lo[t+1]), none crossing a tile
-// boundary) -> d_slab, raw CRC of each of the first n_pages pages ->
-// d_page_crc; then crc_fold_launch folds them per chunk_bytes chunk
+// raw CRC-32 (init 0, no xorout) of every 4 KiB page of d_buf[0, bytes)
+// -> d_page_crc[bytes / 4096] (bytes: a multiple of 4096; d_tabs: the blob of
+// crc_device_tables); the host folds them (ExtentCrc)
+int crc_pages_launch(const uint8_t* d_buf, uint64_t bytes, const uint32_t* d_tabs,
+                     uint32_t* d_page_crc, void* stream);
+// fused pack + page CRCs (fp_pack_crc, ablation): items of n_tiles 32 KiB slab
+// tiles (tile t = items [d_tile_lo[t], d_tile_lo[t+1]), none crossing a tile
+// boundary) -> d_slab, raw CRC of each of the first n_pages pages -> d_page_crc
 int pack_crc_launch(const Item* d_items, const uint32_t* d_tile_lo, uint32_t n_tiles,
                     uint8_t* d_slab, uint32_t n_pages, const uint32_t* d_tabs,
                     uint32_t* d_page_crc, int ctas, void* stream);
-int crc_fold_launch(const uint32_t* d_page_crc, uint64_t bytes, uint64_t chunk_bytes,
-                    const uint32_t* d_tabs, uint32_t* d_chunk_crc, void* stream);
 // device CRC table blob layout (uint32 offsets)
-constexpr uint32_t kCrcPageLevels = 20;
 constexpr uint32_t kTabS4 = 0;
 constexpr uint32_t kTabLane = 4 * 256;
 constexpr uint32_t kLaneLevels = 7;  // products by x^(8*32*2^v), v = 0..6
-constexpr uint32_t kTabPage = kTabLane + kLaneLevels * 1024;
-constexpr uint32_t kTabWords = kTabPage + kCrcPageLevels * 1024;
+constexpr uint32_t kTabWords = kTabLane + kLaneLevels * 1024;
 
 // ---------------------------------------------------------------------------
 // CRC-32 helpers (crc32.cpp)
@@ -189,7 +184,36 @@ uint32_t gf_x8n(uint64_t n);                      // x^(8n) mod P
 uint32_t crc_raw_update(uint32_t c, const uint8_t* p, uint64_t n);
 uint32_t crc_zeros(uint64_t n);                   // standard CRC-32 of n zero bytes
 const uint32_t* crc_tables8();                    // 8 x 256 slicing tables, contiguous
-// the kTabWords-word blob fp_crc_pages / fp_crc_fold read (layout: pack.cu)
+// the kTabWords-word blob fp_crc_pages reads (layout: pack.cu)
 std::vector<uint32_t> crc_device_tables();
+
+// Raw CRC-32 of a file accumulated per extent, in file order. The
+// GPU delivers one raw CRC per 4 KiB page; the host folds them with one
+// constant product per page (R <- R * x^(8*4096) ^ page), so the manifest can
+// carry a CRC per extent (what a partial reader such as fp_ckpt_load verifies)
+// and per file. Runs that are not page-foldable (ragged tails, extents not on
+// 4 KiB boundaries) are added as bytes.
+class ExtentCrc {
+ public:
+  void reset(const std::vector<Extent>& ext);  // extents in file order
+  // [fo, fo + n) can be added as page CRCs: page-aligned, and every extent
+  // boundary inside it is a page boundary
+  bool pages_ok(uint64_t fo, uint64_t n) const;
+  void add_pages(uint64_t fo, const uint32_t* page_crc, uint64_t n_pages);
+  void add_bytes(uint64_t fo, const uint8_t* p, uint64_t n);
+  size_t n() const { return beg_.size(); }
+  uint64_t len(size_t i) const { return len_[i]; }
+  bool complete(size_t i) const { return ok_ && done_[i] == len_[i]; }
+  bool complete() const;
+  uint32_t extent_crc(size_t i) const;  // standard CRC-32 (= zlib.crc32) of extent i
+  uint32_t file_crc() const;            // standard CRC-32 of the whole file
+  bool ok() const { return ok_; }       // false if a run arrived out of order
+ private:
+  size_t find(uint64_t fo);
+  std::vector<uint64_t> beg_, len_, done_;
+  std::vector<uint32_t> raw_;
+  size_t cur_ = 0;
+  bool ok_ = true;
+};
 
 }  // namespace fp

@@ -268,7 +268,7 @@ int gds_wait(GdsPool* pool, double* stall) { return pool->wait_all(stall); }
 // ---------------------------------------------------------------------------
 // save: pack groups double-buffered in the device slab, cuFileWrite each
 // ---------------------------------------------------------------------------
-int fp_ctx::save_shard_gds(int fd, uint32_t* shard_raw) {
+int fp_ctx::save_shard_gds(int fd) {
   using namespace fp;
   void* fh = nullptr;
   int r = gds_handle_open(fd, &fh);
@@ -281,7 +281,7 @@ int fp_ctx::save_shard_gds(int fd, uint32_t* shard_raw) {
   const bool gpu_crc = want_crc && S % 4096 == 0 && d_crc_tabs;
   const uint64_t piece = std::max<uint64_t>(cfg.sqe_bytes, 4ull << 20);
   int status = 0;
-  uint32_t raw = 0;
+  const uint64_t PPG = P / 4096 + 1;  // page CRC entries per slab half
   auto enqueue = [&](uint64_t g) -> int {
     const int h = (int)(g & 1);
     const uint64_t c0 = g * G, c1 = std::min<uint64_t>(c0 + G, C);
@@ -302,14 +302,11 @@ int fp_ctx::save_shard_gds(int fd, uint32_t* shard_raw) {
     CK(cudaEventRecord(gds_ev[3 * h + 1], stream));
     st.kernel_launches += 1;
     if (gpu_crc) {
-      rr = fused ? crc_fold_launch(d_page_crc, round_up(gbytes, 4096), S, d_crc_tabs, d_chunk_crc,
-                                   stream)
-                 : crc_launch(slab, round_up(gbytes, 4096), S, d_crc_tabs, d_page_crc, d_chunk_crc,
-                              stream);
+      rr = fused ? 0 : crc_pages_launch(slab, round_up(gbytes, 4096), d_crc_tabs, d_page_crc, stream);
       if (rr) return rr;
-      CK(cudaMemcpyAsync(h_gds_crc + (size_t)h * (G + 1), d_chunk_crc, (c1 - c0) * 4,
+      CK(cudaMemcpyAsync(h_gds_pcrc + (size_t)h * PPG, d_page_crc, round_up(gbytes, 4096) / 4096 * 4,
                          cudaMemcpyDeviceToHost, stream));
-      st.kernel_launches += fused ? 1 : 2;
+      st.kernel_launches += fused ? 0 : 1;
     }
     CK(cudaEventRecord(gds_ev[3 * h + 2], stream));
     ++st.pack_launches;
@@ -338,9 +335,8 @@ int fp_ctx::save_shard_gds(int fd, uint32_t* shard_raw) {
     if (want_crc) {
       for (uint64_t c = c0; c < c1; ++c) {
         const uint64_t len = std::min<uint64_t>(S, plan.shard_bytes - c * S);
-        uint32_t rc;
-        if (gpu_crc && len % 4096 == 0) {
-          rc = h_gds_crc[(size_t)h * (G + 1) + (c - c0)];
+        if (gpu_crc && len % 4096 == 0 && xcrc.pages_ok(c * S, len)) {
+          xcrc.add_pages(c * S, h_gds_pcrc + (size_t)h * PPG + (c - c0) * (S / 4096), len / 4096);
         } else {  // ragged last chunk (4 KiB-aligned shards never take this)
           std::vector<uint8_t> tmp(len);
           if (cudaMemcpy(tmp.data(), d_slab + (size_t)h * P + (c - c0) * S, len,
@@ -348,9 +344,8 @@ int fp_ctx::save_shard_gds(int fd, uint32_t* shard_raw) {
             status = FP_ECUDA;
             break;
           }
-          rc = crc_raw_update(0, tmp.data(), len);
+          xcrc.add_bytes(c * S, tmp.data(), len);
         }
-        raw = gf_mul(gf_x8n(len), raw) ^ rc;
       }
       if (status) break;
     }
@@ -362,6 +357,5 @@ int fp_ctx::save_shard_gds(int fd, uint32_t* shard_raw) {
   }
   cudaStreamSynchronize(stream);  // never leave a pack writing into the slab
   gds_handle_close(fh);
-  *shard_raw = raw;
   return status;
 }

@@ -272,6 +272,108 @@ class ReadAhead {
   int status_ = 0;
 };
 
+// Page CRCs of the chunks a load copies to the device (fp_crc_pages over the
+// H2D'd bytes), folded on the host in chunk order: chunk j's page
+// CRCs land in the pinned slot j % R of ctx->h_pcrc; that slot's previous
+// chunk (j - R, the oldest one pending) is folded first. A chunk that cannot
+// be folded as pages (ragged, or an extent boundary inside a page) is folded
+// from the host bytes by the caller after flush().
+class LoadCrc {
+ public:
+  using FoldFn = std::function<void(uint64_t chunk, const uint32_t* pages)>;
+  LoadCrc(fp_ctx* c, FoldFn fn)
+      : c_(c), R_(c->cfg.ring_slots), pps_(std::max<uint64_t>(1, c->cfg.slot_bytes / 4096)),
+        fn_(std::move(fn)), pend_(R_, -1) {}
+  // page CRCs of d_buf[0, len) (len % 4096 == 0) for chunk j, on stream st
+  int enqueue(uint64_t j, const uint8_t* d_buf, uint64_t len, cudaStream_t st) {
+    const uint32_t s = (uint32_t)(j % R_);
+    int r = fold_slot(s);
+    if (r) return r;
+    if (crc_pages_launch(d_buf, len, c_->d_crc_tabs, c_->d_page_crc, st) ||
+        cudaMemcpyAsync(c_->h_pcrc + s * pps_, c_->d_page_crc, len / 4096 * 4,
+                        cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaEventRecord(c_->ev_c1[s], st) != cudaSuccess)
+      return FP_ECUDA;
+    pend_[s] = (int64_t)j;
+    ++launches_;
+    return 0;
+  }
+  // fold every pending chunk, oldest first
+  int flush() {
+    for (;;) {
+      int64_t best = -1;
+      uint32_t bs = 0;
+      for (uint32_t s = 0; s < R_; ++s)
+        if (pend_[s] >= 0 && (best < 0 || pend_[s] < best)) best = pend_[s], bs = s;
+      if (best < 0) return 0;
+      int r = fold_slot(bs);
+      if (r) return r;
+    }
+  }
+  uint64_t launches() const { return launches_; }
+
+ private:
+  int fold_slot(uint32_t s) {
+    if (pend_[s] < 0) return 0;
+    if (cudaEventSynchronize(c_->ev_c1[s]) != cudaSuccess) return FP_ECUDA;
+    fn_((uint64_t)pend_[s], c_->h_pcrc + s * pps_);
+    pend_[s] = -1;
+    return 0;
+  }
+  fp_ctx* c_;
+  uint32_t R_;
+  uint64_t pps_;
+  FoldFn fn_;
+  std::vector<int64_t> pend_;
+  uint64_t launches_ = 0;
+};
+
+// manifest CRC records of shard w: "crc32" (whole file) and "extent_crc32"
+struct ShardCrcRec {
+  bool has_file = false;
+  uint32_t file = 0;
+  std::vector<int64_t> ext;  // -1 = absent
+};
+ShardCrcRec crc_record(const JVal& m, int w, size_t n_ext) {
+  ShardCrcRec r;
+  r.ext.assign(n_ext, -1);
+  const JVal* sh = m.get("shards");
+  if (!sh || sh->t != JVal::ARR || (size_t)w >= sh->arr.size()) return r;
+  const JVal& rec = sh->arr[w];
+  if (const JVal* f = rec.get("crc32"))
+    if (f->t == JVal::NUM) r.has_file = true, r.file = (uint32_t)f->num;
+  if (const JVal* e = rec.get("extent_crc32"))
+    if (e->t == JVal::ARR && e->arr.size() == n_ext)
+      for (size_t i = 0; i < n_ext; ++i)
+        if (e->arr[i].t == JVal::NUM) r.ext[i] = (int64_t)(uint32_t)e->arr[i].num;
+  return r;
+}
+
+// Compare what was read of shard `name` with its manifest record: every
+// extent read whole against its extent CRC, the whole file against "crc32".
+// Returns 0 or FP_ECORRUPT (naming the shard and extent on stderr).
+int verify_crc(const ExtentCrc& acc, const ShardCrcRec& rec, const std::string& name) {
+  if (!acc.ok()) {
+    fprintf(stderr, "fastpersist: %s: CRC runs out of order (internal error)\n", name.c_str());
+    return FP_ECORRUPT;
+  }
+  for (size_t i = 0; i < acc.n(); ++i) {
+    if (!acc.complete(i) || rec.ext[i] < 0) continue;
+    const uint32_t got = acc.extent_crc(i);
+    if (got != (uint32_t)rec.ext[i]) {
+      fprintf(stderr, "fastpersist: %s extent %zu CRC-32 %08x != manifest %08x (corrupt data)\n",
+              name.c_str(), i, got, (unsigned)rec.ext[i]);
+      return FP_ECORRUPT;
+    }
+  }
+  if (rec.has_file && acc.complete() && acc.file_crc() != rec.file) {
+    fprintf(stderr, "fastpersist: %s CRC-32 %08x != manifest %08x (corrupt data)\n", name.c_str(),
+            acc.file_crc(), rec.file);
+    return FP_ECORRUPT;
+  }
+  return 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -469,37 +571,86 @@ int fp_ckpt_load(fp_ctx* c, const fp_tensor* t, size_t n, const char* path, int 
   const uint64_t C = lo.size() - 1;
   cudaStream_t st = (cudaStream_t)stream;
   int status = 0;
+  // load-stream chunk ch -> runs {offset in chunk, shard, file offset, bytes},
+  // cut wherever the source shard or extent changes
+  struct Run {
+    uint64_t pos;
+    int w;
+    uint64_t fo, n;
+  };
+  auto chunk_runs = [&](uint64_t ch, std::vector<Run>* out) -> int {
+    out->clear();
+    const uint64_t len = std::min<uint64_t>(S, total - ch * S);
+    for (uint64_t pos = 0; pos < len;) {
+      const uint64_t ls = ch * S + pos;  // load-stream offset -> image offset
+      uint64_t io = 0, lavail = 0;
+      for (auto& e : lp.extents)
+        if (ls >= e.file_off && ls < e.file_off + e.len) {
+          io = e.image_off + (ls - e.file_off);
+          lavail = e.file_off + e.len - ls;
+        }
+      int w;
+      uint64_t fo, avail;
+      if (!lavail || !locate(io, &w, &fo, &avail)) return FP_ECORRUPT;
+      const uint64_t nn = std::min<uint64_t>({len - pos, avail, lavail});
+      out->push_back({pos, w, fo, nn});
+      pos += nn;
+    }
+    return 0;
+  };
+  // integrity: every extent read whole is checked against the
+  // manifest's per-extent CRC-32 (page CRCs of each H2D'd chunk on the GPU,
+  // folded per shard extent on the host)
+  const bool want_crc = !(c->cfg.flags & FP_CFG_NO_CRC);
+  std::vector<ExtentCrc> acc(dp_size);
+  std::vector<ShardCrcRec> recs(dp_size);
+  for (int w = 0; w < dp_size; ++w) {
+    acc[w].reset(c->all_extents[w]);
+    recs[w] = crc_record(m, w, c->all_extents[w].size());
+  }
+  std::vector<Run> fold_runs;
+  LoadCrc lcrc(c, [&](uint64_t ch, const uint32_t* pages) {
+    if (chunk_runs(ch, &fold_runs)) return;
+    for (const Run& u : fold_runs) acc[u.w].add_pages(u.fo, pages + u.pos / 4096, u.n / 4096);
+  });
   {
     // chunk ch = [ch*S, ch*S+len) of the load stream, read from whichever
     // shard holds each piece, R chunks ahead of the GPU scatter
+    std::vector<Run> rr;
     ReadAhead ra(c, C, !c->host, [&](uint64_t ch, std::vector<ReadReq>* out) -> int {
-      const uint64_t len = std::min<uint64_t>(S, total - ch * S);
-      for (uint64_t pos = 0; pos < len;) {
-        const uint64_t ls = ch * S + pos;  // load-stream offset -> image offset
-        uint64_t io = 0;
-        for (auto& e : lp.extents)
-          if (ls >= e.file_off && ls < e.file_off + e.len) io = e.image_off + (ls - e.file_off);
-        int w;
-        uint64_t fo, avail;
-        if (!locate(io, &w, &fo, &avail)) return FP_ECORRUPT;
-        const uint32_t nn = (uint32_t)std::min<uint64_t>({SQ, len - pos, avail});
-        out->push_back({fds[w], fo, pos, nn});
-        pos += nn;
-      }
+      int e = chunk_runs(ch, &rr);
+      if (e) return e;
+      for (const Run& u : rr)
+        for (uint64_t o = 0; o < u.n; o += SQ)
+          out->push_back({fds[u.w], u.fo + o, u.pos + o, (uint32_t)std::min<uint64_t>(SQ, u.n - o)});
       return 0;
     });
+    std::vector<Run> cr;
     for (uint64_t ch = 0; ch < C && !status; ++ch) {
       const uint32_t s = (uint32_t)(ch % c->cfg.ring_slots);
       const uint64_t len = std::min<uint64_t>(S, total - ch * S);
       status = ra.wait(ch);
       if (status) break;
       const uint8_t* slot = ra.slot_of(ch);
+      bool pages = false;
+      if (want_crc) {
+        status = chunk_runs(ch, &cr);
+        if (status) break;
+        pages = !c->host && c->d_crc_tabs && len % 4096 == 0;
+        for (const Run& u : cr)
+          pages = pages && u.pos % 4096 == 0 && u.n % 4096 == 0 && acc[u.w].pages_ok(u.fo, u.n);
+        if (!pages) {  // host bytes, in order behind every pending page fold
+          status = lcrc.flush();
+          for (const Run& u : cr) acc[u.w].add_bytes(u.fo, slot + u.pos, u.n);
+        }
+      }
       if (c->host) {
         for (uint32_t i = lo[ch]; i < lo[ch + 1]; ++i)
           if (items[i].src)
             memcpy((void*)(uintptr_t)items[i].src, slot + items[i].dst, items[i].len);
       } else if (cudaMemcpyAsync(c->d_slab, slot, len, cudaMemcpyHostToDevice, st) != cudaSuccess ||
                  cudaEventRecord(c->ev_d2h[s], st) != cudaSuccess ||
+                 (pages && lcrc.enqueue(ch, c->d_slab, len, st)) ||
                  unpack_launch(d_items + lo[ch], lo[ch + 1] - lo[ch], c->d_slab, c->pack_ctas,
                                st)) {
         status = FP_ECUDA;
@@ -508,6 +659,9 @@ int fp_ckpt_load(fp_ctx* c, const fp_tensor* t, size_t n, const char* path, int 
     }
   }  // ~ReadAhead drains reads still in flight (error paths)
   if (!c->host && cudaStreamSynchronize(st) != cudaSuccess && !status) status = FP_ECUDA;
+  if (!status) status = lcrc.flush();
+  for (int w = 0; w < dp_size && !status && want_crc; ++w)
+    status = verify_crc(acc[w], recs[w], shard_file(w, dp_size));
   if (d_items) cudaFree(d_items);
   close_all();
   return status;
@@ -516,7 +670,6 @@ int fp_ckpt_load(fp_ctx* c, const fp_tensor* t, size_t n, const char* path, int 
 // ---------------------------------------------------------------------------
 // parallel load: own shard only + one all-gather per chunk + unpack
 // ---------------------------------------------------------------------------
-static size_t total_chunks_hint(uint64_t nrep, uint64_t nloc) { return (size_t)(nrep + nloc); }
 
 static int status_min(fp_ctx* c, int k, int s) {
   if (k <= 1) return s;
@@ -689,20 +842,12 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
       memcpy(out->data() + (a - h0), buf + base + (a - io0), b - a);
   };
   const uint64_t total_chunks = nrep + nloc;
-  // CRC-32 of the own shard as it is read, checked against the manifest
-  const JVal* shard_rec = nullptr;
-  if (const JVal* sh = m.get("shards"))
-    if (sh->t == JVal::ARR && (int)sh->arr.size() == k) shard_rec = &sh->arr[rank];
-  const JVal* want_crc = shard_rec ? shard_rec->get("crc32") : nullptr;
-  const bool check_crc = want_crc && want_crc->t == JVal::NUM && !(c->cfg.flags & FP_CFG_NO_CRC);
-  uint32_t* chunk_crc = nullptr;  // raw CRC per chunk (pinned when the GPU computes it)
-  std::vector<uint64_t> chunk_len(total_chunks_hint(nrep, nloc), 0);
-  bool crc_pinned = false;
-  if (check_crc) {
-    crc_pinned = dev && cudaHostAlloc(&chunk_crc, (chunk_len.size() + 1) * 4,
-                                      cudaHostAllocPortable) == cudaSuccess;
-    if (!crc_pinned) chunk_crc = (uint32_t*)calloc(chunk_len.size() + 1, 4);
-  }
+  // CRC-32 of the own shard as it is read (page CRCs on the GPU, folded per
+  // extent on the host), checked against the manifest
+  const bool check_crc = !(c->cfg.flags & FP_CFG_NO_CRC);
+  ExtentCrc acc;
+  acc.reset(c->all_extents[rank]);
+  const ShardCrcRec rec = crc_record(m, rank, c->all_extents[rank].size());
   const bool run = status == 0;  // agreed on every rank by the all-reduce above
   // this rank's bytes of chunk j: (length, offset in the own shard file)
   auto my_span = [&](uint64_t j, uint64_t* foff) -> uint64_t {
@@ -715,6 +860,11 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
     *foff = part_bytes(rank) + jj * CH;
     return std::min(CH, lreg_len - jj * CH);
   };
+  LoadCrc lcrc(c, [&](uint64_t j, const uint32_t* pages) {
+    uint64_t fo = 0;
+    const uint64_t n = my_span(j, &fo);
+    acc.add_pages(fo, pages, n / 4096);
+  });
   // own-shard reads run R chunks ahead of the exchange + scatter
   ReadAhead ra(c, run && !use_gds ? total_chunks : 0, dev,
                [&](uint64_t j, std::vector<ReadReq>* out) -> int {
@@ -731,7 +881,12 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
     uint8_t* slot = ra.slot_of(j);
     uint64_t foff = 0;
     const uint64_t mylen = my_span(j, &foff);
-    const bool gpu_crc = check_crc && dev && mylen % 4096 == 0 && c->d_crc_tabs;
+    const bool gpu_crc =
+        check_crc && dev && mylen % 4096 == 0 && c->d_crc_tabs && acc.pages_ok(foff, mylen);
+    auto host_crc = [&](const uint8_t* p) {  // in order behind the pending page folds
+      if (lcrc.flush() && !status) status = FP_ECUDA;
+      acc.add_bytes(foff, p, mylen);
+    };
     uint8_t* sbuf = use_gds ? send + (j & 1) * CH : send;
     if (use_gds) {
       // the unpack of chunk j-2 read this half: wait for it, then read into it
@@ -747,24 +902,20 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
         if (cudaMemcpy(slot, sbuf, mylen, cudaMemcpyDeviceToHost) != cudaSuccess)
           status = FP_ECUDA;
         else
-          chunk_crc[j] = crc_raw_update(0, slot, mylen);
+          host_crc(slot);
       }
     } else {
       int rr = status ? 0 : ra.wait(j);
       if (rr && !status) status = rr;  // keep exchanging so the collectives stay matched
-      if (check_crc && mylen && !gpu_crc) chunk_crc[j] = crc_raw_update(0, slot, mylen);
+      if (check_crc && mylen && !gpu_crc && !status) host_crc(slot);
     }
-    chunk_len[j] = mylen;
     if (dev) {
       if (!use_gds) {
         if (mylen && cudaMemcpyAsync(send, slot, mylen, cudaMemcpyHostToDevice, st) != cudaSuccess)
           status = status ? status : FP_ECUDA;
         cudaEventRecord(c->ev_d2h[s], st);
       }
-      if (gpu_crc && mylen &&
-          (crc_launch(sbuf, mylen, mylen, c->d_crc_tabs, c->d_page_crc, c->d_chunk_crc, st) ||
-           cudaMemcpyAsync(&chunk_crc[j], c->d_chunk_crc, 4, cudaMemcpyDeviceToHost, st) !=
-               cudaSuccess))
+      if (gpu_crc && mylen && lcrc.enqueue(j, sbuf, mylen, st))
         status = status ? status : FP_ECUDA;
     } else if (mylen) {
       memcpy(send, slot, mylen);
@@ -803,25 +954,10 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
   }
   ra.finish();  // reads still in flight after an error land before the ring is reused
   if (dev && cudaStreamSynchronize(st) != cudaSuccess && !status) status = FP_ECUDA;
-  if (!status && check_crc && run) {
-    uint32_t raw = 0;
-    uint64_t tot = 0;
-    for (size_t j = 0; j < chunk_len.size(); ++j) {
-      if (!chunk_len[j]) continue;
-      raw = gf_mul(gf_x8n(chunk_len[j]), raw) ^ chunk_crc[j];
-      tot += chunk_len[j];
-    }
-    const uint32_t got = raw ^ crc_zeros(tot);
-    if (got != (uint32_t)want_crc->num) {
-      fprintf(stderr, "fastpersist: shard %s CRC-32 %08x != manifest %08x (corrupt data)\n",
-              sf.c_str(), got, (unsigned)want_crc->num);
-      status = FP_ECORRUPT;
-    }
+  if (!status && run && check_crc) {
+    status = lcrc.flush();
+    if (!status) status = verify_crc(acc, rec, sf);
   }
-  if (crc_pinned)
-    cudaFreeHost(chunk_crc);
-  else
-    free(chunk_crc);
   if (!status && (memcmp(ghdr_got.data(), p.ghdr.bytes.data(), ghdr_got.size()) ||
                   memcmp(lhdr_got.data(), p.lhdr.bytes.data(), lhdr_got.size()))) {
     fprintf(stderr, "fastpersist: header bytes gathered from the shards do not match the "

@@ -243,16 +243,14 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
 //                 are combined in a shuffle tree, R(A||B) = R(A)*x^(8|B|) ^ R(B),
 //                 the constant product of level v (|B| = 128*2^v bytes) done
 //                 with four 256-entry tables.
-//  fp_crc_fold  : one raw CRC per chunk from its page CRCs. A block folds the
-//                 chunk padded at the FRONT to 1024*r pages (leading zeros are
-//                 invisible to a raw CRC): thread t runs Horner over r pages
-//                 (x^(8*4096) tables), then a 10-level tree over the block
-//                 (x^(8*4096*r*2^m) tables).
+// The page CRCs go to the host, which folds them per extent in file order
+// (ExtentCrc, crc32.cpp: one constant product per page) — a per-chunk fold
+// kernel (one block per 64 MiB chunk, 4 of 148 SMs busy for ~15 us) was the
+// round-1 design.
 //
 // Device table blob (uint32, built by crc_device_tables on the host):
 //   [kTabS4 .. +1024)   slicing-by-4 tables t[k][b] (b followed by k bytes)
 //   [kTabLane + 1024 v) product by x^(8*32*2^v),   v = 0..6
-//   [kTabPage + 1024 j) product by x^(8*4096*2^j), j = 0..19
 // each product table is four 256-entry tables: M[i][b] = K * (b << 8i).
 // ---------------------------------------------------------------------------
 constexpr int kCrcThreads = 1024;
@@ -430,45 +428,6 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
     }
     if (lane == 0) out[pg] = cl;
   }
-}
-
-__global__ void __launch_bounds__(kCrcThreads)
-    fp_crc_fold(const uint32_t* __restrict__ page_crc, uint32_t pages_per_chunk, uint32_t n_pages,
-                uint32_t log2r, const uint32_t* __restrict__ tabs, uint32_t* __restrict__ out) {
-  __shared__ uint32_t k0[1024];        // x^(8*4096)
-  __shared__ uint32_t km[10][1024];    // x^(8*4096*2^(log2r+m))
-  __shared__ uint32_t red[kCrcThreads];
-  for (int i = threadIdx.x; i < 1024; i += blockDim.x) k0[i] = tabs[kTabPage + i];
-  for (int i = threadIdx.x; i < 10 * 1024; i += blockDim.x)
-    km[i >> 10][i & 1023] = tabs[kTabPage + 1024 * (log2r + (i >> 10)) + (i & 1023)];
-  __syncthreads();
-  const uint32_t p0 = blockIdx.x * pages_per_chunk;
-  const uint32_t np = min(pages_per_chunk, n_pages - p0);
-  const uint32_t r = 1u << log2r;
-  const int64_t pad = (int64_t)kCrcThreads * r - np;  // zero pages in front
-  // Horner over this thread's r pages; the page CRCs of each block of 16 are
-  // loaded first (independent loads in flight), not one load per step
-  uint32_t acc = 0;
-  for (uint32_t i0 = 0; i0 < r; i0 += 16) {
-    uint32_t pv[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int64_t idx = (int64_t)threadIdx.x * r + i0 + i - pad;
-      pv[i] = (i0 + i < r && idx >= 0) ? page_crc[p0 + idx] : 0u;
-    }
-#pragma unroll
-    for (int i = 0; i < 16; ++i)
-      if (i0 + i < r) acc = mul_tab(k0, acc) ^ pv[i];
-  }
-  red[threadIdx.x] = acc;
-  __syncthreads();
-  for (int m = 0; (1 << m) < kCrcThreads; ++m) {
-    const int step = 1 << m;
-    if ((threadIdx.x & (2 * step - 1)) == 0)
-      red[threadIdx.x] = mul_tab(km[m], red[threadIdx.x]) ^ red[threadIdx.x + step];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) out[blockIdx.x] = red[0];
 }
 
 // ---------------------------------------------------------------------------
@@ -717,14 +676,12 @@ static bool encode_page_map(CUtensorMap* m, const uint8_t* d_buf, uint64_t bytes
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int crc_launch(const uint8_t* d_buf, uint64_t bytes, uint64_t chunk_bytes, const uint32_t* d_tabs,
-               uint32_t* d_page_crc, uint32_t* d_chunk_crc, void* stream) {
+int crc_pages_launch(const uint8_t* d_buf, uint64_t bytes, const uint32_t* d_tabs,
+                     uint32_t* d_page_crc, void* stream) {
   if (!bytes) return 0;
-  if (bytes % 4096 || chunk_bytes % 4096) return -EINVAL;
+  if (bytes % 4096) return -EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
-  if (!smem_opt_in<1>(fp_crc_pages, kCrcPagesSmem)) return FP_ECUDA;
   const uint32_t n_pages = (uint32_t)(bytes / 4096);
-  const uint32_t ppc = (uint32_t)(chunk_bytes / 4096);
   CUtensorMap tmap;
   if (encode_page_map(&tmap, d_buf, bytes)) {
     if (!smem_opt_in<2>(fp_crc_pages_tma, kCtSmem)) return FP_ECUDA;
@@ -732,16 +689,10 @@ int crc_launch(const uint8_t* d_buf, uint64_t bytes, uint64_t chunk_bytes, const
                                              (uint32_t)sm_count(-1));
     fp_crc_pages_tma<<<grid, kCtWarps * 32, kCtSmem, st>>>(tmap, n_pages, d_tabs, d_page_crc);
   } else {
+    if (!smem_opt_in<1>(fp_crc_pages, kCrcPagesSmem)) return FP_ECUDA;
     const int grid_p = (int)std::min<uint32_t>((n_pages + 31) / 32, (uint32_t)sm_count(-1));
     fp_crc_pages<<<grid_p, kCrcThreads, kCrcPagesSmem, st>>>(d_buf, n_pages, d_tabs, d_page_crc);
   }
-  const uint32_t n_chunks = (n_pages + ppc - 1) / ppc;
-  const uint32_t per = std::min(ppc, n_pages);
-  uint32_t log2r = 0;
-  while (((uint64_t)kCrcThreads << log2r) < per) ++log2r;
-  if (log2r + 10 > kCrcPageLevels) return -EINVAL;
-  fp_crc_fold<<<n_chunks, kCrcThreads, 0, st>>>(d_page_crc, ppc, n_pages, log2r, d_tabs,
-                                                d_chunk_crc);
   return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
 }
 
@@ -755,22 +706,6 @@ int pack_crc_launch(const Item* d_items, const uint32_t* d_tile_lo, uint32_t n_t
   fp_pack_crc<<<grid, kPcThreads, kPcSmem, (cudaStream_t)stream>>>(d_items, d_tile_lo, n_tiles,
                                                                   d_slab, n_pages, d_tabs,
                                                                   d_page_crc);
-  return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
-}
-
-int crc_fold_launch(const uint32_t* d_page_crc, uint64_t bytes, uint64_t chunk_bytes,
-                    const uint32_t* d_tabs, uint32_t* d_chunk_crc, void* stream) {
-  if (!bytes) return 0;
-  if (bytes % 4096 || chunk_bytes % 4096) return -EINVAL;
-  const uint32_t n_pages = (uint32_t)(bytes / 4096);
-  const uint32_t ppc = (uint32_t)(chunk_bytes / 4096);
-  const uint32_t n_chunks = (n_pages + ppc - 1) / ppc;
-  const uint32_t per = std::min(ppc, n_pages);
-  uint32_t log2r = 0;
-  while (((uint64_t)kCrcThreads << log2r) < per) ++log2r;
-  if (log2r + 10 > kCrcPageLevels) return -EINVAL;
-  fp_crc_fold<<<n_chunks, kCrcThreads, 0, (cudaStream_t)stream>>>(d_page_crc, ppc, n_pages, log2r,
-                                                                  d_tabs, d_chunk_crc);
   return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
 }
 

@@ -105,8 +105,16 @@ int fp_ctx::save_shard() {
   if (!manifest_dir.empty()) {
     // invalidate a manifest of an older generation before any byte of this
     // one lands (readers never see a manifest over torn shards)
+    // and make the unlink durable before the first shard byte is rewritten,
+    // so a power loss mid-write cannot bring the old manifest back over torn
+    // shards (§3.2: the checkpoint is persistent only when committed)
     std::string m = join_path(manifest_dir, "manifest.json");
-    if (unlink(m.c_str()) && errno != ENOENT) return -errno;
+    if (unlink(m.c_str()) == 0) {
+      err = fsync_dir(manifest_dir);
+      if (err) return err;
+    } else if (errno != ENOENT) {
+      return -errno;
+    }
   }
   const std::string file = cfg.io_engine == FP_IO_NULL ? std::string("/dev/null")
                                                         : join_path(shard_dir, shard_file(rank, k));
@@ -137,9 +145,9 @@ int fp_ctx::save_shard() {
   if (gds && !host) {  // device slab -> cuFileWrite, no host ring
     st.engine = FP_IO_GDS;
     st.fallback = gds_p2p ? 0 : 2;
-    uint32_t raw = 0;
-    const int status = save_shard_gds(fd, &raw);
-    return finish_shard(fd, status, raw, t0);
+    xcrc.reset(plan.extents);
+    const int status = save_shard_gds(fd);
+    return finish_shard(fd, status, t0);
   }
   const uint64_t C = item_lo.size() - 1;
   std::vector<uint32_t> slot_out(R, 0);
@@ -179,11 +187,13 @@ int fp_ctx::save_shard() {
   // behind the previous group's copies)
   const bool slabless = cfg.pack_impl == FP_PACK_HOST || cfg.pack_impl == FP_PACK_CE;
   const uint64_t G = host || slabless ? 1 : std::max<uint64_t>(1, cfg.pack_bytes / S);
-  // CRC: raw CRC per chunk (GPU: from the packed slab; otherwise the CPU over
-  // the ring slot), folded in file order: R = R * x^(8 len) ^ R_chunk
+  // CRC: raw CRC per 4 KiB page on the GPU (from the packed slab), folded by
+  // the host per extent in file order (ExtentCrc); host state, slabless packs
+  // and ragged chunks: the CPU over the ring slot
   const bool want_crc = !(cfg.flags & FP_CFG_NO_CRC);
   const bool gpu_crc = want_crc && !host && !slabless && S % 4096 == 0 && d_crc_tabs;
-  uint32_t shard_raw = 0;
+  const uint64_t PPS = S / 4096;  // pages per slot
+  xcrc.reset(plan.extents);
   // default: fp_pack_v4, then fp_crc_pages_tma over the slab; FP_CRC_FUSED=1
   // computes the page CRCs inside the pack (fp_pack_crc, ablation: measured
   // slower)
@@ -247,7 +257,7 @@ int fp_ctx::save_shard() {
         gate_on = gated = false;  // could not launch the gate: run ungated from now on
         cudaGetLastError();
       }
-      st.kernel_launches += (gated ? 1 : 0) + 1 + (gpu_crc ? (fused ? 1 : 2) : 0);
+      st.kernel_launches += (gated ? 1 : 0) + 1 + (gpu_crc && !fused ? 1 : 0);
       // the gate is opened on every path out of this block: a stream left
       // waiting on it would never drain
       int r = cudaEventRecord(ev_p0[s], stream) == cudaSuccess ? 0 : FP_ECUDA;
@@ -260,11 +270,8 @@ int fp_ctx::save_shard() {
         r = pack_launch(cfg.pack_impl, d_items + item_lo[c], item_lo[c1] - item_lo[c], d_slab,
                         pack_ctas, stream);
       if (!r && cudaEventRecord(ev_p1[s], stream) != cudaSuccess) r = FP_ECUDA;
-      if (!r && gpu_crc)
-        r = fused ? crc_fold_launch(d_page_crc, round_up(gbytes, 4096), S, d_crc_tabs,
-                                    d_chunk_crc, stream)
-                  : crc_launch(d_slab, round_up(gbytes, 4096), S, d_crc_tabs, d_page_crc,
-                               d_chunk_crc, stream);
+      if (!r && gpu_crc && !fused)
+        r = crc_pages_launch(d_slab, round_up(gbytes, 4096), d_crc_tabs, d_page_crc, stream);
       if (!r && gpu_crc && cudaEventRecord(ev_c1[s], stream) != cudaSuccess) r = FP_ECUDA;
       if (gated) __atomic_store_n(&h_sig[0], ++gate_seq, __ATOMIC_RELEASE);  // open the gate
       if (r) return r;
@@ -274,8 +281,9 @@ int fp_ctx::save_shard() {
     }
     CK(cudaEventRecord(ev_d0[s], stream));
     CK(cudaMemcpyAsync(slot, d_slab + (c - g0) * S, len, cudaMemcpyDeviceToHost, stream));
-    if (gpu_crc)
-      CK(cudaMemcpyAsync(&h_crc[s], d_chunk_crc + (c - g0), 4, cudaMemcpyDeviceToHost, stream));
+    if (gpu_crc && len % 4096 == 0)
+      CK(cudaMemcpyAsync(h_pcrc + s * PPS, d_page_crc + (c - g0) * PPS, len / 4096 * 4,
+                         cudaMemcpyDeviceToHost, stream));
     CK(cudaEventRecord(ev_d2h[s], stream));
     return 0;
   };
@@ -295,8 +303,11 @@ int fp_ctx::save_shard() {
     }
     uint8_t* slot = ring + (size_t)s * S;
     if (want_crc) {
-      const uint32_t rc = gpu_crc && len % 4096 == 0 ? h_crc[s] : crc_raw_update(0, slot, len);
-      shard_raw = gf_mul(gf_x8n(len), shard_raw) ^ rc;
+      const uint64_t fo = c * S;
+      if (gpu_crc && len % 4096 == 0 && xcrc.pages_ok(fo, len))
+        xcrc.add_pages(fo, h_pcrc + s * PPS, len / 4096);
+      else
+        xcrc.add_bytes(fo, slot, len);
     }
     for (uint64_t off = 0; off < len; off += SQ) {
       const uint32_t n = (uint32_t)std::min<uint64_t>(SQ, len - off);
@@ -355,11 +366,11 @@ int fp_ctx::save_shard() {
     }
   }
   if (!host && stream) cudaStreamSynchronize(stream);  // never leave D2H into the ring pending
-  return finish_shard(fd, status, shard_raw, t0);
+  return finish_shard(fd, status, t0);
 }
 
 // durability (a7) + close + CRC finalisation, shared by the ring and GDS paths
-int fp_ctx::finish_shard(int fd, int status, uint32_t shard_raw, double t0) {
+int fp_ctx::finish_shard(int fd, int status, double t0) {
   if (status == 0 && !(cfg.flags & FP_CFG_NO_FSYNC)) {
     const double tf = now_s();
     NvtxRange nvf("fp.fdatasync");
@@ -368,9 +379,12 @@ int fp_ctx::finish_shard(int fd, int status, uint32_t shard_raw, double t0) {
   }
   if (close(fd) && status == 0) status = -errno;
   st.shard_bytes = plan.shard_bytes;
-  if (status == 0 && !(cfg.flags & FP_CFG_NO_CRC)) {
-    st.shard_crc32 = shard_raw ^ crc_zeros(plan.shard_bytes);
+  n_ext_crc = 0;
+  if (status == 0 && !(cfg.flags & FP_CFG_NO_CRC) && xcrc.complete()) {
+    st.shard_crc32 = xcrc.file_crc();
     st.crc_valid = 1;
+    n_ext_crc = (uint32_t)std::min<size_t>(xcrc.n(), 2);
+    for (uint32_t i = 0; i < n_ext_crc; ++i) ext_crc[i] = xcrc.extent_crc(i);
   }
   st.t_helper = now_s() - t0;
   return status;
@@ -417,9 +431,21 @@ int fp_ctx::write_manifest() {
              r, shard_file(r, k).c_str(), roots.empty() ? (size_t)0 : r % roots.size(),
              (unsigned long long)bytes);
     j += buf;
-    if ((size_t)r < shard_crcs.size() && (shard_crcs[r] >> 32)) {
-      snprintf(buf, sizeof(buf), "\"crc32\": %u, ", (unsigned)(shard_crcs[r] & 0xFFFFFFFFu));
+    if (3 * (size_t)r + 2 < shard_crcs.size() && (shard_crcs[3 * r] >> 32)) {
+      snprintf(buf, sizeof(buf), "\"crc32\": %u, ", (unsigned)(shard_crcs[3 * r] & 0xFFFFFFFFu));
       j += buf;
+      // one CRC-32 per extent (what a reader of part of the shard verifies)
+      bool all = all_extents[r].size() <= 2;
+      for (size_t i = 0; i < all_extents[r].size() && all; ++i) all = shard_crcs[3 * r + 1 + i] >> 32;
+      if (all) {
+        j += "\"extent_crc32\": [";
+        for (size_t i = 0; i < all_extents[r].size(); ++i) {
+          snprintf(buf, sizeof(buf), "%s%u", i ? ", " : "",
+                   (unsigned)(shard_crcs[3 * r + 1 + i] & 0xFFFFFFFFu));
+          j += buf;
+        }
+        j += "], ";
+      }
     }
     j += "\"extents\": [";
     for (size_t i = 0; i < all_extents[r].size(); ++i) {
@@ -486,16 +512,31 @@ int fp::ensure_plan(fp_ctx* c, const fp_tensor* t, size_t n, int rank, int k) {
   std::vector<TensorRef> rep, loc;
   bool host = false;
   int r = import_tensors(t, n, rank, &rep, &loc, &host);
-  if (r) return r;
-  if (!host && c->dev < 0) {
+  if (!r && !host && c->dev < 0) {
     bool any = false;
     for (size_t i = 0; i < n; ++i) any |= t[i].nbytes > 0;
-    if (any) return FP_ENODEV;
+    if (any) r = FP_ENODEV;
   }
   const uint32_t A = c->cfg.alignment;
-  const uint64_t sm = sig_hash(rep, loc, rank, k, A, c->cfg.writer_stride, false);
-  const uint64_t sp = sig_hash(rep, loc, rank, k, A, c->cfg.writer_stride, true) ^ (host ? 1 : 0);
-  const bool new_meta = !c->planned || sm != c->sig_meta;
+  const uint64_t sm = r ? 0 : sig_hash(rep, loc, rank, k, A, c->cfg.writer_stride, false);
+  const uint64_t sp = r ? 0 : sig_hash(rep, loc, rank, k, A, c->cfg.writer_stride, true) ^ (host ? 1 : 0);
+  bool new_meta = !c->planned || sm != c->sig_meta;
+  if (k > 1) {
+    // The replan decision is collective: one all-reduce(MIN) of
+    // {error < 0 | 0 = my signature changed | 1 = unchanged}, so either every
+    // rank runs the all-gather below or none does (a rank whose local
+    // tensors alone changed, or that failed to import, must not leave its
+    // peers in a mismatched collective).
+    if (!c->has_comm) return -EINVAL;
+    int32_t v = r ? r : (new_meta ? 0 : 1);
+    if (c->comm.allreduce_min_i32(c->comm.ctx, &v)) return r ? r : FP_ECOMM;
+    if (v < 0) {
+      c->planned = false;
+      return r ? r : v;  // some rank failed: every rank fails with it
+    }
+    new_meta = v == 0;
+  }
+  if (r) return r;
   if (new_meta) {
     LocalFacts mine;
     plan_local_facts(rep, loc, A, &mine);
@@ -503,7 +544,6 @@ int fp::ensure_plan(fp_ctx* c, const fp_tensor* t, size_t n, int rank, int k) {
     if (k > 1) {
       std::vector<uint64_t> send = {mine.region_bytes, mine.n_local, mine.digest, mine.rep_bytes};
       std::vector<uint64_t> recv(4 * (size_t)k);
-      if (!c->has_comm) return -EINVAL;
       if (c->comm.allgather_u64(c->comm.ctx, send.data(), recv.data(), 4)) return FP_ECOMM;
       for (int q = 0; q < k; ++q)
         all[q] = {recv[4 * q], recv[4 * q + 1], recv[4 * q + 2], recv[4 * q + 3]};
@@ -768,8 +808,8 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
     if (c->gds) {
       c->gds_slab_registered = gds_buf_register(c->d_slab, slab_bytes) == 0;  // best effort
       c->gds_pool = gds_pool_new(std::min<uint32_t>(cfg.io_depth, 16), cuda_device);
-      const uint64_t G = cfg.pack_bytes / cfg.slot_bytes;
-      if (cudaHostAlloc(&c->h_gds_crc, 2 * (G + 1) * 4, cudaHostAllocPortable) != cudaSuccess)
+      if (cudaHostAlloc(&c->h_gds_pcrc, 2 * (cfg.pack_bytes / 4096 + 1) * 4,
+                        cudaHostAllocPortable) != cudaSuccess)
         return fail(-ENOMEM);
       for (auto& e : c->gds_ev)
         if (cudaEventCreate(&e) != cudaSuccess) return fail(FP_ECUDA);
@@ -809,20 +849,24 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
       c->h_sig = (volatile uint32_t*)hg;
       if (cudaHostGetDevicePointer(&dg, hg, 0) != cudaSuccess) return fail(FP_ECUDA);
       c->d_sig = (uint32_t*)dg;
-      // the gate relies on asynchronous launches: a profiler that serialises
-      // kernels (ncu, injected through CUDA_INJECTION64_PATH) would run the
-      // gate kernel to its timeout before the host could open it
-      c->gate_on = !getenv("FP_NO_GATE") && !getenv("CUDA_INJECTION64_PATH");
+      // The launch gate is measurement machinery (opt-in, FP_LAUNCH_GATE=1:
+      // bench.py turns it on so the CUDA events around each pack time the
+      // kernel, not the host's launch latency on an idle stream). It relies
+      // on asynchronous launches: a profiler that serialises kernels (ncu,
+      // injected through CUDA_INJECTION64_PATH) would run the gate kernel to
+      // its timeout before the host could open it, so it is off there.
+      c->gate_on = env_u64("FP_LAUNCH_GATE", 0) == 1 && !getenv("FP_NO_GATE") &&
+                   !getenv("CUDA_INJECTION64_PATH");
     }
     // CRC tables (slicing + constant-product tables, crc_device_tables) and
     // scratch: page CRCs of one pack group, chunk CRCs
     {
       const std::vector<uint32_t> tabs = crc_device_tables();
-      const uint64_t pages = cfg.pack_bytes / 4096 + 1, chunks = cfg.pack_bytes / cfg.slot_bytes + 1;
+      const uint64_t pages = cfg.pack_bytes / 4096 + 1;
+      const uint64_t pps = std::max<uint64_t>(1, cfg.slot_bytes / 4096);
       if (cudaMalloc(&c->d_crc_tabs, tabs.size() * 4) != cudaSuccess ||
           cudaMalloc(&c->d_page_crc, pages * 4) != cudaSuccess ||
-          cudaMalloc(&c->d_chunk_crc, chunks * 4) != cudaSuccess ||
-          cudaHostAlloc(&c->h_crc, cfg.ring_slots * 4, cudaHostAllocPortable) != cudaSuccess)
+          cudaHostAlloc(&c->h_pcrc, cfg.ring_slots * pps * 4, cudaHostAllocPortable) != cudaSuccess)
         return fail(-ENOMEM);
       if (cudaMemcpy(c->d_crc_tabs, tabs.data(), tabs.size() * 4, cudaMemcpyHostToDevice) !=
           cudaSuccess)
@@ -906,13 +950,15 @@ int fp_ckpt_wait(fp_ctx* c, fp_stats* out) {
   }
   // per-shard CRC-32 of every rank for the manifest (status is agreed, so
   // either every rank gathers or none does)
-  c->shard_crcs.assign(c->k, 0);
+  c->shard_crcs.assign(3 * (size_t)c->k, 0);
   if (status == 0) {
-    const uint64_t mine = c->st.crc_valid ? ((1ull << 32) | c->st.shard_crc32) : 0;
+    uint64_t mine[3] = {c->st.crc_valid ? ((1ull << 32) | c->st.shard_crc32) : 0, 0, 0};
+    for (uint32_t i = 0; c->st.crc_valid && i < c->n_ext_crc; ++i)
+      mine[1 + i] = (1ull << 32) | c->ext_crc[i];
     if (c->k > 1) {
-      if (c->comm.allgather_u64(c->comm.ctx, &mine, c->shard_crcs.data(), 1)) status = FP_ECOMM;
+      if (c->comm.allgather_u64(c->comm.ctx, mine, c->shard_crcs.data(), 3)) status = FP_ECOMM;
     } else {
-      c->shard_crcs[0] = mine;
+      std::copy(mine, mine + 3, c->shard_crcs.begin());
     }
   }
   const bool agreed_ok = status == 0;  // the same on every rank
@@ -978,15 +1024,14 @@ void fp_ckpt_destroy(fp_ctx* c) {
     if (c->gds_pool) gds_pool_delete(c->gds_pool);
     for (cudaEvent_t e : c->gds_ev)
       if (e) cudaEventDestroy(e);
-    if (c->h_gds_crc) cudaFreeHost(c->h_gds_crc);
+    if (c->h_gds_pcrc) cudaFreeHost(c->h_gds_pcrc);
     if (c->gds_slab_registered) gds_buf_deregister(c->d_slab);
     if (c->d_slab) cudaFree(c->d_slab);
     if (c->d_items) cudaFree(c->d_items);
     if (c->d_tiles) cudaFree(c->d_tiles);
     if (c->d_crc_tabs) cudaFree(c->d_crc_tabs);
     if (c->d_page_crc) cudaFree(c->d_page_crc);
-    if (c->d_chunk_crc) cudaFree(c->d_chunk_crc);
-    if (c->h_crc) cudaFreeHost(c->h_crc);
+    if (c->h_pcrc) cudaFreeHost(c->h_pcrc);
     if (c->h_sig) cudaFreeHost((void*)c->h_sig);
     if (c->d_hdr) cudaFree(c->d_hdr);
     if (c->ring_cuda_registered) cudaHostUnregister(c->ring);

@@ -232,7 +232,13 @@ class _CallbackComm:
 
 
 class _Comm:
-    """fp_comm callbacks over a torch.distributed group (NCCL or gloo)."""
+    """fp_comm callbacks over a torch.distributed group (NCCL or gloo).
+
+    The two tiny control collectives (plan all-gather, status all-reduce) run
+    on a private side stream when the group is NCCL: their host read-back then
+    waits for the collective only, never for the caller's queued fwd/bwd or
+    optimizer kernels (wait() is called before the optimizer, begin() after
+    it: neither may drain the compute stream)."""
 
     def __init__(self, group, device):
         import torch.distributed as dist
@@ -240,6 +246,7 @@ class _Comm:
         self.group = group
         be = dist.get_backend(group)
         self.dev = device if be == "nccl" else torch.device("cpu")
+        self.side = torch.cuda.Stream(self.dev) if self.dev.type == "cuda" else None
         self.world = dist.get_world_size(group)
         self.device = device
         self.ag = AGFN(self._allgather)
@@ -270,12 +277,17 @@ class _Comm:
             print(f"fastpersist: allgather_bytes failed: {e}")
             return -1
 
+    def _ctl(self):
+        import contextlib
+        return torch.cuda.stream(self.side) if self.side is not None else contextlib.nullcontext()
+
     def _allgather(self, _ctx, send, recv, n):
         try:
             src = torch.tensor([send[i] for i in range(n)], dtype=torch.uint64).view(torch.int64)
-            out = torch.empty(self.world * n, dtype=torch.int64, device=self.dev)
-            self.dist.all_gather_into_tensor(out, src.to(self.dev), group=self.group)
-            vals = out.cpu().view(torch.uint64).tolist()
+            with self._ctl():
+                out = torch.empty(self.world * n, dtype=torch.int64, device=self.dev)
+                self.dist.all_gather_into_tensor(out, src.to(self.dev), group=self.group)
+                vals = out.cpu().view(torch.uint64).tolist()
             for i, v in enumerate(vals):
                 recv[i] = v
             return 0
@@ -285,9 +297,10 @@ class _Comm:
 
     def _allreduce(self, _ctx, inout):
         try:
-            t = torch.tensor([inout[0]], dtype=torch.int32, device=self.dev)
-            self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
-            inout[0] = int(t.item())
+            with self._ctl():
+                t = torch.tensor([inout[0]], dtype=torch.int32, device=self.dev)
+                self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+                inout[0] = int(t.item())
             return 0
         except Exception as e:  # noqa: BLE001
             print(f"fastpersist: allreduce failed: {e}")

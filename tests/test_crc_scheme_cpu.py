@@ -1,5 +1,5 @@
-"""The device CRC-32 scheme (per-lane chains, lane tree, chunk fold through
-constant-product tables) emulated on the host with the library's own table
+"""The device CRC-32 scheme (per-lane chains, lane tree) and the host fold of page CRCs per
+extent (ExtentCrc) emulated on the host with the library's own table
 blob and compared with the plain slicing CRC, which the native CPU tests pin
 to zlib.crc32 through the manifest. Catches a wrong table, shift or fold
 order before any GPU time is spent."""

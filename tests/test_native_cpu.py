@@ -459,3 +459,114 @@ def test_gds_engine_needs_a_device():
     with pytest.raises(FastPersistError) as ei:
         fp.Checkpointer(None, io_engine="gds")
     assert ei.value.code == -22
+
+
+def _flip(path, off_from_end):
+    with open(path, "r+b") as f:
+        f.seek(os.path.getsize(path) - off_from_end)
+        b = f.read(1)
+        f.seek(os.path.getsize(path) - off_from_end)
+        f.write(bytes([b[0] ^ 0x40]))
+
+
+def test_manifest_extent_crcs_are_zlib_crcs_of_the_oracle_extents(tmp_path):
+    """Every shard record carries a CRC-32 per extent (replicated partition,
+    local region) besides the whole-file one: zlib.crc32 of the oracle's bytes
+    of that extent."""
+    import zlib
+    k = 4
+    states = [_state("moe_small", r, k) for r in range(k)]
+    lay = oracle_layout(states, k)
+    comms = ThreadComm.group(k)
+    cks = [fp.Checkpointer(None, comm=comms[r], slot_bytes=1 << 20) for r in range(k)]
+    try:
+        run_threads([lambda r=r: cks[r].save(entries(states[r]), str(tmp_path)) for r in range(k)])
+    finally:
+        for c in cks:
+            c.close()
+    man = json.load(open(tmp_path / "manifest.json"))
+    for r, ext in enumerate(fpck.shard_extents(lay)):
+        assert man["shards"][r]["extent_crc32"] == [zlib.crc32(lay.read(io, n)) for io, _, n in ext]
+
+
+@pytest.mark.parametrize("where", ["payload", "local_region"])
+def test_single_box_load_detects_payload_corruption(tmp_path, where):
+    """fp_ckpt_load (every extent read from whichever shard holds it) checks
+    each extent it reads against the manifest's per-extent CRC-32: a flipped
+    payload byte is FP_ECORRUPT, never a silent wrong restore."""
+    k = 2
+    cfg = "gpt3_odd" if where == "payload" else "moe_small"
+    states = [_state(cfg, r, k) for r in range(k)]
+    comms = ThreadComm.group(k)
+    cks = [fp.Checkpointer(None, comm=comms[r], slot_bytes=1 << 20) for r in range(k)]
+    try:
+        run_threads([lambda r=r: cks[r].save(entries(states[r]), str(tmp_path)) for r in range(k)])
+        # rank 1's shard: the last bytes are replicated payload (gpt3_odd) or
+        # rank 1's own local region (moe_small)
+        _flip(str(tmp_path / fpck.shard_name(1, k)), 3000)
+        codes = [None] * k
+
+        def go(r):
+            dst = [(s, torch.zeros_like(t)) for s, t in states[r]]
+            try:
+                cks[r].load(entries(dst), str(tmp_path))
+                codes[r] = 0
+            except FastPersistError as e:
+                codes[r] = e.code
+        run_threads([lambda r=r: go(r) for r in range(k)])
+    finally:
+        for c in cks:
+            c.close()
+    # replicated bytes are read by every rank; a local region only by its owner
+    assert codes == ([FP_ECORRUPT, FP_ECORRUPT] if where == "payload" else [0, FP_ECORRUPT])
+
+
+def test_replan_is_collective_when_one_rank_changes(tmp_path):
+    """ADVICE r1: only rank 1's local tensor changes size between two saves;
+    the replan (and its all-gather) must still run on every rank, and the
+    second checkpoint must be the oracle's."""
+    k = 2
+    comms = ThreadComm.group(k)
+    cks = [fp.Checkpointer(None, comm=comms[r], slot_bytes=1 << 20) for r in range(k)]
+    g = torch.Generator().manual_seed(7)
+    rep = torch.randn(3000, generator=g)
+    loc = [torch.randn(2000, generator=g), torch.randn(2000, generator=g)]
+
+    def ents(r):
+        return [("rep", rep, "other", -1), (f"loc{r}", loc[r], "other", r)]
+    try:
+        run_threads([lambda r=r: cks[r].save(ents(r), str(tmp_path / "a")) for r in range(k)])
+        loc[1] = torch.randn(5000, generator=g)          # rank 1 alone changes
+        run_threads([lambda r=r: cks[r].save(ents(r), str(tmp_path / "b")) for r in range(k)])
+    finally:
+        for c in cks:
+            c.close()
+    from tests._util import otensor
+    lay = fpck.Layout([otensor("rep", rep, dtype="f32")],
+                      [[otensor("loc0", loc[0], owner=0, dtype="f32")],
+                       [otensor("loc1", loc[1], owner=1, dtype="f32")]], k=k)
+    for r in range(k):
+        assert file_sha(tmp_path / "b" / fpck.shard_name(r, k)) == fpck.shard_sha256(lay, r)
+
+
+def test_import_error_on_one_rank_fails_every_rank_without_hanging(tmp_path):
+    """A rank whose tensor table is invalid (owner != dp_rank) must not leave
+    its peer waiting in the plan all-gather: both return an error."""
+    k = 2
+    comms = ThreadComm.group(k)
+    cks = [fp.Checkpointer(None, comm=comms[r], slot_bytes=1 << 20) for r in range(k)]
+    t = torch.randn(100)
+    codes = [None] * k
+
+    def go(r):
+        try:
+            cks[r].save([("x", t, "other", -1 if r == 0 else 0)], str(tmp_path))
+            codes[r] = 0
+        except FastPersistError as e:
+            codes[r] = e.code
+    try:
+        run_threads([lambda r=r: go(r) for r in range(k)])
+    finally:
+        for c in cks:
+            c.close()
+    assert codes == [-22, -22]

@@ -1,8 +1,8 @@
 // Host emulation of the device CRC-32 scheme (pack.cu: page_crc_warp as used
-// by fp_crc_pages / fp_crc_pages_tma / fp_pack_crc, and fp_crc_fold): the same
-// table blob (crc_device_tables), the same chain split, lane tree and
-// front-padded fold, compared with the plain slicing CRC (crc_raw_update) on
-// random pages, for several page and chunk counts. Built and run by
+// by fp_crc_pages / fp_crc_pages_tma / fp_pack_crc) and the host fold of page
+// CRCs per extent (ExtentCrc): the same table blob (crc_device_tables), the
+// same chain split and lane tree, compared with the plain slicing CRC
+// (crc_raw_update) on random pages, for several page and extent counts. Built and run by
 // tests/test_crc_scheme_cpu.py (no GPU needed).
 #include <cstdio>
 #include <cstdlib>
@@ -43,19 +43,25 @@ int main() {
       pc[pg] = lc[0];
       if (pc[pg] != crc_raw_update(0, buf.data() + (size_t)pg * 4096, 4096)) { printf("page mismatch\n"); return 1; }
     }
-    const uint32_t n_chunks = (n_pages + ppc - 1) / ppc, per = std::min(ppc, n_pages);
-    uint32_t log2r = 0; while ((1024ull << log2r) < per) ++log2r;
-    for (uint32_t ch = 0; ch < n_chunks; ++ch) {
-      const uint32_t p0 = ch * ppc, np = std::min(ppc, n_pages - p0), r = 1u << log2r;
-      const int64_t pad = 1024ll * r - np;
-      std::vector<uint32_t> red(1024);
-      for (int t = 0; t < 1024; ++t) { uint32_t acc = 0;
-        for (uint32_t i = 0; i < r; ++i) { int64_t idx = (int64_t)t * r + i - pad; acc = mul_tab(&T[kTabPage], acc) ^ (idx >= 0 ? pc[p0 + idx] : 0u); }
-        red[t] = acc; }
-      for (int m = 0; (1 << m) < 1024; ++m) { int step = 1 << m;
-        for (int t = 0; t < 1024; t += 2 * step) red[t] = mul_tab(&T[kTabPage + 1024 * (log2r + m)], red[t]) ^ red[t + step]; }
-      if (red[0] != crc_raw_update(0, buf.data() + (size_t)p0 * 4096, (size_t)np * 4096)) { printf("chunk mismatch n=%u ppc=%u ch=%u\n", n_pages, ppc, ch); return 1; }
+    // host fold (ExtentCrc): the pages split into extents at page boundaries
+    // (every ppc pages), some runs added as pages and some as bytes; each
+    // extent's CRC and the file CRC == the standard CRC-32 of those bytes
+    std::vector<Extent> ext;
+    for (uint32_t p0 = 0; p0 < n_pages; p0 += ppc)
+      ext.push_back({0, (uint64_t)p0 * 4096, (uint64_t)std::min(ppc, n_pages - p0) * 4096});
+    ExtentCrc acc;
+    acc.reset(ext);
+    for (uint32_t p0 = 0; p0 < n_pages;) {
+      const uint32_t n = std::min<uint32_t>(n_pages - p0, 1 + rand() % 700);
+      if (rand() & 3) acc.add_pages((uint64_t)p0 * 4096, pc.data() + p0, n);
+      else acc.add_bytes((uint64_t)p0 * 4096, buf.data() + (size_t)p0 * 4096, (size_t)n * 4096);
+      p0 += n;
     }
+    if (!acc.complete()) { printf("fold incomplete\n"); return 1; }
+    auto std_crc = [](const uint8_t* p, size_t n) { return crc_raw_update(0xFFFFFFFFu, p, n) ^ 0xFFFFFFFFu; };
+    for (size_t i = 0; i < ext.size(); ++i)
+      if (acc.extent_crc(i) != std_crc(buf.data() + ext[i].file_off, ext[i].len)) { printf("extent mismatch n=%u ppc=%u i=%zu\n", n_pages, ppc, i); return 1; }
+    if (acc.file_crc() != std_crc(buf.data(), buf.size())) { printf("file mismatch\n"); return 1; }
   }
   printf("emulation ok\n");
 }
