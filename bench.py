@@ -3,6 +3,10 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
+`--gpus N` with N > 1 and no torchrun environment re-launches itself under
+torch.distributed.run (N ranks, NCCL, one GPU per rank); rank 0 prints the
+one JSON line.
+
 Metric (BASELINE.json): "checkpoint persist GB/s and latency at 1/2/4/8 B200;
 % iter overhead per-iter ckpt". Workload: BASELINE.json configs[1], GPT-3 1.3B
 dense mixed-precision Adam state (adam16, 21,053,362,176-byte FPCK v2 image),
@@ -16,8 +20,10 @@ Total work is fixed as N grows (the same 21 GB image is split N ways), so
 
 Extra keys beyond the base contract: roofline (pack kernel, HBM), nvme / pcie
 rooflines measured in the same run, latency_s, overhead (per-iteration
-checkpointing under a synthetic fwd/bwd GEMM stream, §4.3 P:511-517,
-Eq. 1), cpu_baseline (the oracle, rank 0 at N=1).
+checkpointing under a synthetic fwd/bwd GEMM stream, §4.3, with a
+T_FB sweep and the Eq. 1 crossover), cpu_baseline (the
+oracle on rank 0's host cores, every N), storage (per-rank shard roots, their
+block devices and mounts, GPU -> NUMA node).
 """
 from __future__ import annotations
 
@@ -44,6 +50,9 @@ CFG = os.environ.get("FP_BENCH_CFG", "c2_gpt3_1.3b")
 # test hook: all ranks on cuda:0 over gloo (exercises the N>1 code path on a
 # 1-GPU box; NCCL refuses two ranks on one device). Never used for numbers.
 SHARE_GPU = os.environ.get("FP_BENCH_SHARE_GPU") == "1"
+# test hook: host-resident state (FP_TENSOR_HOST), gloo, no CUDA: lets the CPU
+# test suite drive the N-rank launch and JSON line. Never used for numbers.
+HOST_HOOK = os.environ.get("FP_BENCH_HOST") == "1"
 METRIC = "checkpoint persist GB/s and latency at 1/2/4/8 B200; % iter overhead per-iter ckpt"
 SEQ, GBS_1P3B = 2048, 512          # PAPER.md Table tb:gpt-setup: 1.3B, GBS 512
 
@@ -183,6 +192,114 @@ def d2h_roofline(dev, nbytes=256 << 20, reps=10):
 
 
 # ---------------------------------------------------------------------------
+# storage / NUMA topology (SURVEY §7 hard parts 1-2, §8(d): "state the drive
+# and filesystem, the NUMA mapping")
+# ---------------------------------------------------------------------------
+def _sysfs(path, default=None):
+    try:
+        with open(path) as f:
+            return f.read().strip()
+    except OSError:
+        return default
+
+
+def gpu_bdf(index):
+    try:
+        p = torch.cuda.get_device_properties(index)
+        return "%04x:%02x:%02x.0" % (p.pci_domain_id, p.pci_bus_id, p.pci_device_id)
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def numa_node_of(bdf):
+    if not bdf:
+        return -1
+    v = _sysfs(f"/sys/bus/pci/devices/{bdf.lower()}/numa_node", "-1")
+    try:
+        return int(v)
+    except ValueError:
+        return -1
+
+
+def nvme_mounts():
+    """Writable file systems on NVMe block devices: [(mountpoint, device,
+    sysfs PCI path of the controller)], from /proc/mounts."""
+    out, seen = [], set()
+    try:
+        lines = open("/proc/mounts").read().splitlines()
+    except OSError:
+        return out
+    for ln in lines:
+        f = ln.split()
+        if len(f) < 4 or not f[0].startswith("/dev/nvme") or "rw" not in f[3].split(","):
+            continue
+        dev = os.path.basename(f[0])
+        base = dev.split("p")[0] if "p" in dev[4:] else dev     # nvme0n1p2 -> nvme0n1
+        pci = os.path.realpath(f"/sys/block/{base}/device/device") \
+            if os.path.exists(f"/sys/block/{base}") else ""
+        if f[1] in seen or not os.access(f[1], os.W_OK):
+            continue
+        seen.add(f[1])
+        out.append((f[1], f[0], pci))
+    return out
+
+
+def pick_shard_dirs(world, bdfs, mounts=None):
+    """One shard root per rank (rank -> its GPU-local drive).
+
+    FP_CKPT_DIRS (comma-separated) wins; otherwise each rank takes the NVMe
+    mount whose controller shares the longest PCIe path prefix with its GPU
+    (same switch), ties to the least-used mount. None when no NVMe mount is
+    writable (the checkpoints then go under out_root())."""
+    env = os.environ.get("FP_CKPT_DIRS")
+    if env:
+        return [d for d in env.split(",") if d]
+    mounts = nvme_mounts() if mounts is None else mounts
+    if not mounts:
+        return None
+    used = {m[0]: 0 for m in mounts}
+    dirs = []
+    for r in range(world):
+        gp = os.path.realpath(f"/sys/bus/pci/devices/{bdfs[r].lower()}") if bdfs[r] else ""
+
+        def common(pci):
+            a, b = gp.split("/"), pci.split("/")
+            n = 0
+            while n < min(len(a), len(b)) and a[n] == b[n]:
+                n += 1
+            return n
+        best = max(mounts, key=lambda m: (common(m[2]), -used[m[0]]))
+        used[best[0]] += 1
+        dirs.append(best[0])
+    return dirs
+
+
+def storage_record(dirs, bdfs):
+    """lsblk / findmnt facts of the shard roots and the GPU -> NUMA map."""
+    rec = {"dirs": dirs, "gpu_numa": {str(i): numa_node_of(b) for i, b in enumerate(bdfs)},
+           "numa_nodes": len([d for d in os.listdir("/sys/devices/system/node")
+                              if d.startswith("node")]) if os.path.isdir("/sys/devices/system/node")
+           else None}
+    mnts = []
+    for d in sorted(set(dirs)):
+        try:
+            r = subprocess.run(["findmnt", "-n", "-o", "SOURCE,FSTYPE,OPTIONS", "-T", d],
+                               capture_output=True, text=True, timeout=10)
+            src, fst, opts = (r.stdout.split() + ["", "", ""])[:3]
+            mnts.append({"dir": d, "source": src, "fstype": fst, "options": opts[:80]})
+        except Exception:  # noqa: BLE001
+            mnts.append({"dir": d, "source": None})
+    rec["mounts"] = mnts
+    try:
+        r = subprocess.run(["lsblk", "-d", "-n", "-o", "NAME,TYPE,SIZE,ROTA,MODEL"],
+                           capture_output=True, text=True, timeout=10)
+        rec["lsblk"] = [" ".join(ln.split()) for ln in r.stdout.splitlines() if ln.strip()][:16]
+    except Exception:  # noqa: BLE001
+        rec["lsblk"] = None
+    return rec
+
+
+# ---------------------------------------------------------------------------
 # reference arm: the CPU oracle on the host cores
 # ---------------------------------------------------------------------------
 def oracle_sample_tensors(specs, budget_bytes, seed_dev="cpu"):
@@ -259,11 +376,17 @@ def reference_arm(a):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def synthetic_overhead(a, ck, ents, state, dev, rank, world, root, shard_gb):
-    """Per-iteration checkpointing under a synthetic training loop (§4.3):
-    fwd/bwd = bf16 GEMM loop sized to T_FB; wait() before the optimizer;
-    optimizer = foreach update over master/m/v + bf16 param copy; begin()
-    after it. overhead = median iter (ckpt) / median iter (no ckpt) - 1."""
+def synthetic_overhead(a, ck, ents, state, dev, rank, world, path_of, image_gb, persist_gbs):
+    """Per-iteration checkpointing under a synthetic training loop (§4.3,
+    P:511-517): fwd (reads every bf16 param) + bf16 GEMM loop sized to T_FB +
+    bwd (writes every grad) -> wait() -> optimizer (foreach update of master,
+    m, v + bf16 param copy) -> begin(). The checkpointed state is the paper's
+    14 B/param (params, master, m, v): grads are rewritten by every
+    backward inside the overlap window, so they cannot be checkpointed
+    without a snapshot (fastpersist.h: tensors immutable from begin to wait).
+    overhead = median iteration with checkpointing / median without - 1,
+    swept over T_FB (the GAS-sweep analog of P:736) with the Eq. 1 crossover
+    S_C / B (P:320-323)."""
     n = 8192
     A = torch.randn(n, n, device=dev, dtype=torch.bfloat16)
     B = torch.randn(n, n, device=dev, dtype=torch.bfloat16)
@@ -276,22 +399,22 @@ def synthetic_overhead(a, ck, ents, state, dev, rank, world, root, shard_gb):
     for _ in range(50):
         torch.matmul(A, B, out=C)
     torch.cuda.synchronize(dev)
-    t_gemm = (time.perf_counter() - t0) / 50
-    t_fb = a.t_fb
-    if t_fb <= 0:
-        # FLOP-derived: 6 * P * tokens per iteration over the DP group at
-        # 40% of nominal dense bf16, GBS 512 x seq 2048
-        P = 1315819520
-        t_fb = 6 * P * GBS_1P3B * SEQ / (world * 0.4 * 2.25e15)
-    n_gemm = max(1, int(round(t_fb / t_gemm)))
+    t_gemm = allreduce_max((time.perf_counter() - t0) / 50, dev)
     by_sec = {}
     for (s, t) in state:
         by_sec.setdefault(s.section, []).append(t)
-    master, m, v, param = (by_sec.get(x, []) for x in ("master", "exp_avg", "exp_avg_sq", "param"))
+    master, m, v, param, grad = (by_sec.get(x, []) for x in
+                                 ("master", "exp_avg", "exp_avg_sq", "param", "grad"))
+    ov_ents = [e for e in ents if e[2] != "grad"]
+    ov_bytes = sum(t.numel() * t.element_size() for _, t, sec, _ in ov_ents)
 
-    def fwd_bwd():
+    def fwd_bwd(n_gemm):
+        if param:
+            torch._foreach_norm(param)               # fwd reads the params
         for _ in range(n_gemm):
             torch.matmul(A, B, out=C)
+        if grad:
+            torch._foreach_add_(grad, 1e-6)          # bwd writes the grads
 
     def optimizer():
         # memory-bound like Adam: read/write master, m, v; write bf16 params
@@ -301,86 +424,142 @@ def synthetic_overhead(a, ck, ents, state, dev, rank, world, root, shard_gb):
         for p, w in zip(param, master):
             p.copy_(w)
 
-    def loop(ckpt, iters):
+    def loop(ckpt, n_gemm, warm, iters):
         its = []
-        for i in range(iters):
+        for i in range(warm + iters):
             torch.cuda.synchronize(dev)
             barrier()
             t0 = time.perf_counter()
-            fwd_bwd()
+            fwd_bwd(n_gemm)
             if ckpt:
                 ck.wait()                    # fence before the optimizer
             optimizer()
             if ckpt:
-                ck.begin(ents, os.path.join(root, f"gen{i % 2}"))   # after the optimizer
+                ck.begin(ov_ents, path_of(f"ov{i % 2}"))   # after the optimizer
             torch.cuda.synchronize(dev)
-            its.append(allreduce_max(time.perf_counter() - t0, dev))
+            dt = allreduce_max(time.perf_counter() - t0, dev)
+            if i >= warm:
+                its.append(dt)
         if ckpt:
-            t0 = time.perf_counter()
             ck.wait()
         return its
 
-    iters = a.overhead_iters
-    base = loop(False, iters + 1)[1:]
-    with_ck = loop(True, iters + 2)[2:]      # iteration 0 has no pending checkpoint
-    mb, mc = statistics.median(base), statistics.median(with_ck)
-    return {"t_fb_s": round(n_gemm * t_gemm, 3), "gemms_per_iter": n_gemm,
-            "iter_s_no_ckpt": round(mb, 4), "iter_s_ckpt": round(mc, 4),
-            "overhead_pct": round(100 * (mc / mb - 1), 2),
-            "eq1_required_gbs_per_rank": round(shard_gb / (n_gemm * t_gemm), 3),
-            "iters": iters, "workload": CFG}
+    # FLOP-derived T_FB: 6 * P * tokens per iteration over the DP group at 40%
+    # of nominal dense bf16, GBS 512 x seq 2048
+    P = 1315819520
+    t_flop = 6 * P * GBS_1P3B * SEQ / (world * 0.4 * 2.25e15)
+    if a.t_fb > 0:
+        t_flop = a.t_fb
+    sweep = [float(x) for x in a.t_fb_sweep.split(",") if x.strip()] if world == 1 else []
+    pts = sorted(set(sweep + [round(t_flop, 3)]))
+    # Eq. 1 crossover: the checkpoint hides behind fwd/bwd once T_FB >= S_C / B
+    # (S_C = this leg's image, B = the persist rate measured above)
+    crossover = ov_bytes * world / 1e9 / persist_gbs if persist_gbs else None
+    out = []
+    for t_fb in pts:
+        n_gemm = max(1, int(round(t_fb / t_gemm)))
+        base = loop(False, n_gemm, 1, a.overhead_base_iters)
+        with_ck = loop(True, n_gemm, a.overhead_warmup, a.overhead_iters)  # iteration 0 has no
+        mb, mc = statistics.median(base), statistics.median(with_ck)    # pending ckpt
+        out.append({"t_fb_s": round(n_gemm * t_gemm, 3), "flop_derived": t_fb == round(t_flop, 3),
+                    "iter_s_no_ckpt": round(mb, 4), "iter_s_ckpt": round(mc, 4),
+                    "overhead_pct": round(100 * (mc / mb - 1), 2),
+                    "eq1_hidden": crossover is not None and n_gemm * t_gemm >= crossover})
+    head = next(x for x in out if x["flop_derived"])
+    return {"overhead_pct": head["overhead_pct"], "t_fb_s": head["t_fb_s"],
+            "iter_s_no_ckpt": head["iter_s_no_ckpt"], "iter_s_ckpt": head["iter_s_ckpt"],
+            "state": "adam14 (params, master, m, v; grads rewritten by each backward)",
+            "ckpt_bytes": int(ov_bytes * world), "eq1_crossover_s": round(crossover, 3)
+            if crossover else None,
+            "max_overhead_pct_where_hidden": max([x["overhead_pct"] for x in out
+                                                  if x["eq1_hidden"]], default=None),
+            "iters": a.overhead_iters, "warmup": a.overhead_warmup,
+            "base_iters": a.overhead_base_iters, "pack_ctas": a.overlap_ctas,
+            "pack": a.overlap_pack, "sweep": out, "workload": CFG}
 
 
 def our_arm(a):
     ws, rank, lr = env_dist()
+    # measurement machinery: CUDA events around each pack launch time the
+    # kernel, not the host's launch latency (library launch gate, opt-in)
+    os.environ.setdefault("FP_LAUNCH_GATE", "1")
     if ws > 1 and not dist.is_initialized():
-        if SHARE_GPU:
+        if SHARE_GPU or HOST_HOOK:
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", lr))
     world = ws
-    dev = torch.device("cuda", 0 if SHARE_GPU else lr)
-    torch.cuda.set_device(dev)
+    if HOST_HOOK:
+        dev = None
+    else:
+        dev = torch.device("cuda", 0 if SHARE_GPU else lr)
+        torch.cuda.set_device(dev)
 
     import paper_2406_13768_b200 as fp
     from workloads import config_specs, make_state
     fp.lib()                                             # fails loudly if not built
 
     specs = config_specs(CFG, rank, world)
-    state = make_state(specs, dev)
+    state = make_state(specs, dev if dev is not None else "cpu")
     ents = [(s.name, t, s.section, s.owner) for s, t in state]
     state_bytes = sum(s.nbytes for s in specs)
-    torch.cuda.synchronize(dev)
+    sync = (lambda: torch.cuda.synchronize(dev)) if dev is not None else (lambda: None)
+    sync()
 
-    root = os.path.join(out_root(), "ours")
-    if rank == 0:
-        shutil.rmtree(root, ignore_errors=True)
-        os.makedirs(root, exist_ok=True)
+    # ---- per-rank shard roots (GPU-local NVMe when discoverable) -----------
+    n_vis = torch.cuda.device_count() if dev is not None else 0
+    bdfs = [gpu_bdf(0 if SHARE_GPU else r) if r < max(n_vis, 1) and dev is not None else None
+            for r in range(world)]
+    shard_dirs = pick_shard_dirs(world, bdfs)
+    if shard_dirs:
+        sub = "fp_bench"
+
+        def path_of(name):                   # relative: the library joins dirs[r % n]
+            return os.path.join(sub, name)
+        roots = [os.path.join(shard_dirs[r % len(shard_dirs)], sub) for r in range(world)]
+    else:
+        roots = [os.path.join(out_root(), "ours")] * world
+
+        def path_of(name):
+            return os.path.join(roots[0], name)
+    root = roots[rank]
+    my_roots = [root] if roots.index(root) == rank else []   # lowest rank of a root owns it
+    for d in my_roots:
+        shutil.rmtree(d, ignore_errors=True)
     barrier()
+    os.makedirs(root, exist_ok=True)
+    barrier()
+    storage = storage_record(shard_dirs or [os.path.dirname(root)], bdfs)
 
     cfg = dict(pack=a.pack, slot_bytes=a.slot_mib << 20, ring_slots=a.ring_slots,
                io_depth=a.qd, sqe_bytes=a.sqe_kib << 10, pack_bytes=a.pack_mib << 20,
-               prio=a.prio, writer_stride=a.writer_stride, io_engine=a.io_engine)
+               prio=a.prio, writer_stride=a.writer_stride, io_engine=a.io_engine,
+               dirs=shard_dirs)
     peaks, peak_src = measured_peaks()
 
     # ---- rooflines measured in the same run --------------------------------
     with fp.Checkpointer(dev, **cfg) as ck0:
-        ck0.begin(ents, os.path.join(root, "plan"))
+        ck0.begin(ents, path_of("plan"))
         ck0.wait()
         shard_bytes = ck0.plan_info()["extents"]
     shard_bytes = sum(e[2] for e in shard_bytes)
-    shutil.rmtree(os.path.join(root, "plan"), ignore_errors=True) if rank == 0 else None
+    barrier()
+    for d in my_roots:
+        shutil.rmtree(os.path.join(d, "plan"), ignore_errors=True)
     barrier()
     # every rank writes the same amount (a writer subset still has N ranks
     # on the box): the image's per-rank share, capped
     img_total = int(allreduce_sum(shard_bytes, dev))
     nv_bytes = min(-(-img_total // world), int(a.nvme_bytes))
     # the roofline file sits beside two checkpoint generations: keep it within
-    # what the file system can hold (all ranks share one box)
+    # what the file system can hold (ranks sharing a file system share it)
     fs = os.statvfs(root)
     free_now = fs.f_bavail * fs.f_frsize
-    room = (free_now - 2.2 * img_total) / world
-    nv_bytes = int(min(nv_bytes, max(2e9, room * 0.8))) // 4096 * 4096
+    dev_id = os.stat(root).st_dev
+    sharing = sum(1 for d in roots if os.stat(os.path.dirname(d) if shard_dirs else d).st_dev
+                  == dev_id)
+    room = (free_now - 2.2 * img_total * sharing / world) / sharing
+    nv_bytes = int(min(nv_bytes, max(2e8, room * 0.8))) // 4096 * 4096
     barrier()
     os.sync()                                 # settle writeback of earlier runs first
 
@@ -389,31 +568,36 @@ def our_arm(a):
                         ring_slots=a.ring_slots, slot_bytes=a.slot_mib << 20)
         return allreduce_sum(g, dev)          # concurrent writers: aggregate
     nvme_before = nvme_roofline()
-    d2h_gbs = allreduce_sum(d2h_roofline(dev), dev)
+    d2h_gbs = allreduce_sum(d2h_roofline(dev), dev) if dev is not None else None
 
     # ---- the checkpoint steps ----------------------------------------------
     ck = fp.Checkpointer(dev, group=None, **cfg)
     image_bytes = None
     for i in range(a.warmup):
-        s = ck.save(ents, os.path.join(root, f"gen{i % 2}"))
+        s = ck.save(ents, path_of(f"gen{i % 2}"))
         image_bytes = s["image_bytes"]
-    clocks = Clocks(gpu_smi_id(dev)).start()
-    stream = torch.cuda.current_stream(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = Clocks(gpu_smi_id(dev)).start() if dev is not None else None
+    stream = torch.cuda.current_stream(dev) if dev is not None else None
     lat, stats = [], []
     barrier()
-    torch.cuda.synchronize(dev)
-    e0.record(stream)
+    sync()
+    if dev is not None:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+    th0 = time.perf_counter()
     for i in range(a.steps):
         t0 = time.perf_counter()
-        ck.begin(ents, os.path.join(root, f"gen{(a.warmup + i) % 2}"), stream=stream)
+        ck.begin(ents, path_of(f"gen{(a.warmup + i) % 2}"), stream=stream)
         stats.append(ck.wait())
         lat.append(time.perf_counter() - t0)
-    e1.record(stream)
-    torch.cuda.synchronize(dev)
+    if dev is not None:
+        e1.record(stream)
+    sync()
     barrier()
-    ck_clock = clocks.stop()
-    elapsed = allreduce_max(e0.elapsed_time(e1) / 1e3, dev)
+    ck_clock = clocks.stop() if clocks else {"sm_mhz": None, "sm_max_mhz": None,
+                                              "reasons": ["host-state test hook"]}
+    el = e0.elapsed_time(e1) / 1e3 if dev is not None else time.perf_counter() - th0
+    elapsed = allreduce_max(el, dev)
     lat_max = [allreduce_max(x, dev) for x in lat]
     image_bytes = stats[-1]["image_bytes"]
     gbs = image_bytes * a.steps / elapsed / 1e9
@@ -444,18 +628,18 @@ def our_arm(a):
     restore = None
     if not a.no_restore:
         try:
-            last = os.path.join(root, f"gen{(a.warmup + a.steps - 1) % 2}")
+            last = path_of(f"gen{(a.warmup + a.steps - 1) % 2}")
             gr = fp.io_bench(root, nv_bytes, tag=rank, read=True, io_depth=a.qd,
                              sqe_bytes=a.sqe_kib << 10, ring_slots=a.ring_slots,
                              slot_bytes=a.slot_mib << 20)
             nvme_read = allreduce_sum(gr, dev)
-            rl = []
+            rl, rinfo = [], {}
             for _ in range(a.restore_steps):
                 barrier()
-                torch.cuda.synchronize(dev)
+                sync()
                 t0 = time.perf_counter()
-                ck.load_parallel(ents, last, stream=stream)   # synchronous; checks the CRC
-                torch.cuda.synchronize(dev)
+                rinfo = ck.load_parallel(ents, last, stream=stream) or {}   # checks the CRC
+                sync()
                 rl.append(allreduce_max(time.perf_counter() - t0, dev))
             rt = statistics.median(rl)
             restore = {"value": round(image_bytes / rt / 1e9, 4), "unit": "GB/s",
@@ -464,16 +648,17 @@ def our_arm(a):
                        "frac": round(image_bytes / rt / 1e9 / nvme_read, 4),
                        "call": "fp_ckpt_load_parallel (own shard O_DIRECT read-ahead over the "
                                "pinned ring -> H2D -> all-gather -> unpack kernel, CRC-32 checked)",
+                       "exchange": rinfo.get("exchange"),
                        "roofline_how": f"fp_io_bench_read: O_DIRECT io_uring seq read, {a.qd} x "
                                        f"{a.sqe_kib} KiB in flight, best of 2, {world} concurrent "
-                                       f"readers x {nv_bytes} B, same dir, same run"}
+                                       f"readers x {nv_bytes} B, same dirs, same run"}
         except Exception as e:  # noqa: BLE001 - an optional measurement must not lose the line
             print(f"bench: restore failed: {type(e).__name__}: {e}", file=sys.stderr)
             restore = {"error": f"{type(e).__name__}: {e}"}
 
     # ---- e2e: public API with the state sourced from pinned HOST memory ------
     e2e = None
-    if not a.no_e2e:
+    if not a.no_e2e and dev is not None:
         try:
             # this rank sources its share of the state from pinned host memory:
             # tensors are dealt to ranks by the position of their middle byte in
@@ -489,19 +674,19 @@ def our_arm(a):
             for h, t in zip(host, mine):
                 h.copy_(t)
             my_h2d = sum(t.numel() * t.element_size() for t in mine)
-            torch.cuda.synchronize(dev)
+            sync()
             ke = max(1, min(a.steps, a.e2e_steps))
             barrier()
-            torch.cuda.synchronize(dev)
+            sync()
             f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             f0.record(stream)
             for i in range(ke):
                 for h, t in zip(host, mine):
                     t.copy_(h, non_blocking=True)          # H2D of this step's inputs
-                ck.begin(ents, os.path.join(root, f"gen{i % 2}"), stream=stream)
+                ck.begin(ents, path_of(f"gen{i % 2}"), stream=stream)
                 st = ck.wait()                             # result: durable status (host)
             f1.record(stream)
-            torch.cuda.synchronize(dev)
+            sync()
             barrier()
             e_el = allreduce_max(f0.elapsed_time(f1) / 1e3, dev)
             e2e = {"value": round(st["image_bytes"] * ke / e_el / 1e9, 4), "unit": "GB/s",
@@ -515,23 +700,26 @@ def our_arm(a):
             e2e = {"error": f"{type(e).__name__}: {e}"}
 
     overhead = None
-    if not a.no_overhead:
+    if not a.no_overhead and dev is not None:
         try:
             ovcfg = dict(cfg)
             ovcfg["pack_ctas"] = a.overlap_ctas
+            ovcfg["pack"] = a.overlap_pack
             with fp.Checkpointer(dev, **ovcfg) as cko:
-                overhead = synthetic_overhead(a, cko, ents, state, dev, rank, world, root,
-                                              shard_bytes / 1e9)
+                overhead = synthetic_overhead(a, cko, ents, state, dev, rank, world, path_of,
+                                              image_bytes / 1e9, gbs)
         except Exception as e:  # noqa: BLE001 - an optional measurement must not lose the line
             print(f"bench: overhead failed: {type(e).__name__}: {e}", file=sys.stderr)
             overhead = {"error": f"{type(e).__name__}: {e}"}
 
     ck.close()
-    if rank == 0:
-        shutil.rmtree(root, ignore_errors=True)
+    barrier()
+    for d in my_roots:
+        shutil.rmtree(d, ignore_errors=True)
 
+    # the oracle on rank 0's host cores, at every N (a bounded sample)
     cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+    if rank == 0 and not a.no_cpu_baseline:
         try:
             sample, _ = oracle_sample_tensors(specs, int(a.oracle_bytes))
             croot = os.path.join(out_root(), "oracle")
@@ -551,7 +739,7 @@ def our_arm(a):
             shutil.rmtree(croot, ignore_errors=True)
             cpu = {"value": round(cg, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
                    "sample": f"first {len(sample)} tensors of {CFG} ({cimg} image bytes), "
-                             "host-resident, buffered write()+fsync, 1 step",
+                             "host-resident, buffered write()+fsync, 1 step, rank 0",
                    "host_cores_available": cpu_cores(),
                    "torch_save_gbs": round(ts_bytes / ts_dt / 1e9, 4),
                    "torch_save_note": "context only: torch.save(state dict of the same sample) "
@@ -590,7 +778,13 @@ def our_arm(a):
                        "sqe_kib": a.sqe_kib, "qd": a.qd, "engine": stats[-1]["engine"],
                        "io_fallback": stats[-1]["fallback"],
                        "l2": "inputs (21 GB of state) larger than L2; no flush needed",
-                       "dir": root},
+                       "launch": "torchrun" if os.environ.get("FP_BENCH_SELF_LAUNCHED") != "1"
+                       and world > 1 else ("self-launched torch.distributed.run"
+                                           if world > 1 else "single process"),
+                       "backend": dist.get_backend() if dist.is_initialized() else None,
+                       "test_hook": "host-state" if HOST_HOOK else
+                       ("shared-gpu" if SHARE_GPU else None)},
+            "storage": storage,
             "latency_s": {"median": round(statistics.median(lat_max), 4),
                           "min": round(min(lat_max), 4), "max": round(max(lat_max), 4)},
             "roofline": {"bound": "hbm", "kernel": kname,
@@ -598,12 +792,12 @@ def our_arm(a):
                          "frac": round(pack_gbs / hbm, 4), "traffic": traffic,
                          "peak_source": peak_src, "launch_avg_ms": round(launch_avg_ms, 5),
                          "bytes_per_launch": int(2 * pk_bytes / max(1, pk_launches))},
-            # the second library kernel pair of a step: page CRCs + fold over
-            # each packed group (1 B read per slab byte; issue-bound on table
-            # lookups) — reported, not the roofline kernel
+            # the second library kernel of a step: page CRCs over each packed
+            # group (1 B read per slab byte; issue-bound on table lookups, see
+            # DESIGN.md §6) — reported, not the roofline kernel
             "crc_kernels": None if crc_ms <= 0 else {
-                "kernels": "fp_crc_pages_tma + fp_crc_fold" if not os.environ.get("FP_NO_TMA")
-                else "fp_crc_pages + fp_crc_fold",
+                "kernels": "fp_crc_pages_tma" if not os.environ.get("FP_NO_TMA")
+                else "fp_crc_pages",
                 "us_per_launch": round(1e3 * crc_ms / max(1, pk_launches), 2),
                 "read_gbs": round(pk_bytes / (crc_ms / 1e3) / 1e9, 1),
                 "frac_of_hbm": round(pk_bytes / (crc_ms / 1e3) / 1e9 / hbm, 4),
@@ -612,11 +806,11 @@ def our_arm(a):
                      "before_gbs": round(nvme_before, 3), "after_gbs": round(nvme_after, 3),
                      "how": f"built-in fp_io_bench (fio absent): O_DIRECT io_uring seq "
                             f"overwrite, {a.qd} x {a.sqe_kib} KiB in flight, best of 2 timed passes, "
-                            f"{world} concurrent writers x {nv_bytes} B, same dir, same run, "
-                            f"measured before and after the timed steps (max taken)"},
-            "pcie_d2h": {"measured_gbs": round(d2h_gbs, 2), "frac": round(gbs / d2h_gbs, 4),
-                         "ring_d2h_gbs": round(pk_bytes / (d2h_ms / 1e3) / 1e9, 2)
-                         if d2h_ms > 0 else None},
+                            f"{world} concurrent writers x {nv_bytes} B, each in its rank's shard "
+                            f"root, same run, measured before and after the timed steps (max taken)"},
+            "pcie_d2h": None if d2h_gbs is None else {
+                "measured_gbs": round(d2h_gbs, 2), "frac": round(gbs / d2h_gbs, 4),
+                "ring_d2h_gbs": round(pk_bytes / (d2h_ms / 1e3) / 1e9, 2) if d2h_ms > 0 else None},
             "hbm": {"peak_gbs_all_gpus": hbm * world, "frac": round(gbs / (hbm * world), 6)},
             "phase_s_last": {k: round(stats[-1][k], 4) for k in
                              ("t_helper", "t_fsync", "t_barrier", "t_commit", "t_io_stall")},
@@ -631,6 +825,27 @@ def our_arm(a):
     if dist.is_initialized():
         dist.destroy_process_group()
     return 0
+
+
+def _free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(a):
+    """`--gpus N` without a torchrun environment: re-run this script as N
+    ranks under torch.distributed.run (one node, 127.0.0.1), NCCL init logging
+    on so the N ranks are visible in stderr; rank 0 prints the line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ, FP_BENCH_SELF_LAUNCHED="1")
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    print(f"bench.py: launching {a.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.call(cmd, env=env)
 
 
 def main():
@@ -654,9 +869,16 @@ def main():
                     help="cap on the roofline file per rank (default covers a whole C2 shard)")
     ap.add_argument("--oracle-bytes", type=float, default=1.5e9)
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--overhead-iters", type=int, default=4)
+    ap.add_argument("--overhead-iters", type=int, default=10)
+    ap.add_argument("--overhead-warmup", type=int, default=2)
+    ap.add_argument("--overhead-base-iters", type=int, default=3,
+                    help="iterations without checkpointing per T_FB (deterministic GEMM loop)")
     ap.add_argument("--overlap-ctas", type=int, default=16)
-    ap.add_argument("--t-fb", type=float, default=0.0, help="synthetic fwd+bwd seconds (0: FLOP-derived)")
+    ap.add_argument("--overlap-pack", default="v4", choices=["v4", "bulk"])
+    ap.add_argument("--t-fb", type=float, default=0.0,
+                    help="headline synthetic fwd+bwd seconds (0: FLOP-derived)")
+    ap.add_argument("--t-fb-sweep", default="0.5,1,2,4",
+                    help="extra T_FB points (s) at N=1; the FLOP-derived point is always run")
     ap.add_argument("--traffic", type=float, default=None,
                     help="ncu dram bytes per pack launch (from profiles/), echoed into roofline")
     ap.add_argument("--no-e2e", action="store_true")
@@ -669,6 +891,8 @@ def main():
         print("bench.py: --warmup must be >= 3", file=sys.stderr)
     if a.impl == "reference":
         return reference_arm(a)
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(a)
     return our_arm(a)
 
 

@@ -24,3 +24,46 @@ def test_reference_arm_json_line(tmp_path):
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] == 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0
     assert not os.listdir(tmp_path) or os.listdir(tmp_path) == []
+
+
+def test_gpus_2_self_launches_two_ranks(tmp_path):
+    """`bench.py --gpus 2` without torchrun re-launches itself as 2 ranks
+    (torch.distributed.run); rank 0 prints ONE line with n_gpus 2. Host-state
+    test hook (FP_BENCH_HOST=1: gloo, host tensors, no CUDA) on the CPU box."""
+    env = dict(os.environ, FP_BENCH_DIR=str(tmp_path), FP_BENCH_HOST="1", FP_BENCH_CFG="c1_tiny")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                          "--steps", "2", "--warmup", "3", "--nvme-bytes", "1e8",
+                          "--oracle-bytes", "2e7"],
+                         capture_output=True, text=True, env=env, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["dp"] == 2
+    assert d["config"]["launch"] == "self-launched torch.distributed.run"
+    assert d["cpu_baseline"]["kind"] == "oracle"          # cpu_baseline at every N
+    assert d["storage"]["mounts"] and "lsblk" in d["storage"]
+    assert d["restore"]["value"] > 0
+    assert "launching 2 ranks" in out.stderr
+
+
+def test_shard_dirs_follow_pcie_affinity(monkeypatch):
+    """Each rank takes the NVMe mount sharing the longest PCIe path with its
+    GPU (same switch), ties to the least-used one; FP_CKPT_DIRS overrides."""
+    sys.path.insert(0, ROOT)
+    import bench
+    monkeypatch.delenv("FP_CKPT_DIRS", raising=False)
+    mounts = [("/mnt/a", "/dev/nvme0n1", "/sys/devices/pci0000:00/0000:00:01.0/0000:01:00.0"),
+              ("/mnt/b", "/dev/nvme1n1", "/sys/devices/pci0000:80/0000:80:01.0/0000:81:00.0")]
+    monkeypatch.setattr(bench.os.path, "realpath",
+                        lambda p: {"/sys/bus/pci/devices/0000:02:00.0":
+                                   "/sys/devices/pci0000:00/0000:00:01.0/0000:02:00.0",
+                                   "/sys/bus/pci/devices/0000:82:00.0":
+                                   "/sys/devices/pci0000:80/0000:80:01.0/0000:82:00.0"}.get(p, p))
+    got = bench.pick_shard_dirs(4, ["0000:02:00.0", "0000:82:00.0", "0000:02:00.0",
+                                    "0000:82:00.0"], mounts)
+    assert got == ["/mnt/a", "/mnt/b", "/mnt/a", "/mnt/b"]
+    assert bench.pick_shard_dirs(2, [None, None], []) is None
+    monkeypatch.setenv("FP_CKPT_DIRS", "/x,/y")
+    assert bench.pick_shard_dirs(2, [None, None]) == ["/x", "/y"]
