@@ -180,8 +180,10 @@ typedef struct fp_stats {
                               (host tensors: on the CPU); also in the manifest  */
   uint32_t crc_valid;      /* 1 if shard_crc32 was computed                       */
   uint64_t kernel_launches;/* all library kernels launched (pack, CRC, gate)      */
-  double   crc_ms;         /* sum of CUDA-event durations of the CRC kernels
-                              (page CRCs + per-chunk fold) after each pack       */
+  double   crc_ms;         /* sum of CUDA-event durations of the page-CRC kernel
+                              after each pack (folded per extent on the host)  */
+  int32_t  numa_node;      /* NUMA node the pinned ring and helper thread were
+                              placed on (the GPU's; -1: unknown / not placed)  */
 } fp_stats;
 
 typedef struct fp_ctx fp_ctx;
@@ -192,14 +194,18 @@ typedef struct fp_ctx fp_ctx;
  * FP_WRITER_STRIDE, FP_CKPT_DIRS, FP_NO_CRC). Returns 0.
  * Read at run time (not part of fp_config): FP_NO_TMA=1 (LSU page-CRC kernel
  * instead of the TMA-staged one), FP_CRC_FUSED=1 (page CRCs inside the pack
- * kernel, ablation), FP_NO_GATE=1 (no launch gate; automatic when a profiler
- * is injected), FP_GDS_OPEN_TIMEOUT (s, default 20), FP_DEBUG_GDS=1,
- * FP_FAULT_EIO_AT=<n>[@rank] (tests).                                          */
+ * kernel, ablation), FP_LAUNCH_GATE=1 (measurement: queue each pack group
+ * behind a one-warp gate the helper opens after enqueueing, so CUDA events
+ * time the kernel alone; off by default and under a profiler), FP_NUMA=0 (do
+ * not place the ring / helper on the GPU's NUMA node), FP_GDS_OPEN_TIMEOUT
+ * (s, default 20), FP_DEBUG_GDS=1, FP_FAULT_EIO_AT=<n>[@rank] and
+ * FP_FAULT_KILL_AT=<n>[@rank] (tests).                                         */
 int fp_config_default(fp_config *cfg);
 
 /* Create a context bound to CUDA device `cuda_device` (-1: host tensors only).
  * Allocates the pinned ring (slots*slot_bytes, page-locked and registered with
- * the I/O engine), one device slab of pack_bytes, a CUDA stream and
+ * the I/O engine; its pages and the helper thread are placed on the GPU's
+ * NUMA node), one device slab of pack_bytes, a CUDA stream and
  * the helper thread. `comm` may be NULL only if every call uses dp_size == 1.
  * *out receives the context. Errors: -EINVAL (bad config), -ENOMEM, FP_ECUDA. */
 int fp_ckpt_init(const fp_config *cfg, int cuda_device, const fp_comm *comm,

@@ -65,6 +65,7 @@ struct fp_ctx {
   std::string dirs_copy;
   std::vector<std::string> roots;
   int dev = -1;
+  int numa_node = -1;  // NUMA node of the GPU (ring + helper placed there), -1 unknown
   fp_comm comm;
   bool has_comm = false;
   // resources
@@ -96,6 +97,10 @@ struct fp_ctx {
   // completion of a checkpoint (of that rank, or any rank) into -EIO
   int64_t fault_eio_at = -1;
   int fault_rank = -1;
+  // crash injection (tests): FP_FAULT_KILL_AT=<n>[@<rank>] SIGKILLs the
+  // process at the n-th write completion of a checkpoint (a torn generation)
+  int64_t fault_kill_at = -1;
+  int fault_kill_rank = -1;
   // CRC-32 of the shard
   uint32_t* d_crc_tabs = nullptr;  // crc_device_tables() blob
   uint32_t* d_page_crc = nullptr;  // page CRCs of one pack group (device)

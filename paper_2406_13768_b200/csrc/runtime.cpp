@@ -16,12 +16,17 @@
 #include <cuda_runtime.h>
 #include <dirent.h>
 #include <fcntl.h>
+#include <pthread.h>
+#include <sched.h>
+#include <signal.h>
 #include <sys/mman.h>
 #include <sys/stat.h>
+#include <sys/syscall.h>
 #include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
+#include <cctype>
 #include <cerrno>
 #include <chrono>
 #include <condition_variable>
@@ -168,6 +173,8 @@ int fp_ctx::save_shard() {
       ++completions;
       if (completions == fault_eio_at && (fault_rank < 0 || fault_rank == rank))
         done[i].res = -EIO;  // injected (FP_FAULT_EIO_AT)
+      if (completions == fault_kill_at && (fault_kill_rank < 0 || fault_kill_rank == rank))
+        kill(getpid(), SIGKILL);  // injected crash mid-write (FP_FAULT_KILL_AT)
       const uint64_t u = done[i].user;
       const uint32_t s = (uint32_t)(u >> 56);
       const int64_t expect = (int64_t)((u >> 32) & 0xFFFFFF) * 512;
@@ -724,12 +731,60 @@ static IoEngine* open_engine(const fp_config& cfg, int* kind_used) {
   return io;
 }
 
-static uint8_t* alloc_ring(size_t bytes) {
+// NUMA node of a CUDA device (sysfs numa_node of its PCI function), -1 if
+// unknown or single-node
+static int gpu_numa_node(int device) {
+  char bdf[32] = {0};
+  if (device < 0 || cudaDeviceGetPCIBusId(bdf, sizeof(bdf), device) != cudaSuccess) return -1;
+  for (char* q = bdf; *q; ++q) *q = (char)tolower(*q);
+  FILE* f = fopen(("/sys/bus/pci/devices/" + std::string(bdf) + "/numa_node").c_str(), "r");
+  if (!f) return -1;
+  int node = -1;
+  if (fscanf(f, "%d", &node) != 1) node = -1;
+  fclose(f);
+  return node;
+}
+
+// The pinned ring lives on the GPU's NUMA node (SURVEY §8(a') "mmap, mbind to
+// the GPU's NUMA node, cudaHostRegister"): both DMAs that touch it (GPU D2H,
+// NVMe writes) then cross no inter-socket link. MPOL_PREFERRED, set before the
+// pages are faulted in; node < 0 or FP_NUMA=0 leaves the default policy.
+static uint8_t* alloc_ring(size_t bytes, int node) {
   void* p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
   if (p == MAP_FAILED) return nullptr;
   madvise(p, bytes, MADV_HUGEPAGE);
+  if (node >= 0 && node < 64) {
+    const unsigned long mask = 1ul << node;
+    syscall(SYS_mbind, p, bytes, 1 /* MPOL_PREFERRED */, &mask, 64ul, 0u);  // best effort
+  }
   memset(p, 0, bytes);  // fault in now, not on the first checkpoint
   return (uint8_t*)p;
+}
+
+// Pin the calling thread to the CPUs of NUMA node `node` (the helper thread
+// issues the I/O and folds CRCs next to the ring it reads).
+static void bind_thread_to_node(int node) {
+  if (node < 0) return;
+  FILE* f = fopen(("/sys/devices/system/node/node" + std::to_string(node) + "/cpulist").c_str(), "r");
+  if (!f) return;
+  char buf[4096] = {0};
+  const size_t n = fread(buf, 1, sizeof(buf) - 1, f);
+  fclose(f);
+  buf[n] = 0;
+  cpu_set_t set;
+  CPU_ZERO(&set);
+  int cpus = 0;
+  for (char* tok = strtok(buf, ",\n"); tok; tok = strtok(nullptr, ",\n")) {
+    int a = -1, b = -1;
+    if (sscanf(tok, "%d-%d", &a, &b) == 2) {
+    } else if (sscanf(tok, "%d", &a) == 1) {
+      b = a;
+    } else {
+      continue;
+    }
+    for (int x = a; x <= b && x < CPU_SETSIZE; ++x, ++cpus) CPU_SET(x, &set);
+  }
+  if (cpus) pthread_setaffinity_np(pthread_self(), sizeof(set), &set);
 }
 
 int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, fp_ctx** out) {
@@ -781,8 +836,13 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
     c->fault_eio_at = strtoll(f, nullptr, 10);
     if (const char* at = strchr(f, '@')) c->fault_rank = atoi(at + 1);
   }
+  if (const char* f = getenv("FP_FAULT_KILL_AT")) {
+    c->fault_kill_at = strtoll(f, nullptr, 10);
+    if (const char* at = strchr(f, '@')) c->fault_kill_rank = atoi(at + 1);
+  }
   c->ring_bytes = (size_t)cfg.ring_slots * cfg.slot_bytes;
-  c->ring = alloc_ring(c->ring_bytes);
+  c->numa_node = env_u64("FP_NUMA", 1) ? gpu_numa_node(cuda_device) : -1;
+  c->ring = alloc_ring(c->ring_bytes, c->numa_node);
   if (!c->ring) {
     delete c;
     return -ENOMEM;
@@ -877,7 +937,10 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
                                                                                    : FP_PACK_V4,
                                                      cuda_device);
   }
-  c->th = std::thread([c] { c->helper(); });
+  c->th = std::thread([c] {
+    bind_thread_to_node(c->numa_node);
+    c->helper();
+  });
   *out = c;
   return 0;
 }
@@ -910,6 +973,7 @@ int fp_ckpt_begin(fp_ctx* c, const fp_tensor* t, size_t n, const char* path, int
   c->st.err_offset = -1;
   c->st.image_bytes = c->plan.image_bytes;
   c->st.header_bytes = c->plan.header_bytes;
+  c->st.numa_node = c->numa_node;
   if (!c->host) CK(cudaEventRecord(c->ev_producer, (cudaStream_t)producer_stream));
   std::lock_guard<std::mutex> g(c->mu);
   c->t_begin = t0;
@@ -1067,7 +1131,7 @@ static int io_bench(const char* dir, uint64_t bytes, const fp_config* cfg_in, in
   if (r) return r;
   bytes = round_up(bytes, cfg.alignment);
   const size_t ring_bytes = (size_t)cfg.ring_slots * cfg.slot_bytes;
-  uint8_t* ring = alloc_ring(ring_bytes);
+  uint8_t* ring = alloc_ring(ring_bytes, -1);
   if (!ring) return -ENOMEM;
   for (size_t i = 0; i < ring_bytes; i += 8) {  // non-compressible pattern
     uint64_t x = (i + 0x9E3779B97F4A7C15ull) * 0xBF58476D1CE4E5B9ull;

@@ -96,7 +96,8 @@ class fp_stats(C.Structure):
                 ("t_io_stall", C.c_double), ("max_inflight", C.c_uint32),
                 ("fallback", C.c_uint32), ("engine", C.c_int32), ("status", C.c_int32),
                 ("err_offset", C.c_int64), ("shard_crc32", C.c_uint32), ("crc_valid", C.c_uint32),
-                ("kernel_launches", C.c_uint64), ("crc_ms", C.c_double)]
+                ("kernel_launches", C.c_uint64), ("crc_ms", C.c_double),
+                ("numa_node", C.c_int32)]
 
 
 EXPORTS = ("fp_config_default", "fp_ckpt_init", "fp_ckpt_begin", "fp_ckpt_fence", "fp_ckpt_wait",
