@@ -186,6 +186,18 @@ typedef struct fp_stats {
                               placed on (the GPU's; -1: unknown / not placed)  */
 } fp_stats;
 
+/* ---- statistics of the last load (fp_ckpt_load / fp_ckpt_load_parallel) -- */
+typedef struct fp_load_stats {
+  uint64_t bytes_read;      /* bytes this rank read from storage                  */
+  uint64_t kernel_launches; /* library kernels launched (unpack, page CRCs)       */
+  double   t_total;         /* s, call -> return                                  */
+  int32_t  exchange;        /* 0: none (dp_size 1, or fp_ckpt_load); 1: one
+                               comm->allgather_bytes per chunk + fp_unpack_v4;
+                               2: peer memory (fp_unpack_peer reads every
+                               writer's partition from its device buffer)      */
+  int32_t  status;          /* return code of that load                           */
+} fp_load_stats;
+
 typedef struct fp_ctx fp_ctx;
 
 /* Fill *cfg with the defaults above (env overrides: FP_RING_SLOTS,
@@ -259,18 +271,37 @@ int fp_ckpt_load(fp_ctx *ctx, const fp_tensor *t, size_t n, const char *path,
  * loads its checkpoint partition, if any, into GPU memory, and (ii) performs
  * an allgather"): rank r reads ONLY its own shard file, in slot_bytes chunks
  * (O_DIRECT through the pinned ring, ring_slots chunks ahead, then H2D; with
- * FP_IO_GDS, cuFileRead into device memory instead); every chunk of the replicated
- * partitions is exchanged with one comm->allgather_bytes call (bytes =
- * slot_bytes per rank; ranks whose partition is shorter send padding) and the
- * unpack kernel scatters the gathered bytes into t[i] on `stream`; the rank's
- * own local region comes from its own shard. GHDR / LHDR bytes are checked
- * against the target list after the exchange. Collective: every rank of the
- * DP group calls it together; a failure on any rank is returned on all ranks
- * (status all-reduce before the first exchange and at the end). Synchronous.
- * Errors: those of fp_ckpt_load, plus -ENOSYS when dp_size > 1 and
- * comm->allgather_bytes is NULL.                                              */
+ * FP_IO_GDS, cuFileRead into device memory instead).
+ * Exchange of the replicated partitions (fp_load_stats.exchange):
+ *   2 = peer memory (default for device state, dp_size > 1): the whole own
+ *       replicated partition is copied into a device buffer of this ctx
+ *       (part bytes + 4 B per chunk of ready flags), the buffers are mapped
+ *       into every rank (CUDA IPC handles exchanged with comm->allgather_u64;
+ *       the same pointers for ranks that are threads of one process) and one
+ *       fp_unpack_peer launch per chunk on `stream` scatters the chunk of
+ *       every writer straight from its buffer into t[i] (P2P loads over
+ *       NVLink), each CTA first waiting for the writers' ready flags (set by
+ *       their copy engines). FP_LOAD_EXCHANGE=peer requires it (-ENOSYS if a
+ *       buffer cannot be mapped), =nccl disables it. FP_PEER_TIMEOUT_S (600)
+ *       bounds the wait for a peer (then FP_ECOMM).
+ *   1 = gathered (host state, or no IPC): one comm->allgather_bytes per chunk
+ *       (bytes = slot_bytes per rank; shorter partitions send padding), then
+ *       fp_unpack_v4 from the gathered buffer.
+ * The rank's own local region comes from its own shard. GHDR / LHDR bytes
+ * are checked against the target list after the exchange and the own shard's
+ * CRC-32 (per extent) against the manifest. Collective: every rank of the DP
+ * group calls it together; a failure on any rank is returned on all ranks
+ * (status all-reduce before the first exchange and at the end). The targets
+ * are written as chunks arrive: on an error return they hold unspecified
+ * bytes. Synchronous.
+ * Errors: those of fp_ckpt_load, plus -ENOSYS when dp_size > 1, peer mode is
+ * unavailable and comm->allgather_bytes is NULL; FP_ECOMM.                    */
 int fp_ckpt_load_parallel(fp_ctx *ctx, const fp_tensor *t, size_t n, const char *path,
                           int dp_rank, int dp_size, void *stream);
+
+/* Statistics of the last fp_ckpt_load / fp_ckpt_load_parallel on this ctx.
+ * 0, or -EINVAL for a NULL argument.                                          */
+int fp_ckpt_load_stats(fp_ctx *ctx, fp_load_stats *out);
 
 /* Image facts of the last planned checkpoint of this ctx: image/header bytes and
  * this rank's extents as (image_offset, file_offset, length) triples.

@@ -182,6 +182,17 @@ void ExtentCrc::add_bytes(uint64_t fo, const uint8_t* p, uint64_t n) {
   }
 }
 
+void ExtentCrc::add_raw(uint64_t fo, uint64_t n, uint32_t raw) {
+  if (!n) return;
+  const size_t i = find(fo);
+  if (i >= beg_.size() || fo != beg_[i] + done_[i] || done_[i] + n > len_[i]) {
+    ok_ = false;
+    return;
+  }
+  raw_[i] = gf_mul(gf_x8n(n), raw_[i]) ^ raw;
+  done_[i] += n;
+}
+
 bool ExtentCrc::complete() const {
   for (size_t i = 0; i < beg_.size(); ++i)
     if (done_[i] != len_[i]) return false;

@@ -88,7 +88,9 @@ struct fp_ctx {
   //  so the events time the kernel, not the host API latency of an idle stream
   //  done: id of the checkpoint whose shard became durable (or failed), waited
   //  for on the caller's stream by fp_ckpt_fence
-  volatile uint32_t* h_sig = nullptr;  // [0] gate, [16] done, [32] fence timeout
+  // [0] gate, [16] done, [32] fence timeout, [48] constant 1 (source of the
+  // peer-exchange ready flags), [64] peer-exchange timeout
+  volatile uint32_t* h_sig = nullptr;
   uint32_t* d_sig = nullptr;
   bool gate_on = false;
   uint32_t gate_seq = 0;
@@ -148,6 +150,7 @@ struct fp_ctx {
   std::mutex mu;
   std::condition_variable cv;
   enum State { IDLE, PENDING, RUNNING, DONE } state = IDLE;
+  fp_load_stats ld{};  // of the last load on this context
   bool stop = false;
   int result = 0;
   fp_stats st;

@@ -155,6 +155,19 @@ int pack_launch(int impl, const Item* d_items, uint32_t n_items, uint8_t* d_slab
 int unpack_launch(const Item* d_items, uint32_t n_items, const uint8_t* d_slab, int ctas,
                   void* stream);
 int pack_default_ctas(int impl, int device);
+// peer-exchange load (fp_unpack_peer): writer w's replicated partition at
+// base[w], its per-chunk ready flags (u32, nonzero = landed) at flag[w]
+constexpr int kMaxPeers = 64;
+struct PeerTab {
+  uint64_t base[kMaxPeers];
+  uint64_t flag[kMaxPeers];
+};
+// items of exchange chunk `chunk` (Item.len bits 24..31 = writer) scattered
+// from base[w] + chunk * ch_bytes + Item.dst after waiting for flag[w][chunk]
+// of every writer in wmask (max_ns: then *d_timed_out = 1)
+int unpack_peer_launch(const Item* d_items, uint32_t n_items, const PeerTab* d_tab, uint32_t chunk,
+                       uint64_t ch_bytes, uint64_t wmask, uint64_t max_ns, uint32_t* d_timed_out,
+                       int ctas, void* stream);
 // one-warp kernel on `stream` that waits until the mapped word *d_flag
 // reaches `value` (or max_ns passes; then *d_timed_out = 1 if non-null)
 int flag_wait_launch(const uint32_t* d_flag, uint32_t value, uint64_t max_ns,
@@ -201,6 +214,8 @@ class ExtentCrc {
   bool pages_ok(uint64_t fo, uint64_t n) const;
   void add_pages(uint64_t fo, const uint32_t* page_crc, uint64_t n_pages);
   void add_bytes(uint64_t fo, const uint8_t* p, uint64_t n);
+  // a run [fo, fo + n) inside one extent given as its raw CRC
+  void add_raw(uint64_t fo, uint64_t n, uint32_t raw);
   size_t n() const { return beg_.size(); }
   uint64_t len(size_t i) const { return len_[i]; }
   bool complete(size_t i) const { return ok_ && done_[i] == len_[i]; }

@@ -417,6 +417,8 @@ static int pread_all(int fd, void* buf, uint64_t len, uint64_t off) {
 int fp_ckpt_load(fp_ctx* c, const fp_tensor* t, size_t n, const char* path, int dp_rank,
                  int dp_size, void* stream) {
   NvtxRange nv("fp.load");
+  if (c) memset(&c->ld, 0, sizeof(c->ld));
+  const double t_call = now_s();
   if (!c || (!t && n) || !path || dp_size < 1 || dp_rank < 0 || dp_rank >= dp_size)
     return -EINVAL;
   if (dp_size > 1 && !c->has_comm) return -EINVAL;
@@ -662,6 +664,10 @@ int fp_ckpt_load(fp_ctx* c, const fp_tensor* t, size_t n, const char* path, int 
   if (!status) status = lcrc.flush();
   for (int w = 0; w < dp_size && !status && want_crc; ++w)
     status = verify_crc(acc[w], recs[w], shard_file(w, dp_size));
+  c->ld.bytes_read = total;
+  c->ld.kernel_launches = C * (c->host ? 0 : 1) + lcrc.launches();
+  c->ld.status = status;
+  c->ld.t_total = now_s() - t_call;
   if (d_items) cudaFree(d_items);
   close_all();
   return status;
@@ -681,7 +687,7 @@ static int status_min(fp_ctx* c, int k, int s) {
 // Items scattering image range [io0, io0+len) (located at buffer offset
 // `base`) into the tensors; header/padding pieces are skipped.
 static void scatter_items(const std::vector<Piece>& pcs, uint64_t io0, uint64_t len, uint64_t base,
-                          std::vector<Item>* items) {
+                          std::vector<Item>* items, uint32_t len_tag) {
   const uint64_t io1 = io0 + len;
   size_t lo = 0, hi = pcs.size();
   while (lo < hi) {  // first piece ending after io0
@@ -698,7 +704,7 @@ static void scatter_items(const std::vector<Piece>& pcs, uint64_t io0, uint64_t 
     while (a < b) {
       const uint64_t nn = std::min<uint64_t>(b - a, kTile);
       items->push_back({pcs[i].src + (a - pcs[i].image_off), (uint32_t)(base + a - io0),
-                        (uint32_t)nn});
+                        (uint32_t)nn | len_tag});
       a += nn;
     }
   }
@@ -710,8 +716,9 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
   if (!c || (!t && n) || !path || dp_size < 1 || dp_rank < 0 || dp_rank >= dp_size)
     return -EINVAL;
   if (dp_size > 1 && !c->has_comm) return -EINVAL;
-  if (dp_size > 1 && !c->comm.allgather_bytes) return -ENOSYS;
   if (c->cfg.io_engine == FP_IO_NULL) return -EINVAL;
+  const double t_call = now_s();
+  memset(&c->ld, 0, sizeof(c->ld));
   {
     std::lock_guard<std::mutex> g(c->mu);
     if (c->state != fp_ctx::IDLE) return -EBUSY;
@@ -769,10 +776,10 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
   }
   // 3) geometry: replicated partitions (the writer's page-balanced split)
   const uint64_t A = p.align, Q = p.rep_bytes / A;
-  auto first_pg = [&](int w) {
+  auto part_off = [&](int w) {  // image offset of writer w's partition
     uint64_t f, n;
     rep_partition(Q, k, p.writer_stride, w, &f, &n);
-    return f;
+    return f * A;
   };
   auto part_bytes = [&](int w) {
     uint64_t f, n;
@@ -782,47 +789,154 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
   const uint64_t CH = c->cfg.slot_bytes, M = part_bytes(0);  // writer 0 has the largest part
   const uint64_t nrep = (M + CH - 1) / CH;
   const bool dev = !c->host;
+  cudaStream_t st = (cudaStream_t)stream;
   Plan rp = p;  // whole replicated region (+ own local region) as one source map
   rp.extents.assign(1, {0, 0, p.rep_bytes});
   if (!p.regions.empty()) rp.extents.push_back({p.regions[rank].first, p.rep_bytes,
                                                 p.regions[rank].second});
   plan_pieces(&rp, c->rep, c->loc, 0);  // header pieces -> src 0 (skipped)
+  const uint64_t lreg_off = p.regions.empty() ? 0 : p.regions[rank].first;
+  const uint64_t lreg_len = p.regions.empty() ? 0 : p.regions[rank].second;
+  const uint64_t nloc = (lreg_len + CH - 1) / CH;
+  const uint64_t total_chunks = nrep + nloc;
+  // this rank's bytes of chunk j: (length, offset in the own shard file)
+  auto my_span = [&](uint64_t j, uint64_t* foff) -> uint64_t {
+    if (j < nrep) {
+      const uint64_t pb = part_bytes(rank);
+      *foff = j * CH;
+      return j * CH < pb ? std::min(CH, pb - j * CH) : 0;
+    }
+    const uint64_t jj = j - nrep;
+    *foff = part_bytes(rank) + jj * CH;
+    return std::min(CH, lreg_len - jj * CH);
+  };
+
+  // 4) the exchange. Default (device state, k > 1): over peer memory — each
+  // rank's whole replicated partition lands in its own device buffer, the
+  // buffers are mapped into every rank (CUDA IPC; same address space for
+  // thread ranks) and one unpack launch per chunk reads every writer's chunk
+  // straight from its buffer (fp_unpack_peer). Fallback (host state, IPC
+  // unavailable, FP_LOAD_EXCHANGE=nccl): one comm->allgather_bytes per chunk
+  // into a gathered buffer, then fp_unpack_v4. Collective decision.
+  const char* xm = getenv("FP_LOAD_EXCHANGE");
+  const std::string xmode = xm ? xm : "auto";
+  int status = 0;
+  uint8_t* pbuf = nullptr;  // peer mode: [ready flags | own replicated partition]
+  const uint64_t flag_bytes = round_up(std::max<uint64_t>(nrep, 1) * 4, 4096);
+  PeerTab tab{};
+  std::vector<void*> opened;
+  bool peer = false;
+  if (dev && k > 1 && k <= kMaxPeers && xmode != "nccl") {
+    int ok = 1;
+    cudaIpcMemHandle_t h{};
+    if (cudaMalloc(&pbuf, flag_bytes + std::max<uint64_t>(part_bytes(rank), 4096)) != cudaSuccess) {
+      cudaGetLastError();
+      pbuf = nullptr;
+      ok = 0;
+    }
+    if (ok && cudaMemset(pbuf, 0, flag_bytes) != cudaSuccess) ok = 0;
+    const bool ipc_ok = ok && cudaIpcGetMemHandle(&h, pbuf) == cudaSuccess;
+    if (!ipc_ok) cudaGetLastError();
+    std::vector<uint64_t> mine(12, 0), all(12 * (size_t)k, 0);
+    mine[0] = (uint64_t)getpid();
+    mine[1] = (uint64_t)(int64_t)c->dev;
+    mine[2] = ipc_ok ? 1 : 0;
+    mine[3] = (uint64_t)(uintptr_t)pbuf;
+    memcpy(&mine[4], &h, sizeof(h));
+    int32_t v = ok;
+    if (c->comm.allreduce_min_i32(c->comm.ctx, &v)) v = -1;
+    if (v == 1 && c->comm.allgather_u64(c->comm.ctx, mine.data(), all.data(), 12)) v = -1;
+    if (v == 1) {
+      int mok = 1;
+      for (int w = 0; w < k && mok; ++w) {
+        const uint64_t* q = &all[12 * (size_t)w];
+        void* ptr = nullptr;
+        if (q[0] == (uint64_t)getpid()) {  // same process (thread ranks): same address space
+          ptr = (void*)(uintptr_t)q[3];
+          const int pd = (int)(int64_t)q[1];
+          if (pd != c->dev) {
+            const cudaError_t e = cudaDeviceEnablePeerAccess(pd, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) mok = 0;
+            cudaGetLastError();
+          }
+        } else if (q[2]) {
+          cudaIpcMemHandle_t ph;
+          memcpy(&ph, &q[4], sizeof(ph));
+          if (cudaIpcOpenMemHandle(&ptr, ph, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
+            opened.push_back(ptr);
+          } else {
+            cudaGetLastError();
+            mok = 0;
+          }
+        } else {
+          mok = 0;
+        }
+        tab.flag[w] = (uint64_t)(uintptr_t)ptr;
+        tab.base[w] = (uint64_t)(uintptr_t)ptr + flag_bytes;
+      }
+      v = mok;
+      if (c->comm.allreduce_min_i32(c->comm.ctx, &v)) v = -1;
+    }
+    peer = v == 1;
+    if (!peer) {
+      for (void* q : opened) cudaIpcCloseMemHandle(q);
+      opened.clear();
+      if (pbuf) cudaFree(pbuf);
+      pbuf = nullptr;
+      if (xmode == "peer") status = -ENOSYS;  // peer exchange was required
+      if (v < 0) status = FP_ECOMM;
+    }
+  }
+  if (!status && k > 1 && !peer && !c->comm.allgather_bytes) status = -ENOSYS;
+  c->ld.exchange = k == 1 ? 0 : peer ? 2 : 1;
+
+  // work items: chunk j = the j-th CH bytes of every writer's partition
   std::vector<Item> items;
   std::vector<uint32_t> lo(1, 0);
+  std::vector<uint64_t> wmask(nrep, 0);
   for (uint64_t j = 0; j < nrep; ++j) {
     for (int w = 0; w < k; ++w) {
       const uint64_t pb = part_bytes(w);
       if (j * CH >= pb) continue;
-      scatter_items(rp.pieces, first_pg(w) * A + j * CH, std::min(CH, pb - j * CH),
-                    (uint64_t)w * CH, &items);
+      wmask[j] |= 1ull << (w & 63);
+      // peer: offset inside writer w's chunk + writer tag in len bits 24..31;
+      // gathered buffer: offset w*CH
+      scatter_items(rp.pieces, part_off(w) + j * CH, std::min(CH, pb - j * CH),
+                    peer ? 0 : (uint64_t)w * CH, &items, peer ? (uint32_t)w << 24 : 0);
     }
     lo.push_back((uint32_t)items.size());
   }
-  const uint64_t lreg_off = p.regions.empty() ? 0 : p.regions[rank].first;
-  const uint64_t lreg_len = p.regions.empty() ? 0 : p.regions[rank].second;
-  const uint64_t nloc = (lreg_len + CH - 1) / CH;
   for (uint64_t j = 0; j < nloc; ++j) {
-    scatter_items(rp.pieces, lreg_off + j * CH, std::min(CH, lreg_len - j * CH), 0, &items);
+    scatter_items(rp.pieces, lreg_off + j * CH, std::min(CH, lreg_len - j * CH), 0, &items, 0);
     lo.push_back((uint32_t)items.size());
   }
-  // 4) buffers: send = one chunk, recv = k chunks (device, or host for host state)
+  // 5) buffers: send = one chunk (two with GDS), recv = k chunks (gathered
+  // mode only); device, or host for host state
   uint8_t *send = nullptr, *recv = nullptr;
   Item* d_items = nullptr;
-  cudaStream_t st = (cudaStream_t)stream;
-  int status = 0;
+  PeerTab* d_tab = nullptr;
   // GPUDirect Storage: own-shard chunks are read with cuFileRead
-  // straight into a double-buffered device `send` (no ring, no H2D)
+  // straight into device memory (no ring, no H2D)
   const bool use_gds = dev && c->gds;
   void* gfh = nullptr;
   if (use_gds && !status && fd >= 0) status = gds_handle_open(fd, &gfh);
-  if (dev) {
+  cudaStream_t cs = c->stream;     // peer mode: H2D copies + ready flags (copy engine only)
+  cudaStream_t crcs = nullptr;     // peer mode: page CRCs (never waited on before the end)
+  cudaEvent_t ev_h2d = nullptr;
+  if (dev && !status) {
     if (cudaMalloc(&send, CH * (use_gds ? 2 : 1)) != cudaSuccess ||
-        cudaMalloc(&recv, CH * k) != cudaSuccess ||
+        (!peer && cudaMalloc(&recv, CH * k) != cudaSuccess) ||
+        (peer && (cudaMalloc(&d_tab, sizeof(PeerTab)) != cudaSuccess ||
+                  cudaMemcpy(d_tab, &tab, sizeof(PeerTab), cudaMemcpyHostToDevice) != cudaSuccess)) ||
         (!items.empty() && (cudaMalloc(&d_items, items.size() * sizeof(Item)) != cudaSuccess ||
                             cudaMemcpy(d_items, items.data(), items.size() * sizeof(Item),
                                        cudaMemcpyHostToDevice) != cudaSuccess)))
       status = -ENOMEM;
-  } else {
+    if (peer && !status &&
+        (cudaStreamCreateWithFlags(&crcs, cudaStreamNonBlocking) != cudaSuccess ||
+         cudaEventCreateWithFlags(&ev_h2d, cudaEventDisableTiming) != cudaSuccess))
+      status = FP_ECUDA;
+  } else if (!dev) {
     send = (uint8_t*)aligned_alloc(4096, round_up(CH, 4096));
     recv = (uint8_t*)aligned_alloc(4096, round_up(CH * k, 4096));
     if (!send || !recv) status = -ENOMEM;
@@ -837,11 +951,10 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
     if (a >= b) return;
     if (dev)
       cudaMemcpyAsync(out->data() + (a - h0), buf + base + (a - io0), b - a,
-                      cudaMemcpyDeviceToHost, st);
+                      cudaMemcpyDefault, st);
     else
       memcpy(out->data() + (a - h0), buf + base + (a - io0), b - a);
   };
-  const uint64_t total_chunks = nrep + nloc;
   // CRC-32 of the own shard as it is read (page CRCs on the GPU, folded per
   // extent on the host), checked against the manifest
   const bool check_crc = !(c->cfg.flags & FP_CFG_NO_CRC);
@@ -849,22 +962,28 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
   acc.reset(c->all_extents[rank]);
   const ShardCrcRec rec = crc_record(m, rank, c->all_extents[rank].size());
   const bool run = status == 0;  // agreed on every rank by the all-reduce above
-  // this rank's bytes of chunk j: (length, offset in the own shard file)
-  auto my_span = [&](uint64_t j, uint64_t* foff) -> uint64_t {
-    if (j < nrep) {
-      const uint64_t pb = part_bytes(rank);
-      *foff = j * CH;
-      return j * CH < pb ? std::min(CH, pb - j * CH) : 0;
-    }
-    const uint64_t jj = j - nrep;
-    *foff = part_bytes(rank) + jj * CH;
-    return std::min(CH, lreg_len - jj * CH);
-  };
   LoadCrc lcrc(c, [&](uint64_t j, const uint32_t* pages) {
     uint64_t fo = 0;
     const uint64_t n = my_span(j, &fo);
     acc.add_pages(fo, pages, n / 4096);
   });
+  // peer mode keeps every page CRC of the own shard (4 B per 4 KiB) until
+  // the end: no host wait on a CRC kernel while unpacks spin on peers' flags
+  uint32_t* h_allpc = nullptr;
+  uint32_t* d_allpc = nullptr;
+  const uint64_t shard_pages = (part_bytes(rank) + lreg_len) / 4096 + 1;
+  if (peer && run && check_crc &&
+      (cudaHostAlloc(&h_allpc, shard_pages * 4, cudaHostAllocPortable) != cudaSuccess ||
+       cudaMalloc(&d_allpc, shard_pages * 4) != cudaSuccess))
+    status = -ENOMEM;
+  // peer mode, replicated chunks: (file offset, bytes, raw CRC or ~0 = pages
+  // in d_allpc), folded in file order at the end
+  struct Deferred {
+    uint64_t fo, n;
+    uint32_t raw;
+    bool pages;
+  };
+  std::vector<Deferred> deferred;
   // own-shard reads run R chunks ahead of the exchange + scatter
   ReadAhead ra(c, run && !use_gds ? total_chunks : 0, dev,
                [&](uint64_t j, std::vector<ReadReq>* out) -> int {
@@ -875,6 +994,8 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
                       (uint32_t)std::min<uint64_t>(c->cfg.sqe_bytes, len - pos)});
     return 0;
   });
+  const uint64_t spin_ns = env_u64("FP_PEER_TIMEOUT_S", 600) * 1000000000ull;
+  uint64_t launches = 0;
   for (uint64_t j = 0; run && j < total_chunks; ++j) {  // every rank runs every exchange
     const bool is_rep = j < nrep;
     const uint32_t s = (uint32_t)(j % R);
@@ -883,17 +1004,25 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
     const uint64_t mylen = my_span(j, &foff);
     const bool gpu_crc =
         check_crc && dev && mylen % 4096 == 0 && c->d_crc_tabs && acc.pages_ok(foff, mylen);
-    auto host_crc = [&](const uint8_t* p) {  // in order behind the pending page folds
+    auto host_crc = [&](const uint8_t* q) {  // in order behind the pending page folds
+      if (peer && is_rep) {
+        deferred.push_back({foff, mylen, crc_raw_update(0, q, mylen), false});
+        return;
+      }
       if (lcrc.flush() && !status) status = FP_ECUDA;
-      acc.add_bytes(foff, p, mylen);
+      acc.add_bytes(foff, q, mylen);
     };
-    uint8_t* sbuf = use_gds ? send + (j & 1) * CH : send;
+    // where this rank's bytes of chunk j land on the device
+    uint8_t* sbuf = peer && is_rep ? pbuf + flag_bytes + j * CH
+                    : use_gds ? send + (j & 1) * CH : send;
+    cudaStream_t xs = peer && is_rep ? cs : st;  // stream of the H2D
     if (use_gds) {
       // the unpack of chunk j-2 read this half: wait for it, then read into it
-      if (j >= 2 && cudaEventSynchronize(c->gds_ev[j & 1]) != cudaSuccess && !status)
+      if (!(peer && is_rep) && j >= 2 && cudaEventSynchronize(c->gds_ev[j & 1]) != cudaSuccess &&
+          !status)
         status = FP_ECUDA;
       if (mylen && !status) {
-        gds_post(c->gds_pool, false, gfh, send, (j & 1) * CH, foff, mylen,
+        gds_post(c->gds_pool, false, gfh, sbuf, 0, foff, mylen,
                  std::max<uint64_t>(c->cfg.sqe_bytes, 4ull << 20));
         int rr = gds_wait(c->gds_pool, nullptr);
         if (rr && !status) status = rr;  // keep exchanging so the collectives stay matched
@@ -906,22 +1035,41 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
       }
     } else {
       int rr = status ? 0 : ra.wait(j);
-      if (rr && !status) status = rr;  // keep exchanging so the collectives stay matched
+      if (rr && !status) status = rr;  // keep exchanging so the peers are not left waiting
       if (check_crc && mylen && !gpu_crc && !status) host_crc(slot);
     }
     if (dev) {
       if (!use_gds) {
-        if (mylen && cudaMemcpyAsync(send, slot, mylen, cudaMemcpyHostToDevice, st) != cudaSuccess)
-          status = status ? status : FP_ECUDA;
-        cudaEventRecord(c->ev_d2h[s], st);
+        if (mylen && !status &&
+            cudaMemcpyAsync(sbuf, slot, mylen, cudaMemcpyHostToDevice, xs) != cudaSuccess)
+          status = FP_ECUDA;
+        cudaEventRecord(c->ev_d2h[s], xs);
       }
-      if (gpu_crc && mylen && lcrc.enqueue(j, sbuf, mylen, st))
-        status = status ? status : FP_ECUDA;
+      if (peer && is_rep && mylen) {
+        // ready flag of chunk j: a 4-byte copy behind the data on the copy
+        // stream (no kernel: a flag never waits for an SM)
+        if (cudaMemcpyAsync(pbuf + 4 * j, (const void*)&c->h_sig[48], 4, cudaMemcpyHostToDevice,
+                            cs) != cudaSuccess && !status)
+          status = FP_ECUDA;
+      }
+      if (gpu_crc && mylen) {
+        int e = 0;
+        if (peer && is_rep) {  // deferred: CRC stream after the H2D, pages kept to the end
+          e = cudaEventRecord(ev_h2d, xs) != cudaSuccess ||
+              cudaStreamWaitEvent(crcs, ev_h2d, 0) != cudaSuccess ||
+              crc_pages_launch(sbuf, mylen, c->d_crc_tabs, d_allpc + foff / 4096, crcs);
+          deferred.push_back({foff, mylen, 0, true});
+        } else {
+          e = lcrc.enqueue(j, sbuf, mylen, st);
+        }
+        if (e && !status) status = FP_ECUDA;
+        ++launches;
+      }
     } else if (mylen) {
       memcpy(send, slot, mylen);
     }
     const uint8_t* src = sbuf;
-    if (is_rep) {
+    if (is_rep && !peer) {
       if (k > 1) {
         if (c->comm.allgather_bytes(c->comm.ctx, sbuf, recv, CH, dev ? 1 : 0, stream)) {
           status = status ? status : FP_ECOMM;
@@ -932,28 +1080,65 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
       for (int w = 0; w < k; ++w) {
         const uint64_t pb = part_bytes(w);
         if (j * CH >= pb) continue;
-        fetch_hdr(src, first_pg(w) * A + j * CH, std::min(CH, pb - j * CH),
+        fetch_hdr(src, part_off(w) + j * CH, std::min(CH, pb - j * CH),
                   k > 1 ? (uint64_t)w * CH : 0, 0, &ghdr_got);
       }
-    } else {
+    } else if (!is_rep) {
       const uint64_t jj = j - nrep;
       fetch_hdr(src, lreg_off + jj * CH, mylen, 0, lreg_off, &lhdr_got);
     }
     const uint32_t i0 = lo[j], i1 = lo[j + 1];
-    if (i1 > i0 && status == 0) {
+    if (peer && is_rep) {
+      // runs even after a local error: a launch per chunk on every rank keeps
+      // the flags of the peers' buffers consumed in order (status decides)
+      if (unpack_peer_launch(d_items + i0, i1 - i0, d_tab, (uint32_t)j, CH, wmask[j], spin_ns,
+                             c->d_sig + 64, c->pack_ctas, st) && !status)
+        status = FP_ECUDA;
+      ++launches;
+    } else if (i1 > i0 && status == 0) {
       if (dev) {
         if (unpack_launch(d_items + i0, i1 - i0, src, c->pack_ctas, st)) status = FP_ECUDA;
+        ++launches;
       } else {
         for (uint32_t i = i0; i < i1; ++i)
           memcpy((void*)(uintptr_t)items[i].src, src + items[i].dst, items[i].len);
       }
     }
-    if (use_gds && cudaEventRecord(c->gds_ev[j & 1], st) != cudaSuccess && !status)
+    if (use_gds && !(peer && is_rep) && cudaEventRecord(c->gds_ev[j & 1], st) != cudaSuccess &&
+        !status)
       status = FP_ECUDA;  // this half is free once the work above has run
     ra.release(j);
   }
   ra.finish();  // reads still in flight after an error land before the ring is reused
   if (dev && cudaStreamSynchronize(st) != cudaSuccess && !status) status = FP_ECUDA;
+  if (peer) {
+    if (cudaStreamSynchronize(cs) != cudaSuccess && !status) status = FP_ECUDA;
+    if (__atomic_exchange_n(&c->h_sig[64], 0u, __ATOMIC_ACQ_REL) && !status) {
+      fprintf(stderr, "fastpersist: a peer's chunk never arrived (peer exchange timed out)\n");
+      status = FP_ECOMM;
+    }
+    // GHDR bytes straight from the writers' buffers
+    for (int w = 0; w < k && run && !status; ++w) {
+      const uint64_t a0 = part_off(w), pb = part_bytes(w);
+      const uint64_t a1 = std::min<uint64_t>(a0 + pb, ghdr_got.size());
+      if (a0 < a1 && cudaMemcpy(ghdr_got.data() + a0, (const void*)(uintptr_t)tab.base[w],
+                                a1 - a0, cudaMemcpyDefault) != cudaSuccess)
+        status = FP_ECUDA;
+    }
+    if (crcs && cudaStreamSynchronize(crcs) != cudaSuccess && !status) status = FP_ECUDA;
+    if (!status && run && check_crc && !deferred.empty()) {
+      if (h_allpc && cudaMemcpy(h_allpc, d_allpc, shard_pages * 4, cudaMemcpyDeviceToHost) !=
+                         cudaSuccess)
+        status = FP_ECUDA;
+      // replicated chunks in file order (the local region's are already in acc)
+      for (const Deferred& d : deferred) {
+        if (d.pages)
+          acc.add_pages(d.fo, h_allpc + d.fo / 4096, d.n / 4096);
+        else
+          acc.add_raw(d.fo, d.n, d.raw);
+      }
+    }
+  }
   if (!status && run && check_crc) {
     status = lcrc.flush();
     if (!status) status = verify_crc(acc, rec, sf);
@@ -964,12 +1149,23 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
                     "target tensors (corrupt or different state)\n");
     status = FP_ECORRUPT;
   }
+  for (void* q : opened) cudaIpcCloseMemHandle(q);  // before the owners free (barrier below)
   status = status_min(c, k, status);
+  c->ld.kernel_launches = launches;
+  c->ld.bytes_read = part_bytes(rank) + lreg_len;
+  c->ld.status = status;
+  c->ld.t_total = now_s() - t_call;
   if (gfh) gds_handle_close(gfh);
+  if (crcs) cudaStreamDestroy(crcs);
+  if (ev_h2d) cudaEventDestroy(ev_h2d);
+  if (h_allpc) cudaFreeHost(h_allpc);
+  if (d_allpc) cudaFree(d_allpc);
   if (dev) {
     if (send) cudaFree(send);
     if (recv) cudaFree(recv);
     if (d_items) cudaFree(d_items);
+    if (d_tab) cudaFree(d_tab);
+    if (pbuf) cudaFree(pbuf);
   } else {
     free(send);
     free(recv);

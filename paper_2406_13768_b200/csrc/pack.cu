@@ -51,8 +51,20 @@ __device__ __forceinline__ void st_v4(uint4* p, const uint4& v) {
                : "memory");
 }
 
+// coherent 16-B load (data another agent may have written while this kernel
+// was already running: the peer-exchange unpack)
+__device__ __forceinline__ uint4 ld_coherent(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
 // Copy `len` bytes src -> dst with `nthr` threads (index t). src == nullptr
 // means zero fill. Vector body when src and dst share the same 16-B phase.
+// kCoherent: plain (coherent) loads instead of the read-only .nc path.
+template <bool kCoherent = false>
 __device__ __forceinline__ void copy_bytes(uint8_t* __restrict__ dst,
                                            const uint8_t* __restrict__ src, uint32_t len,
                                            int t, int nthr) {
@@ -74,7 +86,7 @@ __device__ __forceinline__ void copy_bytes(uint8_t* __restrict__ dst,
 #pragma unroll
       for (int u = 0; u < kV4Unroll; ++u) {
         const uint32_t j = base + (uint32_t)u * nthr + t;
-        if (j < n16) v[u] = ld_stream(s16 + j);
+        if (j < n16) v[u] = kCoherent ? ld_coherent(s16 + j) : ld_stream(s16 + j);
       }
 #pragma unroll
       for (int u = 0; u < kV4Unroll; ++u) {
@@ -118,6 +130,51 @@ __global__ void __launch_bounds__(kV4Threads) fp_unpack_v4(const Item* __restric
     if (!it.src) continue;  // padding: nothing to restore
     copy_bytes(reinterpret_cast<uint8_t*>(it.src), slab + it.dst, it.len, threadIdx.x,
                kV4Threads);
+  }
+}
+
+// Parallel-load exchange over peer memory (§4.2: each rank
+// "(i) loads its checkpoint partition ... into GPU memory, and (ii) performs
+// an allgather"): every rank's replicated partition sits whole in its own
+// device buffer (CUDA IPC-mapped into the peers, or the same address space
+// for thread ranks); one launch per exchange chunk j scatters the chunk of
+// EVERY writer straight from the writers' buffers into the local tensors (P2P
+// loads over NVLink on a multi-GPU node), so the all-gather and the scatter
+// are one pass with no gathered copy. Before touching writer w's bytes a CTA
+// waits for w's ready flag of chunk j (set by w's copy engine right after
+// the chunk's H2D, stream-ordered), with a timeout that sets *timed_out.
+// Item.len carries the writer index in bits 24..31; Item.dst is the offset
+// inside the writer's chunk.
+__global__ void __launch_bounds__(kV4Threads) fp_unpack_peer(const Item* __restrict__ items,
+                                                             uint32_t n,
+                                                             const PeerTab* __restrict__ tab,
+                                                             uint32_t j, uint64_t ch_bytes,
+                                                             uint64_t wmask, uint64_t max_ns,
+                                                             uint32_t* __restrict__ timed_out) {
+  if (threadIdx.x < 64 && ((wmask >> threadIdx.x) & 1)) {
+    const uint32_t* f = reinterpret_cast<const uint32_t*>(tab->flag[threadIdx.x]) + j;
+    uint64_t t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+      uint32_t x;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(x) : "l"(f) : "memory");
+      if (x) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > max_ns) {
+        if (timed_out) asm volatile("st.release.sys.global.u32 [%0], 1;" ::"l"(timed_out) : "memory");
+        break;
+      }
+      __nanosleep(512);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+    const Item it = items[i];
+    if (!it.src) continue;
+    const uint32_t w = it.len >> 24, len = it.len & 0xFFFFFFu;
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(tab->base[w]) + j * ch_bytes + it.dst;
+    copy_bytes<true>(reinterpret_cast<uint8_t*>(it.src), src, len, threadIdx.x, kV4Threads);
   }
 }
 
@@ -706,6 +763,16 @@ int pack_crc_launch(const Item* d_items, const uint32_t* d_tile_lo, uint32_t n_t
   fp_pack_crc<<<grid, kPcThreads, kPcSmem, (cudaStream_t)stream>>>(d_items, d_tile_lo, n_tiles,
                                                                   d_slab, n_pages, d_tabs,
                                                                   d_page_crc);
+  return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
+}
+
+int unpack_peer_launch(const Item* d_items, uint32_t n_items, const PeerTab* d_tab, uint32_t chunk,
+                       uint64_t ch_bytes, uint64_t wmask, uint64_t max_ns, uint32_t* d_timed_out,
+                       int ctas, void* stream) {
+  if (!n_items) return 0;
+  const int grid = (int)((uint32_t)ctas < n_items ? (uint32_t)ctas : n_items);
+  fp_unpack_peer<<<grid, kV4Threads, 0, (cudaStream_t)stream>>>(d_items, n_items, d_tab, chunk,
+                                                               ch_bytes, wmask, max_ns, d_timed_out);
   return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
 }
 

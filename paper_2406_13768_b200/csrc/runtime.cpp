@@ -907,6 +907,7 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
         return fail(-ENOMEM);
       memset(hg, 0, 4096);
       c->h_sig = (volatile uint32_t*)hg;
+      c->h_sig[48] = 1;  // source word of the peer-exchange ready flags
       if (cudaHostGetDevicePointer(&dg, hg, 0) != cudaSuccess) return fail(FP_ECUDA);
       c->d_sig = (uint32_t*)dg;
       // The launch gate is measurement machinery (opt-in, FP_LAUNCH_GATE=1:
@@ -1050,6 +1051,12 @@ int fp_ckpt_wait(fp_ctx* c, fp_stats* out) {
   std::lock_guard<std::mutex> g(c->mu);
   c->state = fp_ctx::IDLE;
   return status;
+}
+
+int fp_ckpt_load_stats(fp_ctx* c, fp_load_stats* out) {
+  if (!c || !out) return -EINVAL;
+  *out = c->ld;
+  return 0;
 }
 
 int fp_ckpt_plan_info(fp_ctx* c, uint64_t* image_bytes, uint64_t* header_bytes,

@@ -100,9 +100,16 @@ class fp_stats(C.Structure):
                 ("numa_node", C.c_int32)]
 
 
+class fp_load_stats(C.Structure):
+    _fields_ = [("bytes_read", C.c_uint64), ("kernel_launches", C.c_uint64),
+                ("t_total", C.c_double), ("exchange", C.c_int32), ("status", C.c_int32)]
+
+
+EXCHANGES = {0: "none", 1: "allgather_bytes", 2: "peer"}
+
 EXPORTS = ("fp_config_default", "fp_ckpt_init", "fp_ckpt_begin", "fp_ckpt_fence", "fp_ckpt_wait",
-           "fp_ckpt_load", "fp_ckpt_load_parallel", "fp_ckpt_plan_info", "fp_ckpt_destroy", "fp_strerror",
-           "fp_io_bench", "fp_io_bench_read")
+           "fp_ckpt_load", "fp_ckpt_load_parallel", "fp_ckpt_load_stats", "fp_ckpt_plan_info",
+           "fp_ckpt_destroy", "fp_strerror", "fp_io_bench", "fp_io_bench_read")
 
 _lib = None
 
@@ -127,6 +134,7 @@ def lib():
                                C.c_int, C.c_int, C.c_void_p]
     L.fp_ckpt_load_parallel.argtypes = [C.c_void_p, C.POINTER(fp_tensor), C.c_size_t,
                                         C.c_char_p, C.c_int, C.c_int, C.c_void_p]
+    L.fp_ckpt_load_stats.argtypes = [C.c_void_p, C.POINTER(fp_load_stats)]
     L.fp_ckpt_plan_info.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                     C.POINTER(C.c_uint64), C.c_uint32, C.POINTER(C.c_uint32)]
     L.fp_ckpt_destroy.argtypes = [C.c_void_p]
@@ -397,17 +405,28 @@ class Checkpointer:
         self.begin(tensors, path, stream)
         return self.wait()
 
+    def load_stats(self):
+        ls = fp_load_stats()
+        _check(lib().fp_ckpt_load_stats(self.h, C.byref(ls)), "fp_ckpt_load_stats")
+        d = {f: getattr(ls, f) for f, _ in fp_load_stats._fields_}
+        d["exchange"] = EXCHANGES.get(d["exchange"], d["exchange"])
+        return d
+
     def load(self, tensors, path, stream=None):
+        """Single-box restore: every needed extent from whichever shard holds it."""
         arr, n, keep = self._table(tensors)
         _check(lib().fp_ckpt_load(self.h, arr, n, os.fsencode(path), self.rank, self.world,
                                   _stream_handle(stream, self.device)), "fp_ckpt_load")
+        return self.load_stats()
 
     def load_parallel(self, tensors, path, stream=None):
-        """The paper's two-step load: own shard + all-gather + unpack."""
+        """The paper's two-step load: own shard -> device, exchange over
+        peer memory (or all-gather) -> unpack. Returns the load statistics."""
         arr, n, keep = self._table(tensors)
         _check(lib().fp_ckpt_load_parallel(self.h, arr, n, os.fsencode(path), self.rank,
                                            self.world, _stream_handle(stream, self.device)),
                "fp_ckpt_load_parallel")
+        return self.load_stats()
 
     def plan_info(self):
         ib, hb, ne = C.c_uint64(), C.c_uint64(), C.c_uint32()

@@ -204,23 +204,32 @@ def test_c2_gpt3_1p3b_full_size_parity(tmp_path):
     os.remove(path)          # pytest keeps tmp dirs: do not leave 21 GB on the disk
 
 
-@pytest.mark.parametrize("cfg,k", [("gpt3_small", 4), ("moe_small", 2), ("c1_tiny", 3),
-                                   ("gpt3_odd", 1)])
-def test_load_parallel_device(tmp_path, cfg, k):
-    """P:503 two-step load on device: own shard -> H2D -> all-gather (ordered
-    on the library stream) -> unpack kernel scatter."""
+@pytest.mark.parametrize("exchange", ["peer", "nccl"])
+@pytest.mark.parametrize("cfg,k,slot", [("gpt3_small", 4, 1 << 20), ("moe_small", 2, 1 << 20),
+                                        ("c1_tiny", 3, 1 << 20), ("gpt3_odd", 1, 1 << 20),
+                                        ("gpt3_odd", 3, 64 << 10), ("c1_tiny", 8, 8 << 20)])
+def test_load_parallel_device(tmp_path, monkeypatch, cfg, k, slot, exchange):
+    """P:503 two-step load on device: own shard -> H2D -> exchange -> scatter.
+    peer: every rank's partition in its own device buffer, fp_unpack_peer
+    reads all writers' chunks from those buffers after their ready flags
+    (thread ranks share one address space: the same pointers, no IPC);
+    nccl: the comm's allgather_bytes per chunk + fp_unpack_v4."""
+    monkeypatch.setenv("FP_LOAD_EXCHANGE", exchange)
     states = [_state(cfg, r, k) for r in range(k)]
     comms = ThreadComm.group(k)
-    cks = [fp.Checkpointer(DEV, comm=comms[r], slot_bytes=1 << 20) for r in range(k)]
+    cks = [fp.Checkpointer(DEV, comm=comms[r], slot_bytes=slot) for r in range(k)]
     try:
         run_threads([lambda r=r: cks[r].save(entries(states[r]), str(tmp_path))
                      for r in range(k)])
         dst = [[(s, torch.full_like(t, 9) if t.is_floating_point() else torch.zeros_like(t))
                 for s, t in states[r]] for r in range(k)]
         streams = [torch.cuda.Stream(DEV) for _ in range(k)]
-        run_threads([lambda r=r: cks[r].load_parallel(entries(dst[r]), str(tmp_path),
-                                                      stream=streams[r]) for r in range(k)])
+        res = run_threads([lambda r=r: cks[r].load_parallel(entries(dst[r]), str(tmp_path),
+                                                            stream=streams[r]) for r in range(k)])
         torch.cuda.synchronize()
+        want = "none" if k == 1 else ("peer" if exchange == "peer" else "allgather_bytes")
+        assert [x["exchange"] for x in res] == [want] * k
+        assert all(x["status"] == 0 and x["kernel_launches"] > 0 for x in res)
         for r in range(k):
             for (_, a), (_, b) in zip(states[r], dst[r]):
                 assert torch.equal(a.reshape(-1).view(torch.uint8), b.reshape(-1).view(torch.uint8))
@@ -229,9 +238,11 @@ def test_load_parallel_device(tmp_path, cfg, k):
             c.close()
 
 
-def test_load_parallel_device_detects_payload_corruption(tmp_path):
+@pytest.mark.parametrize("exchange", ["peer", "nccl"])
+def test_load_parallel_device_detects_payload_corruption(tmp_path, monkeypatch, exchange):
     """The own-shard CRC-32 (GPU kernels over the H2D'd chunk) is checked
     against the manifest on load: a flipped payload byte fails every rank."""
+    monkeypatch.setenv("FP_LOAD_EXCHANGE", exchange)
     k = 2
     states = [_state("gpt3_small", r, k) for r in range(k)]
     comms = ThreadComm.group(k)
@@ -300,6 +311,41 @@ def test_load_read_ahead_ring_depths(tmp_path, slots, how):
         torch.cuda.synchronize()
     for (_, a), (_, b) in zip(st, dst):
         assert torch.equal(a.reshape(-1).view(torch.uint8), b.reshape(-1).view(torch.uint8))
+
+
+@pytest.mark.parametrize("cfg,k,stride", [("gpt3_odd", 4, 2), ("moe_small", 4, 4),
+                                          ("c1_tiny", 3, 2)])
+def test_writer_stride_device(tmp_path, cfg, k, stride):
+    """Writer subsets on device state ("use a subset of DP ranks"):
+    only ranks 0, s, 2s, ... pack and write replicated bytes; every shard ==
+    the oracle's, and both loads follow the writer's partition."""
+    states = [_state(cfg, r, k) for r in range(k)]
+    lay = oracle_layout(states, k)
+    comms = ThreadComm.group(k)
+    cks = [fp.Checkpointer(DEV, comm=comms[r], slot_bytes=1 << 20, writer_stride=stride)
+           for r in range(k)]
+    try:
+        res = run_threads([lambda r=r: cks[r].save(entries(states[r]), str(tmp_path))
+                           for r in range(k)])
+        ext = fpck.shard_extents(lay, stride)
+        for r in range(k):
+            p = os.path.join(str(tmp_path), fpck.shard_name(r, k))
+            assert file_sha(p) == fpck.shard_sha256(lay, r, stride), r
+            assert res[r]["shard_bytes"] == sum(n for _, _, n in ext[r])
+            if r % stride and not lay.regions:
+                assert res[r]["shard_bytes"] == 0
+        for how in ("load", "load_parallel"):
+            dst = [[(s, torch.full_like(t, 5) if t.is_floating_point() else torch.zeros_like(t))
+                    for s, t in states[r]] for r in range(k)]
+            run_threads([lambda r=r: getattr(cks[r], how)(entries(dst[r]), str(tmp_path))
+                         for r in range(k)])
+            torch.cuda.synchronize()
+            for r in range(k):
+                for (_, a), (_, b) in zip(states[r], dst[r]):
+                    assert torch.equal(a.reshape(-1).view(torch.uint8), b.reshape(-1).view(torch.uint8))
+    finally:
+        for c in cks:
+            c.close()
 
 
 _GDS_UNAVAILABLE = []   # reason, once the first GDS case found no cuFile driver
