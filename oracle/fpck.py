@@ -248,14 +248,18 @@ def partition_units(Q, k):
     return out
 
 
-def shard_extents(layout: Layout, writer_stride=1):
+def shard_extents(layout: Layout, writer_stride=1, balance="pages"):
     """Per rank: [(image_offset, file_offset, length)] in image order.
 
-    The replicated region is split page-granular (reading R5) over the
-    writers — every rank, or with writer_stride s only ranks 0, s, 2s, ...
-    (the paper's writer subsets, "use a subset of DP ranks", P:495-499);
-    rank r's local region LREG_r goes wholly to rank r (reading R9)."""
-    A = layout.align
+    The replicated region is split over the writers — every rank, or with
+    writer_stride s only ranks 0, s, 2s, ... (the paper's writer subsets, "use
+    a subset of DP ranks") — in `alignment` pages (reading R5,
+    the default), or with balance="bytes" in single bytes, the paper's own
+    granularity ("partitions data on byte granularity ... imbalance to at most
+    one byte"); rank r's local region LREG_r goes wholly to rank r
+    and follows its replicated bytes in its file (reading R9)."""
+    A = layout.align if balance == "pages" else 1
+    assert balance in ("pages", "bytes")
     Q = layout.rep_bytes // A
     s = max(1, writer_stride)
     writers = [r for r in range(layout.k) if r % s == 0]
@@ -279,12 +283,13 @@ def shard_name(r, k):
     return f"shard-{r}-of-{k}.fpck"
 
 
-def shard_bytes(layout, r, writer_stride=1):
-    return b"".join(layout.read(io, n) for io, _, n in shard_extents(layout, writer_stride)[r])
+def shard_bytes(layout, r, writer_stride=1, balance="pages"):
+    return b"".join(layout.read(io, n)
+                    for io, _, n in shard_extents(layout, writer_stride, balance)[r])
 
 
-def iter_shard(layout, r, piece=64 << 20, writer_stride=1):
-    for io, _, n in shard_extents(layout, writer_stride)[r]:
+def iter_shard(layout, r, piece=64 << 20, writer_stride=1, balance="pages"):
+    for io, _, n in shard_extents(layout, writer_stride, balance)[r]:
         p = 0
         while p < n:
             m = min(piece, n - p)
@@ -292,24 +297,24 @@ def iter_shard(layout, r, piece=64 << 20, writer_stride=1):
             p += m
 
 
-def shard_sha256(layout, r, writer_stride=1):
+def shard_sha256(layout, r, writer_stride=1, balance="pages"):
     h = hashlib.sha256()
-    for b in iter_shard(layout, r, writer_stride=writer_stride):
+    for b in iter_shard(layout, r, writer_stride=writer_stride, balance=balance):
         h.update(b)
     return h.hexdigest()
 
 
-def shard_crc32(layout, r, writer_stride=1):
+def shard_crc32(layout, r, writer_stride=1, balance="pages"):
     """CRC-32 (IEEE 802.3 / zlib) of shard r's bytes — the integrity record the
     manifest carries per shard (SPEC.md S:157 checksums in the
     manifest). zlib.crc32 is the library routine; no custom arithmetic."""
     c = 0
-    for b in iter_shard(layout, r, writer_stride=writer_stride):
+    for b in iter_shard(layout, r, writer_stride=writer_stride, balance=balance):
         c = zlib.crc32(b, c)
     return c
 
 
-def save(layout, dirpath, ranks=None):
+def save(layout, dirpath, ranks=None, balance="pages"):
     """Write shard files with buffered write() + fsync; return {rank: sha256}.
 
     This is the slow baseline writer (one core, page cache, then fsync)."""
@@ -318,7 +323,7 @@ def save(layout, dirpath, ranks=None):
     for r in (range(layout.k) if ranks is None else ranks):
         h = hashlib.sha256()
         with open(os.path.join(dirpath, shard_name(r, layout.k)), "wb") as f:
-            for b in iter_shard(layout, r):
+            for b in iter_shard(layout, r, balance=balance):
                 f.write(b)
                 h.update(b)
             f.flush()

@@ -388,3 +388,48 @@ def test_writer_subset_extents_brute_force(stride):
             for io, fo, n in ext[r]:
                 img[io:io + n] = data[fo:fo + n]
         assert bytes(img) == lay.image()
+
+
+@pytest.mark.parametrize("stride", [1, 2, 3])
+def test_byte_balance_extents_brute_force(stride):
+    """Byte-granular balance ("partitions data on byte granularity
+    ... tightly bound imbalance to at most one byte"): the writers' replicated
+    byte counts differ by at most ONE BYTE, tile the replicated region once in
+    rank order, and the shards (replicated bytes, then the local region)
+    reassemble into the image; with every writer's share a page multiple the
+    split equals the page-granular one."""
+    rng = random.Random(100 + stride)
+    nrng = np.random.default_rng(stride)
+    for k in list(range(1, 9)) * 3:
+        rep = [fpck.OTensor(f"r{i}", "u8", "other", -1, (n,), nrng.bytes(n))
+               for i, n in enumerate(rng.randint(0, 30000) for _ in range(rng.randint(0, 5)))]
+        local = [[] for _ in range(k)]
+        for j in range(rng.randint(0, 3)):
+            r, n = rng.randrange(k), rng.randint(0, 7000)
+            local[r].append(fpck.OTensor(f"l{j}", "u8", "other", r, (n,), nrng.bytes(n)))
+        lay = fpck.Layout(rep, local, k=k)
+        ext = fpck.shard_extents(lay, stride, balance="bytes")
+        writers = [r for r in range(k) if r % stride == 0]
+        sizes = []
+        pos = 0
+        for r in range(k):
+            rp = [(io, fo, n) for io, fo, n in ext[r] if io < lay.rep_bytes]
+            if r not in writers:
+                assert rp == []
+                continue
+            (io, fo, n), = rp
+            assert io == pos and fo == 0                 # contiguous, rank order
+            pos += n
+            sizes.append(n)
+        assert pos == lay.rep_bytes
+        assert max(sizes) - min(sizes) <= 1              # the paper's one-byte bound
+        assert sizes == sorted(sizes, reverse=True)      # extra bytes to the lowest writers
+        img = bytearray(lay.image_bytes)
+        for r in range(k):
+            data = fpck.shard_bytes(lay, r, stride, balance="bytes")
+            assert len(data) == sum(n for _, _, n in ext[r])
+            for io, fo, n in ext[r]:
+                img[io:io + n] = data[fo:fo + n]
+        assert bytes(img) == lay.image()
+        if (lay.rep_bytes // lay.align) % len(writers) == 0:   # page multiples: same split
+            assert ext == fpck.shard_extents(lay, stride)
