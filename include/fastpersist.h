@@ -124,6 +124,16 @@ enum fp_pack_impl { FP_PACK_V4 = 0,     /* LSU 16-B vector gather -> device slab
 #define FP_CFG_NO_CRC   4u     /* skip the per-shard CRC-32          */
 #define FP_CFG_PRIO_LOW 2u     /* pack/D2H stream at the least priority (default:
                                   greatest)                    */
+#define FP_CFG_BALANCE_BYTES 8u /* partition the replicated region on BYTE
+                                  granularity (imbalance <= 1 byte;
+                                  env FP_BALANCE_BYTES=1) instead of `alignment`
+                                  pages: shard starts are then unaligned in the
+                                  image (the pack gathers byte-shifted) and each
+                                  shard's unaligned suffix (< alignment bytes)
+                                  is written with buffered I/O into the same
+                                  file (P:477 prefix/suffix); the manifest
+                                  records it ("balance": "bytes") and loads
+                                  follow the manifest                            */
 
 typedef struct fp_config {
   uint32_t ring_slots;   /* pinned host slots; 2 = the paper's double buffer

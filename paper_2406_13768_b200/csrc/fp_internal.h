@@ -61,6 +61,9 @@ struct Piece {
 // Everything rank `rank` needs to write (or read) its shard.
 struct Plan {
   uint32_t align = 4096, writer_stride = 1;
+  // replicated-region partition unit: `align` (page-granular, reading R5) or
+  // 1 (byte-granular, FP_CFG_BALANCE_BYTES: the paper's <= 1 byte imbalance)
+  uint64_t unit = 4096;
   int rank = 0, k = 1;
   uint64_t header_bytes = 0, rep_bytes = 0, image_bytes = 0, digest = 0;
   std::vector<std::pair<uint64_t, uint64_t>> regions;  // (offset, bytes) per rank or empty
@@ -88,8 +91,10 @@ void rep_partition(uint64_t Q, int k, uint32_t writer_stride, int w, uint64_t* f
                    uint64_t* n_pages);
 // Layout pass 2: needs all ranks' facts (k entries). Returns 0 / FP_EMISMATCH.
 int plan_build(const std::vector<TensorRef>& rep, const std::vector<TensorRef>& loc,
-               uint32_t align, int rank, int k, uint32_t writer_stride,
+               uint32_t align, int rank, int k, uint32_t writer_stride, bool balance_bytes,
                const std::vector<LocalFacts>& all, Plan* out);
+// (image offset, bytes) of writer w's share of the replicated region
+void rep_share(const Plan& p, int w, uint64_t* off, uint64_t* bytes);
 // Rebase header pieces onto hdr_base (ghdr at +0, lhdr at +ghdr.size());
 // hdr_base == 0 turns header pieces into skip (zero) items, as load needs.
 void plan_pieces(Plan* p, const std::vector<TensorRef>& rep, const std::vector<TensorRef>& loc,

@@ -184,8 +184,15 @@ void rep_partition(uint64_t Q, int k, uint32_t writer_stride, int w, uint64_t* f
   *n_pages = q + (i < rem ? 1 : 0);
 }
 
+void rep_share(const Plan& p, int w, uint64_t* off, uint64_t* bytes) {
+  uint64_t f = 0, n = 0;
+  rep_partition(p.rep_bytes / p.unit, p.k, p.writer_stride, w, &f, &n);
+  *off = f * p.unit;
+  *bytes = n * p.unit;
+}
+
 int plan_build(const std::vector<TensorRef>& rep, const std::vector<TensorRef>& loc,
-               uint32_t align, int rank, int k, uint32_t writer_stride,
+               uint32_t align, int rank, int k, uint32_t writer_stride, bool balance_bytes,
                const std::vector<LocalFacts>& all, Plan* p) {
   for (int r = 1; r < k; ++r)
     if (all[r].digest != all[0].digest || all[r].rep_bytes != all[0].rep_bytes)
@@ -194,6 +201,7 @@ int plan_build(const std::vector<TensorRef>& rep, const std::vector<TensorRef>& 
   for (int r = 0; r < k; ++r) has_local |= all[r].n_local > 0;
   const uint64_t n_reg = has_local ? (uint64_t)k : 0;
   p->align = align;
+  p->unit = balance_bytes ? 1 : align;
   p->writer_stride = writer_stride > 1 ? writer_stride : 1;
   p->rank = rank;
   p->k = k;
@@ -226,15 +234,16 @@ int plan_build(const std::vector<TensorRef>& rep, const std::vector<TensorRef>& 
     if (c - start != p->regions[rank].second) return FP_EMISMATCH;
     encode_header(loc, p->loc_off, {}, align, c - start, rank, kFlagLocal, &p->lhdr);
   }
-  // partition of the replicated region: Q pages over the writers, contiguous
-  // in rank order, sizes differ by <= 1 page, lowest writers take the extras
-  uint64_t first = 0, npg = 0;
-  rep_partition(p->rep_bytes / align, k, p->writer_stride, rank, &first, &npg);
+  // partition of the replicated region: Q units (pages, or bytes) over the
+  // writers, contiguous in rank order, sizes differ by <= 1 unit, lowest
+  // writers take the extras
+  uint64_t first = 0, nb = 0;
+  rep_share(*p, rank, &first, &nb);
   p->extents.clear();
   uint64_t fo = 0;
-  if (npg) {
-    p->extents.push_back({first * align, 0, npg * align});
-    fo = npg * align;
+  if (nb) {
+    p->extents.push_back({first, 0, nb});
+    fo = nb;
   }
   if (has_local) {
     p->extents.push_back({p->regions[rank].first, fo, p->regions[rank].second});

@@ -124,15 +124,26 @@ struct JParser {
   }
 };
 
-// Loads plan with the writer subset recorded in the manifest (absent = 1).
-struct WriterStrideScope {
+// Loads plan with the writer's partition as the manifest records it: its
+// writer subset (absent = 1) and its balance unit ("bytes" or pages).
+struct PartitionScope {
   fp_ctx* c;
-  uint32_t saved;
-  WriterStrideScope(fp_ctx* ctx, unsigned long long ws) : c(ctx), saved(ctx->cfg.writer_stride) {
+  uint32_t saved_ws, saved_flags;
+  PartitionScope(fp_ctx* ctx, unsigned long long ws, bool bytes)
+      : c(ctx), saved_ws(ctx->cfg.writer_stride), saved_flags(ctx->cfg.flags) {
     c->cfg.writer_stride = (ws == ~0ull || ws == 0) ? 1u : (uint32_t)ws;
+    c->cfg.flags = bytes ? (c->cfg.flags | FP_CFG_BALANCE_BYTES)
+                         : (c->cfg.flags & ~FP_CFG_BALANCE_BYTES);
   }
-  ~WriterStrideScope() { c->cfg.writer_stride = saved; }
+  ~PartitionScope() {
+    c->cfg.writer_stride = saved_ws;
+    c->cfg.flags = saved_flags;
+  }
 };
+bool manifest_bytes_balance(const JVal& m) {
+  const JVal* b = m.get("balance");
+  return b && b->t == JVal::STR && b->str == "bytes";
+}
 
 // Read-ahead over the pinned ring (the load-side mirror of the save pipeline,
 // §4.1 P:473 double buffering): chunk j's reads land in ring slot j % R and up
@@ -445,7 +456,7 @@ int fp_ckpt_load(fp_ctx* c, const fp_tensor* t, size_t n, const char* path, int 
   if (num("dp_size") != (uint64_t)dp_size || num("alignment") != c->cfg.alignment)
     return FP_EMISMATCH;
   // the partition is the writer's (its writer subset), not this context's
-  WriterStrideScope wss(c, num("writer_stride"));
+  PartitionScope wss(c, num("writer_stride"), manifest_bytes_balance(m));
   r = ensure_plan(c, t, n, dp_rank, dp_size);
   if (r) return r;
   Plan& p = c->plan;
@@ -456,9 +467,11 @@ int fp_ckpt_load(fp_ctx* c, const fp_tensor* t, size_t n, const char* path, int 
   // open every shard we may read from (single box: all files visible; the
   // NCCL all-gather variant of P:503 reads only its own shard)
   const size_t nroots = c->roots.empty() ? 1 : c->roots.size();
-  std::vector<int> fds(dp_size, -1);
+  std::vector<int> fds(dp_size, -1), bfds(dp_size, -1);
   auto close_all = [&] {
     for (int fd : fds)
+      if (fd >= 0) close(fd);
+    for (int fd : bfds)
       if (fd >= 0) close(fd);
   };
   for (int w = 0; w < dp_size; ++w) {
@@ -484,6 +497,14 @@ int fp_ckpt_load(fp_ctx* c, const fp_tensor* t, size_t n, const char* path, int 
       return FP_ECORRUPT;
     }
     fds[w] = fd;
+    // requests that are not block-aligned (byte-granular partitions: shard
+    // suffixes and unaligned local-region starts) take a buffered descriptor
+    bfds[w] = open(f.c_str(), O_RDONLY);
+    if (bfds[w] < 0) {
+      r = -errno;
+      close_all();
+      return r;
+    }
   }
   // image offset -> (shard, file offset) for the bytes this rank needs
   const uint32_t A = p.align;
@@ -623,8 +644,11 @@ int fp_ckpt_load(fp_ctx* c, const fp_tensor* t, size_t n, const char* path, int 
       int e = chunk_runs(ch, &rr);
       if (e) return e;
       for (const Run& u : rr)
-        for (uint64_t o = 0; o < u.n; o += SQ)
-          out->push_back({fds[u.w], u.fo + o, u.pos + o, (uint32_t)std::min<uint64_t>(SQ, u.n - o)});
+        for (uint64_t o = 0; o < u.n; o += SQ) {
+          const uint32_t len = (uint32_t)std::min<uint64_t>(SQ, u.n - o);
+          const bool aligned = (u.fo + o) % A == 0 && len % A == 0 && (u.pos + o) % A == 0;
+          out->push_back({aligned ? fds[u.w] : bfds[u.w], u.fo + o, u.pos + o, len});
+        }
       return 0;
     });
     std::vector<Run> cr;
@@ -744,15 +768,16 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
     r = FP_EMISMATCH;
   r = status_min(c, k, r);
   if (r) return r;
-  WriterStrideScope wss(c, num("writer_stride"));  // the writer's partition
+  PartitionScope wss(c, num("writer_stride"), manifest_bytes_balance(m));  // the writer's partition
   r = ensure_plan(c, t, n, rank, k);  // all-gather of sizes when the signature is new
   if (r) return r;
   const Plan& p = c->plan;
   if (num("image_bytes") != p.image_bytes || num("layout_digest") != p.digest) r = FP_EMISMATCH;
   // 2) this rank's own shard, nothing else
   const std::string sf = join_path(c->shard_dir, shard_file(rank, k));
-  int fd = -1;
+  int fd = -1, bfd = -1;  // bfd: buffered, for requests that are not block-aligned
   if (!r) {
+    bfd = open(sf.c_str(), O_RDONLY);
     fd = open(sf.c_str(), O_RDONLY | O_DIRECT);
     if (fd < 0 && errno == EINVAL) fd = open(sf.c_str(), O_RDONLY);
     if (fd < 0) {
@@ -772,19 +797,19 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
   r = status_min(c, k, r);
   if (r) {
     if (fd >= 0) close(fd);
+    if (bfd >= 0) close(bfd);
     return r;
   }
   // 3) geometry: replicated partitions (the writer's page-balanced split)
-  const uint64_t A = p.align, Q = p.rep_bytes / A;
   auto part_off = [&](int w) {  // image offset of writer w's partition
     uint64_t f, n;
-    rep_partition(Q, k, p.writer_stride, w, &f, &n);
-    return f * A;
+    rep_share(p, w, &f, &n);
+    return f;
   };
   auto part_bytes = [&](int w) {
     uint64_t f, n;
-    rep_partition(Q, k, p.writer_stride, w, &f, &n);
-    return n * A;
+    rep_share(p, w, &f, &n);
+    return n;
   };
   const uint64_t CH = c->cfg.slot_bytes, M = part_bytes(0);  // writer 0 has the largest part
   const uint64_t nrep = (M + CH - 1) / CH;
@@ -989,9 +1014,12 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
                [&](uint64_t j, std::vector<ReadReq>* out) -> int {
     uint64_t foff = 0;
     const uint64_t len = my_span(j, &foff);
-    for (uint64_t pos = 0; pos < len; pos += c->cfg.sqe_bytes)
-      out->push_back({fd, foff + pos, pos,
-                      (uint32_t)std::min<uint64_t>(c->cfg.sqe_bytes, len - pos)});
+    const uint64_t al = p.align;
+    for (uint64_t pos = 0; pos < len; pos += c->cfg.sqe_bytes) {
+      const uint32_t n1 = (uint32_t)std::min<uint64_t>(c->cfg.sqe_bytes, len - pos);
+      const bool aligned = (foff + pos) % al == 0 && n1 % al == 0;
+      out->push_back({aligned ? fd : bfd, foff + pos, pos, n1});
+    }
     return 0;
   });
   const uint64_t spin_ns = env_u64("FP_PEER_TIMEOUT_S", 600) * 1000000000ull;
@@ -1171,6 +1199,7 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
     free(recv);
   }
   close(fd);
+  if (bfd >= 0) close(bfd);
   return status;
 }
 

@@ -154,6 +154,26 @@ int fp_ctx::save_shard() {
     const int status = save_shard_gds(fd);
     return finish_shard(fd, status, t0);
   }
+  // the shard's unaligned suffix (byte-granular balance: < A bytes at the
+  // end) goes through a buffered descriptor of the same file, the aligned
+  // prefix through the O_DIRECT engine ("writes the checkpoint prefix
+  // using NVMe-optimized libraries, and the suffix using traditional I/O
+  // libraries, into the same checkpoint file")
+  int bfd = -1;
+  if (plan.shard_bytes % A && cfg.io_engine != FP_IO_NULL) {
+    bfd = open(file.c_str(), O_WRONLY);
+    if (bfd < 0) {
+      err = -errno;
+      close(fd);
+      return err;
+    }
+  }
+  struct BfdCloser {
+    int fd;
+    ~BfdCloser() {
+      if (fd >= 0) close(fd);
+    }
+  } bfd_closer{bfd};
   const uint64_t C = item_lo.size() - 1;
   std::vector<uint32_t> slot_out(R, 0);
   uint64_t next_gpu = 0, next_io = 0;
@@ -317,12 +337,27 @@ int fp_ctx::save_shard() {
         xcrc.add_bytes(fo, slot, len);
     }
     for (uint64_t off = 0; off < len; off += SQ) {
-      const uint32_t n = (uint32_t)std::min<uint64_t>(SQ, len - off);
+      uint32_t n = (uint32_t)std::min<uint64_t>(SQ, len - off);
+      const uint64_t fo = c * S + off;
+      if (n % A) {  // the shard's unaligned suffix: buffered, synchronous
+        const uint32_t tail = n % A;
+        const uint8_t* p = slot + off + (n - tail);
+        for (uint32_t done = 0; done < tail;) {
+          const ssize_t w = pwrite(bfd, p + done, tail - done, (off_t)(fo + n - tail + done));
+          if (w < 0 && errno == EINTR) continue;
+          if (w <= 0) {
+            st.err_offset = (int64_t)(fo + n - tail + done);
+            return w < 0 ? -errno : -EIO;
+          }
+          done += (uint32_t)w;
+        }
+        n -= tail;
+        if (!n) continue;
+      }
       while (inflight >= io->capacity()) {
         int r = reap(1);
         if (r) return r;
       }
-      const uint64_t fo = c * S + off;
       const uint64_t user = ((uint64_t)s << 56) | ((uint64_t)(n / 512) << 32) | (fo / 512);
       int r = io->queue(true, fd, slot + off, n, fo, (int)s, user);
       if (r == -EAGAIN) {
@@ -423,10 +458,12 @@ int fp_ctx::write_manifest() {
   char buf[512];
   snprintf(buf, sizeof(buf),
            "  \"alignment\": %u,\n  \"image_bytes\": %llu,\n  \"header_bytes\": %llu,\n"
-           "  \"dp_size\": %d,\n  \"writer_stride\": %u,\n  \"layout_digest\": %llu,\n  \"n_roots\": %zu,\n"
+           "  \"dp_size\": %d,\n  \"writer_stride\": %u,\n  \"balance\": \"%s\",\n"
+           "  \"layout_digest\": %llu,\n  \"n_roots\": %zu,\n"
            "  \"shards\": [\n",
            plan.align, (unsigned long long)plan.image_bytes,
            (unsigned long long)plan.header_bytes, k, plan.writer_stride,
+           plan.unit == 1 ? "bytes" : "pages",
            (unsigned long long)plan.digest,
            roots.empty() ? (size_t)1 : roots.size());
   j += buf;
@@ -525,7 +562,9 @@ int fp::ensure_plan(fp_ctx* c, const fp_tensor* t, size_t n, int rank, int k) {
     if (any) r = FP_ENODEV;
   }
   const uint32_t A = c->cfg.alignment;
-  const uint64_t sm = r ? 0 : sig_hash(rep, loc, rank, k, A, c->cfg.writer_stride, false);
+  const uint32_t bal = (c->cfg.flags & FP_CFG_BALANCE_BYTES) ? 1 : 0;
+  const uint64_t sm =
+      r ? 0 : sig_hash(rep, loc, rank, k, A, c->cfg.writer_stride, false) ^ (bal * 0x5bd1e995ull);
   const uint64_t sp = r ? 0 : sig_hash(rep, loc, rank, k, A, c->cfg.writer_stride, true) ^ (host ? 1 : 0);
   bool new_meta = !c->planned || sm != c->sig_meta;
   if (k > 1) {
@@ -558,7 +597,8 @@ int fp::ensure_plan(fp_ctx* c, const fp_tensor* t, size_t n, int rank, int k) {
       all[0] = mine;
     }
     Plan p;
-    r = plan_build(rep, loc, A, rank, k, c->cfg.writer_stride, all, &p);
+    r = plan_build(rep, loc, A, rank, k, c->cfg.writer_stride,
+                   (c->cfg.flags & FP_CFG_BALANCE_BYTES) != 0, all, &p);
     if (r) {
       c->planned = false;
       return r;
@@ -567,12 +607,12 @@ int fp::ensure_plan(fp_ctx* c, const fp_tensor* t, size_t n, int rank, int k) {
     c->all_extents.assign(k, {});
     {
       for (int w = 0; w < k; ++w) {
-        uint64_t first = 0, npg = 0;
-        rep_partition(p.rep_bytes / A, k, p.writer_stride, w, &first, &npg);
+        uint64_t first = 0, nb = 0;
+        rep_share(p, w, &first, &nb);
         uint64_t fo = 0;
-        if (npg) {
-          c->all_extents[w].push_back({first * A, 0, npg * A});
-          fo = npg * A;
+        if (nb) {
+          c->all_extents[w].push_back({first, 0, nb});
+          fo = nb;
         }
         if (!p.regions.empty()) c->all_extents[w].push_back({p.regions[w].first, fo,
                                                                p.regions[w].second});
@@ -680,6 +720,7 @@ int fp_config_default(fp_config* cfg) {
   cfg->pack_bytes = env_u64("FP_PACK_BYTES", 256ull << 20);
   cfg->writer_stride = (uint32_t)env_u64("FP_WRITER_STRIDE", 1);
   if (getenv("FP_NO_CRC")) cfg->flags |= FP_CFG_NO_CRC;
+  if (env_u64("FP_BALANCE_BYTES", 0)) cfg->flags |= FP_CFG_BALANCE_BYTES;
   const char* pr = getenv("FP_PACK_PRIO");
   if (pr && !strcmp(pr, "low")) cfg->flags |= FP_CFG_PRIO_LOW;
   const char* e = getenv("FP_IO_ENGINE");

@@ -31,6 +31,7 @@ FP_TENSOR_HOST = 1
 FP_CFG_NO_FSYNC = 1
 FP_CFG_PRIO_LOW = 2
 FP_CFG_NO_CRC = 4
+FP_CFG_BALANCE_BYTES = 8
 IO_ENGINES = {"uring": 0, "pwrite": 1, "buffered": 2, "null": 3, "gds": 4}
 PACK_IMPLS = {"v4": 0, "bulk": 1, "host": 2, "ce": 3}
 SECTIONS = {"param": 0, "grad": 1, "master": 2, "exp_avg": 3, "exp_avg_sq": 4, "other": 5}
@@ -191,6 +192,9 @@ def make_config(**kw) -> fp_config:
             k, v = "flags", cfg.flags | (FP_CFG_NO_FSYNC if v else 0)
         elif k == "no_crc":
             k, v = "flags", cfg.flags | (FP_CFG_NO_CRC if v else 0)
+        elif k == "balance":
+            k, v = "flags", (cfg.flags & ~FP_CFG_BALANCE_BYTES) | \
+                (FP_CFG_BALANCE_BYTES if v == "bytes" else 0)
         elif k == "prio":
             k, v = "flags", (cfg.flags & ~FP_CFG_PRIO_LOW) | (FP_CFG_PRIO_LOW if v == "low" else 0)
         elif k == "dirs":

@@ -570,3 +570,45 @@ def test_import_error_on_one_rank_fails_every_rank_without_hanging(tmp_path):
         for c in cks:
             c.close()
     assert codes == [-22, -22]
+
+
+@pytest.mark.parametrize("cfg,k,stride", [("gpt3_odd", 3, 1), ("moe_small", 4, 1), ("c1_tiny", 7, 1),
+                                          ("gpt3_small", 6, 2), ("zero_small", 2, 1)])
+@pytest.mark.parametrize("engine", ["uring", "buffered"])
+def test_byte_balance_matches_oracle_and_loads(tmp_path, cfg, k, stride, engine):
+    """FP_CFG_BALANCE_BYTES (byte-granular partition, imbalance <= 1
+    byte): shard starts are unaligned in the image and each shard's suffix
+    (< 4096 B) is written with buffered I/O into the same file; the
+    shards are the oracle's (balance="bytes"), the manifest records the mode,
+    and both loads follow it."""
+    states = [_state(cfg, r, k) for r in range(k)]
+    lay = oracle_layout(states, k)
+    comms = ThreadComm.group(k)
+    cks = [fp.Checkpointer(None, comm=comms[r], slot_bytes=1 << 20, balance="bytes",
+                           writer_stride=stride, io_engine=engine, sqe_bytes=256 << 10)
+           for r in range(k)]
+    try:
+        res = run_threads([lambda r=r: cks[r].save(entries(states[r]), str(tmp_path))
+                           for r in range(k)])
+        ext = fpck.shard_extents(lay, stride, balance="bytes")
+        man = json.load(open(tmp_path / "manifest.json"))
+        assert man["balance"] == "bytes"
+        sizes = [sum(n for io, _, n in ext[r] if io < lay.rep_bytes) for r in range(0, k, stride)]
+        assert max(sizes) - min(sizes) <= 1
+        for r in range(k):
+            assert cks[r].plan_info()["extents"] == [tuple(e) for e in ext[r]]
+            assert file_sha(tmp_path / fpck.shard_name(r, k)) == \
+                fpck.shard_sha256(lay, r, stride, balance="bytes"), r
+            assert man["shards"][r]["crc32"] == res[r]["shard_crc32"] == \
+                fpck.shard_crc32(lay, r, stride, balance="bytes")
+        for how in ("load", "load_parallel"):
+            dst = [[(s, torch.zeros_like(t)) for s, t in states[r]] for r in range(k)]
+            run_threads([lambda r=r: getattr(cks[r], how)(entries(dst[r]), str(tmp_path))
+                         for r in range(k)])
+            for r in range(k):
+                for (s, a), (_, b) in zip(states[r], dst[r]):
+                    assert torch.equal(a.reshape(-1).view(torch.uint8),
+                                       b.reshape(-1).view(torch.uint8)), (how, r, s.name)
+    finally:
+        for c in cks:
+            c.close()
