@@ -106,7 +106,7 @@ std::vector<uint32_t> crc_device_tables() {
   init_tab();
   std::vector<uint32_t> t(kTabWords, 0);
   for (int k = 0; k < 4; ++k) memcpy(&t[kTabS4 + 256 * k], tab[k], 256 * 4);
-  for (uint32_t v = 0; v < kLaneLevels; ++v) mul_tables(gf_x8n(32ull << v), &t[kTabLane + 1024 * v]);
+  for (uint32_t l = 0; l < 32; ++l) t[kTabLaneK + l] = gf_x8n(128ull * (31 - l));
   return t;
 }
 

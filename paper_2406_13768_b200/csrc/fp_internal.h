@@ -190,9 +190,8 @@ int pack_crc_launch(const Item* d_items, const uint32_t* d_tile_lo, uint32_t n_t
                     uint32_t* d_page_crc, int ctas, void* stream);
 // device CRC table blob layout (uint32 offsets)
 constexpr uint32_t kTabS4 = 0;
-constexpr uint32_t kTabLane = 4 * 256;
-constexpr uint32_t kLaneLevels = 7;  // products by x^(8*32*2^v), v = 0..6
-constexpr uint32_t kTabWords = kTabLane + kLaneLevels * 1024;
+constexpr uint32_t kTabLaneK = 4 * 256;  // 32 lane-combine constants x^(8*128*(31-l))
+constexpr uint32_t kTabWords = kTabLaneK + 32;
 
 // ---------------------------------------------------------------------------
 // CRC-32 helpers (crc32.cpp)

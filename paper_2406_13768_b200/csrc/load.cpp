@@ -859,7 +859,12 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
       pbuf = nullptr;
       ok = 0;
     }
-    if (ok && cudaMemset(pbuf, 0, flag_bytes) != cudaSuccess) ok = 0;
+    // zero the ready flags, ordered before this rank's flag copies (same
+    // stream) and complete before any peer can look at them (the sync below
+    // precedes the handle exchange)
+    if (ok && (cudaMemsetAsync(pbuf, 0, flag_bytes, c->stream) != cudaSuccess ||
+               cudaStreamSynchronize(c->stream) != cudaSuccess))
+      ok = 0;
     const bool ipc_ok = ok && cudaIpcGetMemHandle(&h, pbuf) == cudaSuccess;
     if (!ipc_ok) cudaGetLastError();
     std::vector<uint64_t> mine(12, 0), all(12 * (size_t)k, 0);
@@ -945,6 +950,9 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
   const bool use_gds = dev && c->gds;
   void* gfh = nullptr;
   if (use_gds && !status && fd >= 0) status = gds_handle_open(fd, &gfh);
+  uint32_t* h_allpc = nullptr;
+  uint32_t* d_allpc = nullptr;
+  const uint64_t shard_pages = (part_bytes(rank) + lreg_len) / 4096 + 1;
   cudaStream_t cs = c->stream;     // peer mode: H2D copies + ready flags (copy engine only)
   cudaStream_t crcs = nullptr;     // peer mode: page CRCs (never waited on before the end)
   cudaEvent_t ev_h2d = nullptr;
@@ -961,6 +969,16 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
         (cudaStreamCreateWithFlags(&crcs, cudaStreamNonBlocking) != cudaSuccess ||
          cudaEventCreateWithFlags(&ev_h2d, cudaEventDisableTiming) != cudaSuccess))
       status = FP_ECUDA;
+    // peer mode keeps every page CRC of the own shard (4 B per 4 KiB) until
+    // the end: no host wait on a CRC kernel while unpacks spin on peers'
+    // flags. Allocated here, before the status all-reduce that releases the
+    // ranks into the exchange loop: an allocation call may wait for the
+    // device, and once any rank spins on flags this rank must not block on
+    // anything but its own copies.
+    if (peer && !status && !(c->cfg.flags & FP_CFG_NO_CRC) &&
+        (cudaHostAlloc(&h_allpc, shard_pages * 4, cudaHostAllocPortable) != cudaSuccess ||
+         cudaMalloc(&d_allpc, shard_pages * 4) != cudaSuccess))
+      status = -ENOMEM;
   } else if (!dev) {
     send = (uint8_t*)aligned_alloc(4096, round_up(CH, 4096));
     recv = (uint8_t*)aligned_alloc(4096, round_up(CH * k, 4096));
@@ -992,15 +1010,6 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
     const uint64_t n = my_span(j, &fo);
     acc.add_pages(fo, pages, n / 4096);
   });
-  // peer mode keeps every page CRC of the own shard (4 B per 4 KiB) until
-  // the end: no host wait on a CRC kernel while unpacks spin on peers' flags
-  uint32_t* h_allpc = nullptr;
-  uint32_t* d_allpc = nullptr;
-  const uint64_t shard_pages = (part_bytes(rank) + lreg_len) / 4096 + 1;
-  if (peer && run && check_crc &&
-      (cudaHostAlloc(&h_allpc, shard_pages * 4, cudaHostAllocPortable) != cudaSuccess ||
-       cudaMalloc(&d_allpc, shard_pages * 4) != cudaSuccess))
-    status = -ENOMEM;
   // peer mode, replicated chunks: (file offset, bytes, raw CRC or ~0 = pages
   // in d_allpc), folded in file order at the end
   struct Deferred {

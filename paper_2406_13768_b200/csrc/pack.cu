@@ -61,6 +61,44 @@ __device__ __forceinline__ uint4 ld_coherent(const uint4* p) {
   return r;
 }
 
+// Mutually misaligned src / dst (src - dst not a multiple of 16: odd storage
+// offsets, byte-granular shard starts): 16-B aligned stores; each destination
+// vector is funnel-shifted out of the two aligned source vectors that cover
+// it (both loads are aligned 16-B loads inside the 16-B blocks that hold the
+// needed bytes, so they never leave the source allocation's granule).
+template <bool kCoherent>
+__device__ __forceinline__ void copy_shifted(uint8_t* __restrict__ dst,
+                                             const uint8_t* __restrict__ src, uint32_t len, int t,
+                                             int nthr) {
+  uint32_t head = (16 - (uint32_t)((uintptr_t)dst & 15)) & 15;
+  if (head > len) head = len;
+  if ((uint32_t)t < head) dst[t] = src[t];
+  const uint32_t n16 = (len - head) >> 4;
+  if (n16) {
+    const uint8_t* s = src + head;
+    const uint32_t sh = (uint32_t)((uintptr_t)s & 15);  // != 0 here
+    const uint4* a16 = reinterpret_cast<const uint4*>(s - sh);
+    uint4* d16 = reinterpret_cast<uint4*>(dst + head);
+    const uint32_t q = sh >> 2, r8 = (sh & 3) * 8;
+    for (uint32_t j = t; j < n16; j += nthr) {
+      const uint4 x = kCoherent ? ld_coherent(a16 + j) : ld_stream(a16 + j);
+      const uint4 y = kCoherent ? ld_coherent(a16 + j + 1) : ld_stream(a16 + j + 1);
+      const uint32_t w[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+      uint32_t o[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        // words q+i and q+i+1 of the 32-byte window (q uniform per item)
+        const uint32_t lo = q == 0 ? w[i] : q == 1 ? w[i + 1] : q == 2 ? w[i + 2] : w[i + 3];
+        const uint32_t hi = q == 0 ? w[i + 1] : q == 1 ? w[i + 2] : q == 2 ? w[i + 3] : w[i + 4];
+        o[i] = __funnelshift_r(lo, hi, r8);
+      }
+      st_v4(d16 + j, make_uint4(o[0], o[1], o[2], o[3]));
+    }
+  }
+  const uint32_t done = head + (n16 << 4);
+  for (uint32_t i = done + t; i < len; i += nthr) dst[i] = src[i];
+}
+
 // Copy `len` bytes src -> dst with `nthr` threads (index t). src == nullptr
 // means zero fill. Vector body when src and dst share the same 16-B phase.
 // kCoherent: plain (coherent) loads instead of the read-only .nc path.
@@ -71,7 +109,7 @@ __device__ __forceinline__ void copy_bytes(uint8_t* __restrict__ dst,
   const uint32_t phase = (uint32_t)((uintptr_t)dst & 15);
   const bool coaligned = !src || (((uintptr_t)src & 15) == phase);
   if (!coaligned) {
-    for (uint32_t i = t; i < len; i += nthr) dst[i] = src[i];
+    copy_shifted<kCoherent>(dst, src, len, t, nthr);
     return;
   }
   uint32_t head = (16 - phase) & 15;
@@ -307,61 +345,60 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
 //
 // Device table blob (uint32, built by crc_device_tables on the host):
 //   [kTabS4 .. +1024)   slicing-by-4 tables t[k][b] (b followed by k bytes)
-//   [kTabLane + 1024 v) product by x^(8*32*2^v),   v = 0..6
+//   [kTabLaneK + l)     x^(8*128*(31-l)), the lane-combine constant of lane l
 // each product table is four 256-entry tables: M[i][b] = K * (b << 8i).
 // ---------------------------------------------------------------------------
 constexpr int kCrcThreads = 1024;
-constexpr size_t kCrcTabWords = 4 * 256 * 32 + kLaneLevels * 1024;  // per-lane + level tables
-constexpr size_t kCrcPagesSmem = kCrcTabWords * sizeof(uint32_t);      // 156 KiB
+constexpr size_t kCrcTabWords = 4 * 256 * 32;                      // per-lane slicing tables
+constexpr size_t kCrcPagesSmem = kCrcTabWords * sizeof(uint32_t);  // 128 KiB
+constexpr uint32_t kPolyRefl = 0xEDB88320u;
 
-__device__ __forceinline__ uint32_t mul_tab(const uint32_t* __restrict__ m, uint32_t a) {
-  return m[a & 255] ^ m[256 + ((a >> 8) & 255)] ^ m[512 + ((a >> 16) & 255)] ^ m[768 + (a >> 24)];
+// Lane combine without shared memory: lane l's raw CRC R_l of its 128 bytes
+// enters the page CRC as R_l * x^(8*128*(31-l)) (the bytes after it), and
+// the lanes' terms are XOR-reduced. The product by the lane's constant K_l is
+// done in registers: kv[i] = K_l * x^i (reflected, bit 31 = x^0), so
+// R * K_l = XOR of kv[i] over the bits i of R (bit 31-i) — 32 predicated
+// XORs, no table lookups (the round-1 shuffle tree did 5 levels of 4
+// bank-conflicting lookups into shared constant-product tables: ~30 % of the
+// kernel's shared-memory wavefronts).
+__device__ __forceinline__ void lane_k_init(uint32_t K, uint32_t (&kv)[32]) {
+  kv[0] = K;
+#pragma unroll
+  for (int i = 1; i < 32; ++i) kv[i] = (kv[i - 1] >> 1) ^ ((kv[i - 1] & 1) ? kPolyRefl : 0u);
+}
+__device__ __forceinline__ uint32_t gf_mul_k(uint32_t a, const uint32_t (&kv)[32]) {
+  uint32_t p = 0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) p ^= (0u - ((a >> (31 - i)) & 1u)) & kv[i];
+  return p;
+}
+__device__ __forceinline__ uint32_t lanes_combine(uint32_t c, const uint32_t (&kv)[32]) {
+  c = gf_mul_k(c, kv);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) c ^= __shfl_xor_sync(0xffffffffu, c, o);
+  return c;  // valid in every lane
 }
 
 // Raw CRC of one 4 KiB page held by a warp, lane l owning bytes
-// [128 l, 128 l + 128) as v[0..7]; the result is valid in lane 0. Each lane
-// runs four independent 32-B slicing-by-4 chains (ILP: the chains' table
-// lookups overlap instead of waiting on each other), combines them with the
-// products by x^(8*32) and x^(8*64), then the lanes are combined in a
-// 5-level shuffle tree (x^(8*128*2^v)). rep = per-lane copies of the 4
-// slicing tables (entry e of table k at (k*256 + e)*32 + lane), lvl = the
-// kLaneLevels constant-product tables.
-template <int kChains>
+// [128 l, 128 l + 128) as v[0..7]: one slicing-by-4 chain of 32 words per
+// lane through per-lane (bank-private) copies of the 4 tables (entry e of
+// table k at (k*256 + e)*32 + lane), then lanes_combine.
 __device__ __forceinline__ uint32_t page_crc_warp(const uint4 (&v)[8], const uint32_t* rep,
-                                                  const uint32_t* lvl, int lane) {
-  static_assert(kChains == 1 || kChains == 4, "1 chain of 128 B or 4 chains of 32 B");
+                                                  const uint32_t (&kv)[32], int lane) {
   const uint32_t* r0 = rep + lane;
   const uint32_t* r1 = rep + 256 * 32 + lane;
   const uint32_t* r2 = rep + 2 * 256 * 32 + lane;
   const uint32_t* r3 = rep + 3 * 256 * 32 + lane;
-  constexpr int kWords = 32 / kChains;  // words per chain
-  uint32_t c[kChains];
+  uint32_t c = 0;
 #pragma unroll
-  for (int j = 0; j < kChains; ++j) c[j] = 0;
-#pragma unroll
-  for (int q = 0; q < kWords; ++q) {
-#pragma unroll
-    for (int j = 0; j < kChains; ++j) {
-      const int wi = j * kWords + q;  // word index in the lane's 128 B
-      const uint4& vv = v[wi >> 2];
-      const uint32_t w = (wi & 3) == 0 ? vv.x : (wi & 3) == 1 ? vv.y : (wi & 3) == 2 ? vv.z : vv.w;
-      const uint32_t x = c[j] ^ w;
-      c[j] = r3[(x & 255) << 5] ^ r2[((x >> 8) & 255) << 5] ^ r1[((x >> 16) & 255) << 5] ^
-             r0[(x >> 24) << 5];
-    }
+  for (int q = 0; q < 32; ++q) {
+    const uint4& vv = v[q >> 2];
+    const uint32_t w = (q & 3) == 0 ? vv.x : (q & 3) == 1 ? vv.y : (q & 3) == 2 ? vv.z : vv.w;
+    const uint32_t x = c ^ w;
+    c = r3[(x & 255) << 5] ^ r2[((x >> 8) & 255) << 5] ^ r1[((x >> 16) & 255) << 5] ^
+        r0[(x >> 24) << 5];
   }
-  uint32_t cl = c[0];
-  if (kChains == 4) {
-    const uint32_t ab = mul_tab(lvl, c[0]) ^ c[1];
-    const uint32_t cd = mul_tab(lvl, c[kChains > 2 ? 2 : 0]) ^ c[kChains > 3 ? 3 : 0];
-    cl = mul_tab(lvl + 1024, ab) ^ cd;
-  }
-#pragma unroll
-  for (int v2 = 0; v2 < 5; ++v2) {
-    const uint32_t o = __shfl_down_sync(0xffffffffu, cl, 1 << v2);
-    if ((lane & ((2 << v2) - 1)) == 0) cl = mul_tab(lvl + 1024 * (2 + v2), cl) ^ o;
-  }
-  return cl;
+  return lanes_combine(c, kv);
 }
 
 __global__ void __launch_bounds__(kCrcThreads, 1)
@@ -369,18 +406,18 @@ __global__ void __launch_bounds__(kCrcThreads, 1)
                  const uint32_t* __restrict__ tabs, uint32_t* __restrict__ out) {
   extern __shared__ __align__(16) uint32_t crc_smem[];
   uint32_t* rep = crc_smem;                    // [4][256][32] per-lane copies
-  uint32_t* lvl = crc_smem + 4 * 256 * 32;     // [kLaneLevels][4][256]
   for (int i = threadIdx.x; i < 4 * 256 * 32; i += blockDim.x) rep[i] = tabs[kTabS4 + (i >> 5)];
-  for (int i = threadIdx.x; i < (int)kLaneLevels * 1024; i += blockDim.x) lvl[i] = tabs[kTabLane + i];
   __syncthreads();
   const int lane = threadIdx.x & 31;
+  uint32_t kv[32];
+  lane_k_init(tabs[kTabLaneK + lane], kv);
   const uint32_t wpb = blockDim.x >> 5;
   for (uint32_t pg = blockIdx.x * wpb + (threadIdx.x >> 5); pg < n_pages; pg += gridDim.x * wpb) {
     const uint4* src = reinterpret_cast<const uint4*>(buf + (size_t)pg * 4096 + lane * 128);
     uint4 v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) v[u] = __ldg(src + u);
-    const uint32_t c = page_crc_warp<1>(v, rep, lvl, lane);
+    const uint32_t c = page_crc_warp(v, rep, kv, lane);
     if (lane == 0) out[pg] = c;
   }
 }
@@ -400,29 +437,28 @@ __global__ void __launch_bounds__(kCrcThreads, 1)
 // immediate of the load.
 constexpr int kCtWarps = 16;
 constexpr size_t kCtTabBytes = 4 * 256 * 32 * 4;  // paired per-lane tables
-constexpr size_t kCtSmem = kCtTabBytes + kLaneLevels * 1024 * 4 + 256 + 1024 +
-                           (size_t)kCtWarps * 4096;
+constexpr size_t kCtSmem = kCtTabBytes + 256 + 1024 + (size_t)kCtWarps * 4096;
 
 __global__ void __launch_bounds__(kCtWarps * 32, 1)
     fp_crc_pages_tma(const __grid_constant__ CUtensorMap tmap, uint32_t n_pages,
                      const uint32_t* __restrict__ tabs, uint32_t* __restrict__ out) {
   extern __shared__ __align__(16) uint8_t ct_raw[];
-  uint32_t* lvl = reinterpret_cast<uint32_t*>(ct_raw + kCtTabBytes);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(ct_raw + kCtTabBytes + kLaneLevels * 1024 * 4);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(ct_raw + kCtTabBytes);
   uint8_t* stages = reinterpret_cast<uint8_t*>(
-      ((uintptr_t)(ct_raw + kCtTabBytes + kLaneLevels * 1024 * 4 + 256) + 1023) & ~(uintptr_t)1023);
+      ((uintptr_t)(ct_raw + kCtTabBytes + 256) + 1023) & ~(uintptr_t)1023);
   for (int i = threadIdx.x; i < 4 * 256 * 32; i += blockDim.x) {
     const int k = i >> 13, e = (i >> 5) & 255, l = i & 31;
     *reinterpret_cast<uint32_t*>(ct_raw + (k >> 1) * 65536 + e * 256 + (k & 1) * 128 + l * 4) =
         tabs[kTabS4 + k * 256 + e];
   }
-  for (int i = threadIdx.x; i < (int)kLaneLevels * 1024; i += blockDim.x) lvl[i] = tabs[kTabLane + i];
   if (threadIdx.x < kCtWarps)
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[threadIdx.x])));
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t lane4 = (uint32_t)lane * 4;
+  uint32_t kv[32];
+  lane_k_init(tabs[kTabLaneK + lane], kv);
   const uint32_t gw = blockIdx.x * kCtWarps + (uint32_t)w, nw = gridDim.x * kCtWarps;
   uint8_t* stage = stages + (size_t)w * 4096;
   const uint32_t bar = smem_u32(&mbar[w]);
@@ -463,26 +499,16 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
       v[u] = *reinterpret_cast<const uint4*>(row + ((u ^ (lane & 7)) << 4));
     __syncwarp();
     if (lane == 0) issue(k + 1);  // every lane has its copy of this page
-    uint32_t c[4] = {0, 0, 0, 0};  // four 32-B chains (ILP)
+    // one chain of 32 words per lane; 16 warps per SM supply the parallelism
+    uint32_t c = 0;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int wi = j * 8 + q;
-        const uint4& vv = v[wi >> 2];
-        const uint32_t wd = (wi & 3) == 0 ? vv.x : (wi & 3) == 1 ? vv.y : (wi & 3) == 2 ? vv.z : vv.w;
-        const uint32_t x = c[j] ^ wd;
-        c[j] = lk(x, 0, 3) ^ lk(x, 1, 2) ^ lk(x, 2, 1) ^ lk(x, 3, 0);
-      }
+    for (int q = 0; q < 32; ++q) {
+      const uint4& vv = v[q >> 2];
+      const uint32_t wd = (q & 3) == 0 ? vv.x : (q & 3) == 1 ? vv.y : (q & 3) == 2 ? vv.z : vv.w;
+      const uint32_t x = c ^ wd;
+      c = lk(x, 0, 3) ^ lk(x, 1, 2) ^ lk(x, 2, 1) ^ lk(x, 3, 0);
     }
-    const uint32_t ab = mul_tab(lvl, c[0]) ^ c[1];
-    const uint32_t cd = mul_tab(lvl, c[2]) ^ c[3];
-    uint32_t cl = mul_tab(lvl + 1024, ab) ^ cd;
-#pragma unroll
-    for (int v2 = 0; v2 < 5; ++v2) {
-      const uint32_t o = __shfl_down_sync(0xffffffffu, cl, 1 << v2);
-      if ((lane & ((2 << v2) - 1)) == 0) cl = mul_tab(lvl + 1024 * (2 + v2), cl) ^ o;
-    }
+    const uint32_t cl = lanes_combine(c, kv);
     if (lane == 0) out[pg] = cl;
   }
 }
@@ -506,7 +532,7 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
 constexpr int kPcThreads = 512;
 constexpr int kPcProducers = 256;
 constexpr size_t kPcTabWords = kCrcTabWords;
-constexpr size_t kPcSmem = kPcTabWords * 4 + 2 * (size_t)kTile;  // 220 KiB
+constexpr size_t kPcSmem = kPcTabWords * 4 + 2 * (size_t)kTile;  // 192 KiB
 
 __device__ __forceinline__ uint32_t stage_off(uint32_t off) {  // swizzled byte offset
   const uint32_t c = off >> 4;
@@ -584,10 +610,8 @@ __global__ void __launch_bounds__(kPcThreads, 1)
                 const uint32_t* __restrict__ tabs, uint32_t* __restrict__ page_crc) {
   extern __shared__ __align__(16) uint32_t pc_smem[];
   uint32_t* rep = pc_smem;                    // [4][256][32] per-lane copies
-  uint32_t* lvl = pc_smem + 4 * 256 * 32;     // [5][4][256]
   uint8_t* stage0 = reinterpret_cast<uint8_t*>(pc_smem + kPcTabWords);
   for (int i = threadIdx.x; i < 4 * 256 * 32; i += blockDim.x) rep[i] = tabs[kTabS4 + (i >> 5)];
-  for (int i = threadIdx.x; i < (int)kLaneLevels * 1024; i += blockDim.x) lvl[i] = tabs[kTabLane + i];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp < kPcProducers / 32) {
@@ -609,6 +633,8 @@ __global__ void __launch_bounds__(kPcThreads, 1)
     for (uint32_t j = (k >= 2 ? k - 2 : 0); j < k; ++j) bar_sync(3 + (int)(j & 1), kPcThreads);
   } else {
     const int w = warp - kPcProducers / 32;  // page of the tile
+    uint32_t kv[32];
+    lane_k_init(tabs[kTabLaneK + lane], kv);
     uint32_t k = 0;
     for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
       const int b = (int)(k & 1);
@@ -622,7 +648,7 @@ __global__ void __launch_bounds__(kPcThreads, 1)
             stage + stage_off((uint32_t)w * 4096 + (uint32_t)lane * 128 + 16 * u));
       bar_arrive(3 + b, kPcThreads);  // EMPTY[b]: the page is in registers
       if (pg < n_pages) {
-        const uint32_t c = page_crc_warp<4>(v, rep, lvl, lane);
+        const uint32_t c = page_crc_warp(v, rep, kv, lane);
         if (lane == 0) page_crc[pg] = c;
       }
     }

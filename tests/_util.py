@@ -131,3 +131,19 @@ def run_threads(fns):
         if e is not None:
             raise e
     return res
+
+
+class MirrorComm:
+    """The collectives of ONE rank of a k-rank job, answered locally: every
+    rank reports this rank's own facts. Exact for the BASELINE configs C3/C4
+    (identical replicated lists; rank-local partitions of identical sizes and
+    name lengths), so one GPU can write rank r's true shard of a DP=8 job."""
+
+    def __init__(self, rank, k):
+        self.rank, self.world = rank, k
+
+    def allgather(self, vals):
+        return list(vals) * self.world
+
+    def allreduce_min(self, v):
+        return v

@@ -1,4 +1,4 @@
-"""The device CRC-32 scheme (per-lane chains, lane tree) and the host fold of page CRCs per
+"""The device CRC-32 scheme (per-lane chain, register lane combine) and the host fold of page CRCs per
 extent (ExtentCrc) emulated on the host with the library's own table
 blob and compared with the plain slicing CRC, which the native CPU tests pin
 to zlib.crc32 through the manifest. Catches a wrong table, shift or fold

@@ -12,7 +12,7 @@ import torch
 
 import paper_2406_13768_b200 as fp
 from oracle import fpck
-from tests._util import (ThreadComm, entries, file_sha, oracle_layout, run_threads)
+from tests._util import (ThreadComm, entries, file_sha, oracle_layout, otensor, run_threads)
 from workloads import config_specs, make_state
 
 pytestmark = pytest.mark.gpu
@@ -202,6 +202,63 @@ def test_c2_gpt3_1p3b_full_size_parity(tmp_path):
             assert f.read(4096) == lay.read(pg * 4096, 4096), pg
     assert file_sha(path) == fpck.shard_sha256(lay, 0)
     os.remove(path)          # pytest keeps tmp dirs: do not leave 21 GB on the disk
+
+
+def _one_rank_of_8_full_size(tmp_path, cfg, rank, need_bytes):
+    """BASELINE configs that need 8 GPUs: rank `rank` of DP=8 on this GPU
+    (MirrorComm answers its collectives exactly, see tests/_util.py), in the
+    bench launch configuration; the whole shard's sha256 against the oracle
+    streaming the same tensors."""
+    from tests._util import MirrorComm
+    free = os.statvfs(str(tmp_path))
+    if free.f_bavail * free.f_frsize < need_bytes * 1.2:
+        pytest.skip(f"needs {need_bytes * 1.2 / 1e9:.0f} GB free disk")
+    torch.cuda.empty_cache()
+    k = 8
+    st = _state(cfg, rank, k)
+    mine = [otensor(s, t, lazy=True) for s, t in st]
+    if any(s.owner >= 0 for s, _ in st):
+        # rank-local partitions: the other ranks' regions only fix offsets
+        # (same sizes and name lengths on every rank); their bytes are never read
+        def ghost(r):
+            return [fpck.OTensor(s.name, s.dtype, s.section, r, s.shape, lambda off, n: bytes(n))
+                    for s in config_specs(cfg, r, k) if s.owner >= 0]
+        local = [mine if r == rank else ghost(r) for r in range(k)]
+        lay = fpck.Layout([], local, k=k)
+    else:
+        lay = fpck.Layout(mine, k=k)
+    with fp.Checkpointer(DEV, comm=MirrorComm(rank, k)) as ck:
+        s = ck.save(entries(st), str(tmp_path))
+    assert s["image_bytes"] == lay.image_bytes
+    path = os.path.join(str(tmp_path), fpck.shard_name(rank, k))
+    assert os.path.getsize(path) == s["shard_bytes"] >= need_bytes * 0.99
+    import hashlib
+    import zlib
+    h, c = hashlib.sha256(), 0
+    for b in fpck.iter_shard(lay, rank):         # one oracle pass: sha256 + CRC-32
+        h.update(b)
+        c = zlib.crc32(b, c)
+    assert s["shard_crc32"] == c
+    assert file_sha(path) == h.hexdigest()
+    os.remove(path)          # pytest keeps tmp dirs: do not leave the shard on the disk
+    del st
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+@pytest.mark.timeout(1500)
+def test_c3_gpt3_6p7b_rank3_of_8_full_size_parity(tmp_path):
+    """BASELINE configs[2] (GPT-3 6.7B, ~107 GB replicated, DP=8): rank 3's
+    13.3 GB shard, byte for byte (sha256 and CRC-32) against the oracle."""
+    _one_rank_of_8_full_size(tmp_path, "c3_gpt3_6.7b", 3, 13.3e9)
+
+
+@pytest.mark.slow
+@pytest.mark.timeout(1500)
+def test_c4_gpt3_13b_zero_rank0_of_8_full_size_parity(tmp_path):
+    """BASELINE configs[3] (GPT-3 13B, ZeRO-partitioned, ~208 GB over 8):
+    rank 0's 25.7 GB partition shard against the oracle."""
+    _one_rank_of_8_full_size(tmp_path, "c4_gpt3_13b_zero", 0, 25.7e9)
 
 
 @pytest.mark.parametrize("exchange", ["peer", "nccl"])

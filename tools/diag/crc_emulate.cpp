@@ -1,7 +1,7 @@
 // Host emulation of the device CRC-32 scheme (pack.cu: page_crc_warp as used
 // by fp_crc_pages / fp_crc_pages_tma / fp_pack_crc) and the host fold of page
 // CRCs per extent (ExtentCrc): the same table blob (crc_device_tables), the
-// same chain split and lane tree, compared with the plain slicing CRC
+// same per-lane chain and register lane combine, compared with the plain slicing CRC
 // (crc_raw_update) on random pages, for several page and extent counts. Built and run by
 // tests/test_crc_scheme_cpu.py (no GPU needed).
 #include <cstdio>
@@ -9,9 +9,6 @@
 #include <vector>
 #include "fp_internal.h"
 using namespace fp;
-static uint32_t mul_tab(const uint32_t* m, uint32_t a) {
-  return m[a & 255] ^ m[256 + ((a >> 8) & 255)] ^ m[512 + ((a >> 16) & 255)] ^ m[768 + (a >> 24)];
-}
 int main() {
   auto T = crc_device_tables();
   const uint32_t* t0 = &T[kTabS4], *t1 = t0 + 256, *t2 = t0 + 512, *t3 = t0 + 768;
@@ -20,27 +17,22 @@ int main() {
     for (auto& b : buf) b = rand() & 255;
     std::vector<uint32_t> pc(n_pages);
     for (uint32_t pg = 0; pg < n_pages; ++pg) {
-      uint32_t lc[32];
-      const int chains = (pg & 1) ? 4 : 1;  // both variants of page_crc_warp
+      // pack.cu page_crc_warp / fp_crc_pages_tma: one slicing-by-4 chain per
+      // lane over its 128 bytes, then R_l * K_l (K_l = x^(8*128*(31-l)), the
+      // product through kv[i] = K_l * x^i as lane_k_init / gf_mul_k do), XOR
+      uint32_t crc = 0;
       for (int lane = 0; lane < 32; ++lane) {
         const uint32_t* w = (const uint32_t*)(buf.data() + (size_t)pg * 4096 + lane * 128);
-        uint32_t c[4] = {0,0,0,0};
-        const int kw = 32 / chains;
-        for (int q = 0; q < kw; ++q) for (int j = 0; j < chains; ++j) { uint32_t x = c[j] ^ w[kw*j + q]; c[j] = t3[x & 255] ^ t2[(x >> 8) & 255] ^ t1[(x >> 16) & 255] ^ t0[x >> 24]; }
-        if (chains == 4) {
-          uint32_t ab = mul_tab(&T[kTabLane], c[0]) ^ c[1], cd = mul_tab(&T[kTabLane], c[2]) ^ c[3];
-          lc[lane] = mul_tab(&T[kTabLane + 1024], ab) ^ cd;
-        } else {
-          lc[lane] = c[0];
-        }
+        uint32_t c = 0;
+        for (int q = 0; q < 32; ++q) { uint32_t x = c ^ w[q]; c = t3[x & 255] ^ t2[(x >> 8) & 255] ^ t1[(x >> 16) & 255] ^ t0[x >> 24]; }
+        uint32_t kv[32];
+        kv[0] = T[kTabLaneK + lane];
+        for (int i = 1; i < 32; ++i) kv[i] = (kv[i - 1] >> 1) ^ ((kv[i - 1] & 1) ? 0xEDB88320u : 0u);
+        uint32_t p = 0;
+        for (int i = 0; i < 32; ++i) p ^= (0u - ((c >> (31 - i)) & 1u)) & kv[i];
+        crc ^= p;
       }
-      for (int v = 0; v < 5; ++v) {
-        uint32_t nc[32];
-        for (int l = 0; l < 32; ++l) { uint32_t o = l + (1 << v) < 32 ? lc[l + (1 << v)] : lc[l];
-          nc[l] = ((l & ((2 << v) - 1)) == 0) ? mul_tab(&T[kTabLane + 1024 * (2 + v)], lc[l]) ^ o : lc[l]; }
-        for (int l = 0; l < 32; ++l) lc[l] = nc[l];
-      }
-      pc[pg] = lc[0];
+      pc[pg] = crc;
       if (pc[pg] != crc_raw_update(0, buf.data() + (size_t)pg * 4096, 4096)) { printf("page mismatch\n"); return 1; }
     }
     // host fold (ExtentCrc): the pages split into extents at page boundaries
