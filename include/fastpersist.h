@@ -206,6 +206,7 @@ typedef struct fp_load_stats {
                                2: peer memory (fp_unpack_peer reads every
                                writer's partition from its device buffer)      */
   int32_t  status;          /* return code of that load                           */
+  double   t_exchange_wait; /* s the host waited for peers' chunks (exchange 2)    */
 } fp_load_stats;
 
 typedef struct fp_ctx fp_ctx;
@@ -290,10 +291,13 @@ int fp_ckpt_load(fp_ctx *ctx, const fp_tensor *t, size_t n, const char *path,
  *       the same pointers for ranks that are threads of one process) and one
  *       fp_unpack_peer launch per chunk on `stream` scatters the chunk of
  *       every writer straight from its buffer into t[i] (P2P loads over
- *       NVLink), each CTA first waiting for the writers' ready flags (set by
- *       their copy engines). FP_LOAD_EXCHANGE=peer requires it (-ENOSYS if a
- *       buffer cannot be mapped), =nccl disables it. FP_PEER_TIMEOUT_S (600)
- *       bounds the wait for a peer (then FP_ECOMM).
+ *       NVLink). Each writer's copy engine sets a ready flag per chunk (a
+ *       4-byte copy behind the chunk's H2D into a POSIX shared-memory
+ *       segment registered with CUDA); the host launches the unpack of chunk
+ *       j once every writer's flag j is set (no GPU-side spinning).
+ *       FP_LOAD_EXCHANGE=peer requires it (-ENOSYS if a buffer cannot be
+ *       mapped), =nccl disables it. FP_PEER_TIMEOUT_S (600) bounds the wait
+ *       for a peer (then FP_ECOMM).
  *   1 = gathered (host state, or no IPC): one comm->allgather_bytes per chunk
  *       (bytes = slot_bytes per rank; shorter partitions send padding), then
  *       fp_unpack_v4 from the gathered buffer.

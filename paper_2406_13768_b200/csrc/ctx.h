@@ -88,8 +88,7 @@ struct fp_ctx {
   //  so the events time the kernel, not the host API latency of an idle stream
   //  done: id of the checkpoint whose shard became durable (or failed), waited
   //  for on the caller's stream by fp_ckpt_fence
-  // [0] gate, [16] done, [32] fence timeout, [48] constant 1 (source of the
-  // peer-exchange ready flags), [64] peer-exchange timeout
+  // [0] gate, [16] done, [32] fence timeout
   volatile uint32_t* h_sig = nullptr;
   uint32_t* d_sig = nullptr;
   bool gate_on = false;

@@ -160,19 +160,16 @@ int pack_launch(int impl, const Item* d_items, uint32_t n_items, uint8_t* d_slab
 int unpack_launch(const Item* d_items, uint32_t n_items, const uint8_t* d_slab, int ctas,
                   void* stream);
 int pack_default_ctas(int impl, int device);
-// peer-exchange load (fp_unpack_peer): writer w's replicated partition at
-// base[w], its per-chunk ready flags (u32, nonzero = landed) at flag[w]
+// peer-exchange load (fp_unpack_peer): writer w's replicated partition at base[w]
 constexpr int kMaxPeers = 64;
 struct PeerTab {
   uint64_t base[kMaxPeers];
-  uint64_t flag[kMaxPeers];
 };
 // items of exchange chunk `chunk` (Item.len bits 24..31 = writer) scattered
-// from base[w] + chunk * ch_bytes + Item.dst after waiting for flag[w][chunk]
-// of every writer in wmask (max_ns: then *d_timed_out = 1)
+// from base[w] + chunk * ch_bytes + Item.dst (launched once every writer's
+// chunk has landed)
 int unpack_peer_launch(const Item* d_items, uint32_t n_items, const PeerTab* d_tab, uint32_t chunk,
-                       uint64_t ch_bytes, uint64_t wmask, uint64_t max_ns, uint32_t* d_timed_out,
-                       int ctas, void* stream);
+                       uint64_t ch_bytes, int ctas, void* stream);
 // one-warp kernel on `stream` that waits until the mapped word *d_flag
 // reaches `value` (or max_ns passes; then *d_timed_out = 1 if non-null)
 int flag_wait_launch(const uint32_t* d_flag, uint32_t value, uint64_t max_ns,

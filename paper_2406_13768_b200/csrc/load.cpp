@@ -3,8 +3,11 @@
 // two-step load, §4.2: own partition + all-gather).
 #include <cuda_runtime.h>
 #include <fcntl.h>
+#include <sys/mman.h>
 #include <sys/stat.h>
 #include <unistd.h>
+
+#include <atomic>
 
 #include <algorithm>
 #include <cerrno>
@@ -846,11 +849,30 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
   const char* xm = getenv("FP_LOAD_EXCHANGE");
   const std::string xmode = xm ? xm : "auto";
   int status = 0;
-  uint8_t* pbuf = nullptr;  // peer mode: [ready flags | own replicated partition]
-  const uint64_t flag_bytes = round_up(std::max<uint64_t>(nrep, 1) * 4, 4096);
+  uint8_t* pbuf = nullptr;  // peer mode: [4 KiB: ready-flag source word | own partition]
+  const uint64_t flag_bytes = 4096;
   PeerTab tab{};
   std::vector<void*> opened;
   bool peer = false;
+  // Ready flags: one u32 per (writer, chunk) in a POSIX shared-memory segment
+  // that rank 0 creates and every rank maps and registers with CUDA. Writer
+  // w's copy engine sets flag (w, j) right behind the H2D of its chunk j (a
+  // 4-byte D2H on the same stream); a consumer's HOST waits for the flags of
+  // chunk j before it launches the unpack of chunk j. No kernel ever spins:
+  // with streams of several ranks (or several streams of one rank) sharing a
+  // hardware queue, a GPU-side wait could sit in front of the very copy it
+  // waits for.
+  volatile uint32_t* rflags = nullptr;
+  size_t rflags_bytes = 0;
+  bool rflags_reg = false;
+  std::string shm_name;
+  auto drop_flags = [&](bool unlink_it) {
+    if (rflags_reg) cudaHostUnregister((void*)rflags);
+    if (rflags) munmap((void*)rflags, rflags_bytes);
+    rflags = nullptr;
+    rflags_reg = false;
+    if (unlink_it && rank == 0 && !shm_name.empty()) shm_unlink(shm_name.c_str());
+  };
   if (dev && k > 1 && k <= kMaxPeers && xmode != "nccl") {
     int ok = 1;
     cudaIpcMemHandle_t h{};
@@ -859,27 +881,51 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
       pbuf = nullptr;
       ok = 0;
     }
-    // zero the ready flags, ordered before this rank's flag copies (same
-    // stream) and complete before any peer can look at them (the sync below
-    // precedes the handle exchange)
-    if (ok && (cudaMemsetAsync(pbuf, 0, flag_bytes, c->stream) != cudaSuccess ||
+    // the source word of this rank's flag copies (nonzero), ready before use
+    if (ok && (cudaMemsetAsync(pbuf, 1, 4, c->stream) != cudaSuccess ||
                cudaStreamSynchronize(c->stream) != cudaSuccess))
       ok = 0;
     const bool ipc_ok = ok && cudaIpcGetMemHandle(&h, pbuf) == cudaSuccess;
     if (!ipc_ok) cudaGetLastError();
-    std::vector<uint64_t> mine(12, 0), all(12 * (size_t)k, 0);
+    static std::atomic<uint64_t> seq{0};
+    const uint64_t my_seq = ++seq;
+    rflags_bytes = round_up((uint64_t)k * std::max<uint64_t>(nrep, 1) * 4, 4096);
+    if (ok && rank == 0) {  // created (zero-filled) before anyone learns its name
+      const std::string nm = "/fpld." + std::to_string(getpid()) + "." + std::to_string(my_seq);
+      const int sfd = shm_open(nm.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
+      if (sfd < 0 || ftruncate(sfd, (off_t)rflags_bytes)) ok = 0;
+      if (sfd >= 0) close(sfd);
+      if (ok) shm_name = nm;
+    }
+    std::vector<uint64_t> mine(13, 0), all(13 * (size_t)k, 0);
     mine[0] = (uint64_t)getpid();
     mine[1] = (uint64_t)(int64_t)c->dev;
     mine[2] = ipc_ok ? 1 : 0;
     mine[3] = (uint64_t)(uintptr_t)pbuf;
     memcpy(&mine[4], &h, sizeof(h));
+    mine[12] = my_seq;
     int32_t v = ok;
     if (c->comm.allreduce_min_i32(c->comm.ctx, &v)) v = -1;
-    if (v == 1 && c->comm.allgather_u64(c->comm.ctx, mine.data(), all.data(), 12)) v = -1;
+    if (v == 1 && c->comm.allgather_u64(c->comm.ctx, mine.data(), all.data(), 13)) v = -1;
     if (v == 1) {
       int mok = 1;
+      shm_name = "/fpld." + std::to_string(all[0]) + "." + std::to_string(all[12]);
+      const int sfd = shm_open(shm_name.c_str(), O_RDWR, 0600);
+      void* mp = sfd < 0 ? MAP_FAILED
+                         : mmap(nullptr, rflags_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, sfd, 0);
+      if (sfd >= 0) close(sfd);
+      if (mp == MAP_FAILED) {
+        mok = 0;
+      } else {
+        rflags = (volatile uint32_t*)mp;
+        rflags_reg = cudaHostRegister(mp, rflags_bytes, cudaHostRegisterPortable) == cudaSuccess;
+        if (!rflags_reg) {
+          cudaGetLastError();
+          mok = 0;
+        }
+      }
       for (int w = 0; w < k && mok; ++w) {
-        const uint64_t* q = &all[12 * (size_t)w];
+        const uint64_t* q = &all[13 * (size_t)w];
         void* ptr = nullptr;
         if (q[0] == (uint64_t)getpid()) {  // same process (thread ranks): same address space
           ptr = (void*)(uintptr_t)q[3];
@@ -901,7 +947,6 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
         } else {
           mok = 0;
         }
-        tab.flag[w] = (uint64_t)(uintptr_t)ptr;
         tab.base[w] = (uint64_t)(uintptr_t)ptr + flag_bytes;
       }
       v = mok;
@@ -911,10 +956,14 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
     if (!peer) {
       for (void* q : opened) cudaIpcCloseMemHandle(q);
       opened.clear();
+      drop_flags(false);
       if (pbuf) cudaFree(pbuf);
       pbuf = nullptr;
       if (xmode == "peer") status = -ENOSYS;  // peer exchange was required
       if (v < 0) status = FP_ECOMM;
+      // every rank has stopped using the segment (the all-reduce above)
+      if (rank == 0 && !shm_name.empty()) shm_unlink(shm_name.c_str());
+      shm_name.clear();
     }
   }
   if (!status && k > 1 && !peer && !c->comm.allgather_bytes) status = -ENOSYS;
@@ -1031,7 +1080,8 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
     }
     return 0;
   });
-  const uint64_t spin_ns = env_u64("FP_PEER_TIMEOUT_S", 600) * 1000000000ull;
+  const double spin_s = (double)env_u64("FP_PEER_TIMEOUT_S", 600);
+  bool peer_failed = false;
   uint64_t launches = 0;
   for (uint64_t j = 0; run && j < total_chunks; ++j) {  // every rank runs every exchange
     const bool is_rep = j < nrep;
@@ -1083,10 +1133,11 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
         cudaEventRecord(c->ev_d2h[s], xs);
       }
       if (peer && is_rep && mylen) {
-        // ready flag of chunk j: a 4-byte copy behind the data on the copy
-        // stream (no kernel: a flag never waits for an SM)
-        if (cudaMemcpyAsync(pbuf + 4 * j, (const void*)&c->h_sig[48], 4, cudaMemcpyHostToDevice,
-                            cs) != cudaSuccess && !status)
+        // ready flag (rank, j): a 4-byte copy behind the data on the copy
+        // stream into the shared segment (no kernel: a flag never waits for
+        // an SM)
+        if (cudaMemcpyAsync((void*)&rflags[(size_t)rank * nrep + j], pbuf, 4,
+                            cudaMemcpyDeviceToHost, cs) != cudaSuccess && !status)
           status = FP_ECUDA;
       }
       if (gpu_crc && mylen) {
@@ -1126,11 +1177,31 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
     }
     const uint32_t i0 = lo[j], i1 = lo[j + 1];
     if (peer && is_rep) {
-      // runs even after a local error: a launch per chunk on every rank keeps
-      // the flags of the peers' buffers consumed in order (status decides)
-      if (unpack_peer_launch(d_items + i0, i1 - i0, d_tab, (uint32_t)j, CH, wmask[j], spin_ns,
-                             c->d_sig + 64, c->pack_ctas, st) && !status)
+      // every writer's chunk j has landed in its buffer (its flag): then the
+      // unpack reads them all straight from the writers' buffers
+      if (!peer_failed) {
+        const double t_w = now_s();
+        for (int w = 0; w < k && !peer_failed; ++w) {
+          if (!((wmask[j] >> w) & 1)) continue;
+          const volatile uint32_t* f = &rflags[(size_t)w * nrep + j];
+          for (uint32_t spins = 0; !__atomic_load_n(f, __ATOMIC_ACQUIRE); ++spins) {
+            if (now_s() - t_w > spin_s) {
+              fprintf(stderr, "fastpersist: rank %d: chunk %llu of rank %d never arrived "
+                              "(peer exchange timed out)\n", rank, (unsigned long long)j, w);
+              peer_failed = true;
+              break;
+            }
+            if (spins > 64) usleep(20);
+          }
+        }
+        c->ld.t_exchange_wait += now_s() - t_w;
+      }
+      if (peer_failed) {
+        if (!status) status = FP_ECOMM;  // keep publishing our flags: peers are not left waiting
+      } else if (unpack_peer_launch(d_items + i0, i1 - i0, d_tab, (uint32_t)j, CH, c->pack_ctas,
+                                    st) && !status) {
         status = FP_ECUDA;
+      }
       ++launches;
     } else if (i1 > i0 && status == 0) {
       if (dev) {
@@ -1150,10 +1221,6 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
   if (dev && cudaStreamSynchronize(st) != cudaSuccess && !status) status = FP_ECUDA;
   if (peer) {
     if (cudaStreamSynchronize(cs) != cudaSuccess && !status) status = FP_ECUDA;
-    if (__atomic_exchange_n(&c->h_sig[64], 0u, __ATOMIC_ACQ_REL) && !status) {
-      fprintf(stderr, "fastpersist: a peer's chunk never arrived (peer exchange timed out)\n");
-      status = FP_ECOMM;
-    }
     // GHDR bytes straight from the writers' buffers
     for (int w = 0; w < k && run && !status; ++w) {
       const uint64_t a0 = part_off(w), pb = part_bytes(w);
@@ -1187,7 +1254,9 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
     status = FP_ECORRUPT;
   }
   for (void* q : opened) cudaIpcCloseMemHandle(q);  // before the owners free (barrier below)
+  if (peer) drop_flags(false);
   status = status_min(c, k, status);
+  if (peer && rank == 0 && !shm_name.empty()) shm_unlink(shm_name.c_str());  // all unmapped
   c->ld.kernel_launches = launches;
   c->ld.bytes_read = part_bytes(rank) + lreg_len;
   c->ld.status = status;

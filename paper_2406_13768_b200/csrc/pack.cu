@@ -38,17 +38,36 @@ namespace {
 constexpr int kV4Threads = 256;
 constexpr int kV4Unroll = 8;  // 256 thr x 8 x 16 B = 32 KiB = kTile per pass
 
+// Streaming accesses (SURVEY §8(a'): the pack must not evict the training
+// stream's L2 working set): loads bypass L1 and, like the stores, carry an
+// L2 evict-first policy — every byte is touched once (the slab is re-read by
+// the copy engine, but a 256 MiB group exceeds the 126 MB L2 anyway).
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ uint4 ld_stream(const uint4* p) {
   uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
+  asm volatile(
+      "{\n"
+      ".reg .b64 pol;\n"
+      "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+      "ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], pol;\n"
+      "}\n"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p));
   return r;
 }
 __device__ __forceinline__ void st_v4(uint4* p, const uint4& v) {
-  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
-               "r"(v.w)
-               : "memory");
+  asm volatile(
+      "{\n"
+      ".reg .b64 pol;\n"
+      "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+      "st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, pol;\n"
+      "}\n" ::"l"(p),
+      "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+      : "memory");
 }
 
 // coherent 16-B load (data another agent may have written while this kernel
@@ -178,35 +197,14 @@ __global__ void __launch_bounds__(kV4Threads) fp_unpack_v4(const Item* __restric
 // for thread ranks); one launch per exchange chunk j scatters the chunk of
 // EVERY writer straight from the writers' buffers into the local tensors (P2P
 // loads over NVLink on a multi-GPU node), so the all-gather and the scatter
-// are one pass with no gathered copy. Before touching writer w's bytes a CTA
-// waits for w's ready flag of chunk j (set by w's copy engine right after
-// the chunk's H2D, stream-ordered), with a timeout that sets *timed_out.
-// Item.len carries the writer index in bits 24..31; Item.dst is the offset
-// inside the writer's chunk.
+// are one pass with no gathered copy. The host launches it only once every
+// writer's chunk j has landed (their ready flags). Item.len carries the
+// writer index in bits 24..31; Item.dst is the offset inside the writer's
+// chunk. Coherent loads: the buffers were written by other engines.
 __global__ void __launch_bounds__(kV4Threads) fp_unpack_peer(const Item* __restrict__ items,
                                                              uint32_t n,
                                                              const PeerTab* __restrict__ tab,
-                                                             uint32_t j, uint64_t ch_bytes,
-                                                             uint64_t wmask, uint64_t max_ns,
-                                                             uint32_t* __restrict__ timed_out) {
-  if (threadIdx.x < 64 && ((wmask >> threadIdx.x) & 1)) {
-    const uint32_t* f = reinterpret_cast<const uint32_t*>(tab->flag[threadIdx.x]) + j;
-    uint64_t t0, t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    for (;;) {
-      uint32_t x;
-      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(x) : "l"(f) : "memory");
-      if (x) break;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      if (t - t0 > max_ns) {
-        if (timed_out) asm volatile("st.release.sys.global.u32 [%0], 1;" ::"l"(timed_out) : "memory");
-        break;
-      }
-      __nanosleep(512);
-    }
-    __threadfence();
-  }
-  __syncthreads();
+                                                             uint32_t j, uint64_t ch_bytes) {
   for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
     const Item it = items[i];
     if (!it.src) continue;
@@ -251,7 +249,8 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
 
   if (warp == 0) {
     // warp 0 walks the items 32 at a time (one coalesced descriptor load per
-    // lane); lane 0 alone issues the bulk copies.
+    // lane); lane 0 alone issues the bulk copies (L2 evict-first both ways).
+    const uint64_t pol = evict_first_policy();
     uint32_t issued = 0, stored = 0;
     auto store_one = [&]() {
       const uint32_t s = stored % kBulkStages;
@@ -266,10 +265,11 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
           "}\n" ::"r"(bar),
           "r"(parity)
           : "memory");
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
-                       slab + st_dst[s]),
-                   "r"(smem_u32(smem + (size_t)s * kBulkStageBytes)), "r"(st_len[s])
-                   : "memory");
+      asm volatile(
+          "cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
+              slab + st_dst[s]),
+          "r"(smem_u32(smem + (size_t)s * kBulkStageBytes)), "r"(st_len[s]), "l"(pol)
+          : "memory");
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       ++stored;
     };
@@ -298,9 +298,9 @@ __global__ void __launch_bounds__(kBulkThreads, 1)
                        "r"(bytes)
                        : "memory");
           asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], "
-              "%2, [%3];" ::"r"(smem_u32(smem + (size_t)s * kBulkStageBytes)),
-              "l"(src), "r"(bytes), "r"(bar)
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+              "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(smem + (size_t)s * kBulkStageBytes)),
+              "l"(src), "r"(bytes), "r"(bar), "l"(pol)
               : "memory");
           ++issued;
         }
@@ -793,12 +793,11 @@ int pack_crc_launch(const Item* d_items, const uint32_t* d_tile_lo, uint32_t n_t
 }
 
 int unpack_peer_launch(const Item* d_items, uint32_t n_items, const PeerTab* d_tab, uint32_t chunk,
-                       uint64_t ch_bytes, uint64_t wmask, uint64_t max_ns, uint32_t* d_timed_out,
-                       int ctas, void* stream) {
+                       uint64_t ch_bytes, int ctas, void* stream) {
   if (!n_items) return 0;
   const int grid = (int)((uint32_t)ctas < n_items ? (uint32_t)ctas : n_items);
   fp_unpack_peer<<<grid, kV4Threads, 0, (cudaStream_t)stream>>>(d_items, n_items, d_tab, chunk,
-                                                               ch_bytes, wmask, max_ns, d_timed_out);
+                                                               ch_bytes);
   return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
 }
 

@@ -948,7 +948,6 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
         return fail(-ENOMEM);
       memset(hg, 0, 4096);
       c->h_sig = (volatile uint32_t*)hg;
-      c->h_sig[48] = 1;  // source word of the peer-exchange ready flags
       if (cudaHostGetDevicePointer(&dg, hg, 0) != cudaSuccess) return fail(FP_ECUDA);
       c->d_sig = (uint32_t*)dg;
       // The launch gate is measurement machinery (opt-in, FP_LAUNCH_GATE=1:
