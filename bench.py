@@ -754,7 +754,8 @@ def our_arm(a):
         fused = a.pack == "v4" and bool(os.environ.get("FP_CRC_FUSED")) \
             and not os.environ.get("FP_NO_CRC")
         kname = {"v4": "fp_pack_crc" if fused else "fp_pack_v4",
-                 "bulk": "fp_pack_bulk", "host": "fp_pack_v4 (to mapped host)"}.get(a.pack)
+                 "bulk": "fp_pack_bulk" if os.environ.get("FP_NO_CRC") else "fp_pack_bulk_crc",
+                 "host": "fp_pack_v4 (to mapped host)"}.get(a.pack)
         traffic = a.traffic
         try:   # ncu-measured DRAM bytes per launch of this launch shape (profiles/)
             with open(os.path.join(ROOT, "profiles", "pack_traffic.json")) as f:

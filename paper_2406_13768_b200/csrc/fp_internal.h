@@ -179,6 +179,13 @@ int flag_wait_launch(const uint32_t* d_flag, uint32_t value, uint64_t max_ns,
 // crc_device_tables); the host folds them (ExtentCrc)
 int crc_pages_launch(const uint8_t* d_buf, uint64_t bytes, const uint32_t* d_tabs,
                      uint32_t* d_page_crc, void* stream);
+// fused TMA-engine pack + page CRCs (fp_pack_bulk_crc, the default with
+// FP_PACK_BULK): tiles as below, gbytes = slab bytes of the group; the raw CRC
+// of every page starting below gbytes -> d_page_crc (a ragged last page's CRC
+// covers stale bytes: the host CRCs ragged chunks itself)
+int pack_bulk_crc_launch(const Item* d_items, const uint32_t* d_tile_lo, uint32_t n_tiles,
+                         uint64_t gbytes, uint8_t* d_slab, const uint32_t* d_tabs,
+                         uint32_t* d_page_crc, int ctas, void* stream);
 // fused pack + page CRCs (fp_pack_crc, ablation): items of n_tiles 32 KiB slab
 // tiles (tile t = items [d_tile_lo[t], d_tile_lo[t+1]), none crossing a tile
 // boundary) -> d_slab, raw CRC of each of the first n_pages pages -> d_page_crc

@@ -514,6 +514,235 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
 }
 
 // ---------------------------------------------------------------------------
+// fp_pack_bulk_crc: the TMA-engine pack and the page CRCs in ONE pass (SURVEY
+// f4 "per-shard checksum fused into the pack kernel"). Work unit: one 32 KiB
+// slab tile (8 pages); items never cross a tile (plan_tiles). One CTA per SM,
+// 3 shared-memory stages of one tile each:
+//   warp 0 (producer): lane 0 issues cp.async.bulk G2S for the 16-B aligned
+//     bodies of the tile's items into the stage (mbarrier complete_tx), and
+//     once the stage is FULL, one cp.async.bulk S2G of the whole tile to the
+//     slab; it refills a stage when its S2G has been read out of shared
+//     memory and the CRC warps released it (EMPTY), signalling FREE to the
+//     LSU warps; L2 evict-first both ways.
+//   warps 1-2 (LSU): zero fill, misaligned items and <16 B tails straight
+//     into the stage (generic stores + proxy fence), then arrive on FULL.
+//   warps 3-10 (CRC): page p of the tile from the stage — lane l reads its
+//     128-B row with the 16-B chunks rotated by (l & 7) (conflict-free:
+//     a linear TMA row layout puts every lane's row in the same banks) and
+//     puts them back in order with a 3-level register barrel shift — one
+//     slicing-by-4 chain per lane, lanes_combine; arrive on EMPTY.
+// The slab is written and read once (2 B of HBM per image byte): the CRC no
+// longer re-reads it (the separate fp_crc_pages_tma pass: +1 B per byte).
+// ---------------------------------------------------------------------------
+constexpr int kBcStages = 3;
+constexpr int kBcLsuWarps = 2;
+constexpr int kBcCrcWarps = kTile / 4096;  // 8: one page each
+constexpr int kBcThreads = 32 * (1 + kBcLsuWarps + kBcCrcWarps);
+constexpr size_t kBcSmem = kCtTabBytes + (size_t)kBcStages * kTile + 128;
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+// generic-proxy copy of `len` bytes into shared memory (src == nullptr: zeros)
+__device__ __forceinline__ void copy_to_smem(uint8_t* dst, const uint8_t* __restrict__ src,
+                                             uint32_t len, int t, int nthr) {
+  const bool vec = !(((uintptr_t)dst | (uintptr_t)src | len) & 15);
+  if (vec) {
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    for (uint32_t j = t; j < len / 16; j += nthr)
+      reinterpret_cast<uint4*>(dst)[j] = src ? ld_stream(reinterpret_cast<const uint4*>(src) + j) : z;
+    return;
+  }
+  for (uint32_t j = t; j < len; j += nthr) dst[j] = src ? src[j] : 0;
+}
+
+__global__ void __launch_bounds__(kBcThreads, 1)
+    fp_pack_bulk_crc(const Item* __restrict__ items, const uint32_t* __restrict__ tile_lo,
+                     uint32_t n_tiles, uint64_t gbytes, uint8_t* __restrict__ slab,
+                     const uint32_t* __restrict__ tabs, uint32_t* __restrict__ page_crc) {
+  extern __shared__ __align__(128) uint8_t bc_raw[];
+  uint8_t* stages = bc_raw + kCtTabBytes;  // kCtTabBytes is a multiple of 128
+  uint64_t* full = reinterpret_cast<uint64_t*>(stages + (size_t)kBcStages * kTile);
+  uint64_t* empty = full + kBcStages;
+  uint64_t* freeb = empty + kBcStages;
+  for (int i = threadIdx.x; i < 4 * 256 * 32; i += blockDim.x) {  // paired per-lane tables
+    const int k = i >> 13, e = (i >> 5) & 255, l = i & 31;
+    *reinterpret_cast<uint32_t*>(bc_raw + (k >> 1) * 65536 + e * 256 + (k & 1) * 128 + l * 4) =
+        tabs[kTabS4 + k * 256 + e];
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kBcStages; ++s) {
+      mbar_init(&full[s], 1 + kBcLsuWarps);
+      mbar_init(&empty[s], kBcCrcWarps);
+      mbar_init(&freeb[s], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (blockIdx.x >= n_tiles) return;
+  const uint32_t nt = (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;  // tiles of this CTA
+  auto tile_of = [&](uint32_t i) { return blockIdx.x + i * gridDim.x; };
+  auto tile_len = [&](uint32_t t) {
+    const uint64_t left = gbytes - (uint64_t)t * kTile;
+    return (uint32_t)(left < kTile ? left : kTile);
+  };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0) {
+    const uint64_t pol = evict_first_policy();
+    auto fill = [&](uint32_t i) {  // G2S of tile i's 16-B aligned item bodies
+      const uint32_t t = tile_of(i), s = i % kBcStages;
+      uint8_t* st = stages + (size_t)s * kTile;
+      const uint32_t lo = tile_lo[t], hi = tile_lo[t + 1];
+      uint32_t total = 0;
+      for (uint32_t b = lo; b < hi; b += 32) {
+        Item it = {0, 0, 0};
+        if (b + lane < hi) it = items[b + lane];
+        total += (b + lane < hi && bulk_ok(it)) ? (it.len & ~15u) : 0u;
+      }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+      const uint32_t bar = smem_u32(&full[s]);
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_tx(bar, total);
+      }
+      for (uint32_t b = lo; b < hi; b += 32) {
+        Item mine = {0, 0, 0};
+        if (b + lane < hi) mine = items[b + lane];
+        uint32_t mask = __ballot_sync(0xffffffffu, b + lane < hi && bulk_ok(mine));
+        while (mask) {
+          const int j = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const uint64_t src = __shfl_sync(0xffffffffu, mine.src, j);
+          const uint32_t dst = __shfl_sync(0xffffffffu, mine.dst, j);
+          const uint32_t len = __shfl_sync(0xffffffffu, mine.len, j);
+          if (lane == 0)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+                " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(st + (dst % kTile))),
+                "l"(src), "r"(len & ~15u), "r"(bar), "l"(pol)
+                : "memory");
+        }
+      }
+    };
+    const uint32_t ahead = nt < (uint32_t)kBcStages ? nt : (uint32_t)kBcStages;
+    for (uint32_t i = 0; i < ahead; ++i) fill(i);
+    for (uint32_t i = 0; i < nt; ++i) {
+      const uint32_t s = i % kBcStages, t = tile_of(i), tl = tile_len(t);
+      uint8_t* st = stages + (size_t)s * kTile;
+      mbar_wait(smem_u32(&full[s]), (i / kBcStages) & 1);
+      const uint32_t body = tl & ~15u;
+      if (lane == 0 && body) {
+        asm volatile(
+            "cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
+                slab + (uint64_t)t * kTile),
+            "r"(smem_u32(st)), "r"(body), "l"(pol)
+            : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      if ((uint32_t)lane < tl - body) slab[(uint64_t)t * kTile + body + lane] = st[body + lane];
+      if (i + kBcStages < nt) {
+        // the stage is refilled once its S2G has read it and the CRC warps let go
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        mbar_wait(smem_u32(&empty[s]), (i / kBcStages) & 1);
+        if (lane == 0) mbar_arrive(smem_u32(&freeb[s]));
+        fill(i + kBcStages);
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  } else if (warp <= kBcLsuWarps) {
+    const int t0 = threadIdx.x - 32, nthr = 32 * kBcLsuWarps;
+    for (uint32_t i = 0; i < nt; ++i) {
+      const uint32_t s = i % kBcStages, t = tile_of(i);
+      uint8_t* st = stages + (size_t)s * kTile;
+      if (i >= (uint32_t)kBcStages) mbar_wait(smem_u32(&freeb[s]), (i / kBcStages - 1) & 1);
+      for (uint32_t k = tile_lo[t]; k < tile_lo[t + 1]; ++k) {
+        const Item it = items[k];
+        const uint32_t off = it.dst % kTile;
+        if (bulk_ok(it)) {
+          const uint32_t body = it.len & ~15u;
+          if ((uint32_t)t0 < it.len - body)
+            st[off + body + t0] = reinterpret_cast<const uint8_t*>(it.src)[body + t0];
+        } else {
+          copy_to_smem(st + off, reinterpret_cast<const uint8_t*>(it.src), it.len, t0, nthr);
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the S2G
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&full[s]));
+    }
+  } else {
+    const int p = warp - 1 - kBcLsuWarps;  // page of the tile
+    const uint32_t lane4 = (uint32_t)lane * 4, rot = (uint32_t)lane & 7;
+    uint32_t kv[32];
+    lane_k_init(tabs[kTabLaneK + lane], kv);
+    auto lk = [&](uint32_t x, const int b, const int tb) -> uint32_t {
+      const uint32_t r = __byte_perm(x, lane4, 4u | ((uint32_t)b << 4) | (5u << 8) | (5u << 12));
+      return *reinterpret_cast<const uint32_t*>(bc_raw + r + ((tb >> 1) * 65536 + (tb & 1) * 128));
+    };
+    for (uint32_t i = 0; i < nt; ++i) {
+      const uint32_t s = i % kBcStages, t = tile_of(i);
+      mbar_wait(smem_u32(&full[s]), (i / kBcStages) & 1);
+      const uint32_t pg = t * (kTile / 4096) + (uint32_t)p;
+      const bool live = (uint64_t)pg * 4096 < gbytes;
+      if (live) {
+        const uint8_t* row = stages + (size_t)s * kTile + (size_t)p * 4096 + lane * 128;
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)  // chunk (u + rot) & 7 lands in v[u]
+          v[u] = *reinterpret_cast<const uint4*>(row + (((u + rot) & 7) << 4));
+        // v[u] holds chunk (u + rot) & 7: rotate right by rot so v[c] = chunk c
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          if (rot & (1u << b)) {
+            uint4 w[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) w[u] = v[(u - (1 << b)) & 7];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = w[u];
+          }
+        }
+        uint32_t c = 0;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const uint4& vv = v[q >> 2];
+          const uint32_t wd = (q & 3) == 0 ? vv.x : (q & 3) == 1 ? vv.y : (q & 3) == 2 ? vv.z : vv.w;
+          const uint32_t x = c ^ wd;
+          c = lk(x, 0, 3) ^ lk(x, 1, 2) ^ lk(x, 2, 1) ^ lk(x, 3, 0);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&empty[s]));  // the page is in registers
+        c = lanes_combine(c, kv);
+        if (lane == 0) page_crc[pg] = c;
+      } else {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // fp_pack_crc: the pack and the page CRCs in ONE pass over the data (the
 // separate fp_crc_pages re-reads the whole slab from HBM). Work unit: one
 // 32 KiB tile of the slab (8 pages); items never cross a tile boundary and
@@ -776,6 +1005,18 @@ int crc_pages_launch(const uint8_t* d_buf, uint64_t bytes, const uint32_t* d_tab
     const int grid_p = (int)std::min<uint32_t>((n_pages + 31) / 32, (uint32_t)sm_count(-1));
     fp_crc_pages<<<grid_p, kCrcThreads, kCrcPagesSmem, st>>>(d_buf, n_pages, d_tabs, d_page_crc);
   }
+  return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
+}
+
+int pack_bulk_crc_launch(const Item* d_items, const uint32_t* d_tile_lo, uint32_t n_tiles,
+                         uint64_t gbytes, uint8_t* d_slab, const uint32_t* d_tabs,
+                         uint32_t* d_page_crc, int ctas, void* stream) {
+  if (!n_tiles) return 0;
+  if (!smem_opt_in<4>(fp_pack_bulk_crc, kBcSmem)) return FP_ECUDA;
+  const int sms = sm_count(-1);
+  const int grid = (int)std::min<uint32_t>(n_tiles, (uint32_t)std::min(ctas > 0 ? ctas : sms, sms));
+  fp_pack_bulk_crc<<<grid, kBcThreads, kBcSmem, (cudaStream_t)stream>>>(
+      d_items, d_tile_lo, n_tiles, gbytes, d_slab, d_tabs, d_page_crc);
   return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
 }
 

@@ -221,11 +221,13 @@ int fp_ctx::save_shard() {
   const bool gpu_crc = want_crc && !host && !slabless && S % 4096 == 0 && d_crc_tabs;
   const uint64_t PPS = S / 4096;  // pages per slot
   xcrc.reset(plan.extents);
-  // default: fp_pack_v4, then fp_crc_pages_tma over the slab; FP_CRC_FUSED=1
-  // computes the page CRCs inside the pack (fp_pack_crc, ablation: measured
-  // slower)
-  const bool fused = gpu_crc && cfg.pack_impl == FP_PACK_V4 && getenv("FP_CRC_FUSED") &&
-                     !group_tile_off.empty();
+  // FP_PACK_V4: fp_pack_v4, then fp_crc_pages_tma over the slab;
+  // FP_PACK_BULK: fp_pack_bulk_crc computes the page CRCs from its shared-
+  // memory stages (one pass); FP_CRC_FUSED=1 with v4: fp_pack_crc (LSU
+  // fused ablation)
+  const bool bulk_crc = gpu_crc && cfg.pack_impl == FP_PACK_BULK && !group_tile_off.empty();
+  const bool fused = bulk_crc || (gpu_crc && cfg.pack_impl == FP_PACK_V4 &&
+                                  getenv("FP_CRC_FUSED") && !group_tile_off.empty());
   auto stage = [&](uint64_t c) -> int {
     const uint32_t s = (uint32_t)(c % R);
     const uint64_t len = std::min<uint64_t>(S, plan.shard_bytes - c * S);
@@ -288,7 +290,11 @@ int fp_ctx::save_shard() {
       // the gate is opened on every path out of this block: a stream left
       // waiting on it would never drain
       int r = cudaEventRecord(ev_p0[s], stream) == cudaSuccess ? 0 : FP_ECUDA;
-      if (!r && fused)  // pack + page CRCs in one pass over the data
+      if (!r && bulk_crc)  // TMA pack + page CRCs from the stages, one pass
+        r = pack_bulk_crc_launch(d_items + item_lo[c], d_tiles + group_tile_off[c / G],
+                                 (uint32_t)((gbytes + kTile - 1) / kTile), gbytes, d_slab,
+                                 d_crc_tabs, d_page_crc, pack_ctas, stream);
+      else if (!r && fused)  // pack + page CRCs in one pass over the data
         r = pack_crc_launch(d_items + item_lo[c], d_tiles + group_tile_off[c / G],
                             (uint32_t)((gbytes + kTile - 1) / kTile), d_slab,
                             (uint32_t)(round_up(gbytes, 4096) / 4096), d_crc_tabs, d_page_crc,
