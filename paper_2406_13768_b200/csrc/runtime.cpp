@@ -305,7 +305,7 @@ int fp_ctx::save_shard() {
       if (!r && cudaEventRecord(ev_p1[s], stream) != cudaSuccess) r = FP_ECUDA;
       if (!r && gpu_crc && !fused)
         r = crc_pages_launch(d_slab, round_up(gbytes, 4096), d_crc_tabs, d_page_crc, stream);
-      if (!r && gpu_crc && cudaEventRecord(ev_c1[s], stream) != cudaSuccess) r = FP_ECUDA;
+      if (!r && gpu_crc && !fused && cudaEventRecord(ev_c1[s], stream) != cudaSuccess) r = FP_ECUDA;
       if (gated) __atomic_store_n(&h_sig[0], ++gate_seq, __ATOMIC_RELEASE);  // open the gate
       if (r) return r;
       has_pack[s] = 1;
@@ -330,7 +330,7 @@ int fp_ctx::save_shard() {
       if (has_pack[s] && cudaEventElapsedTime(&a, ev_p0[s], ev_p1[s]) == cudaSuccess)
         st.pack_ms += a;
       float cm = 0;
-      if (has_pack[s] && gpu_crc && cudaEventElapsedTime(&cm, ev_p1[s], ev_c1[s]) == cudaSuccess)
+      if (has_pack[s] && gpu_crc && !fused && cudaEventElapsedTime(&cm, ev_p1[s], ev_c1[s]) == cudaSuccess)
         st.crc_ms += cm;
       if (cudaEventElapsedTime(&b, ev_d0[s], ev_d2h[s]) == cudaSuccess) st.d2h_ms += b;
     }
