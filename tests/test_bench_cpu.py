@@ -11,7 +11,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def test_reference_arm_json_line(tmp_path):
     env = dict(os.environ, FP_BENCH_DIR=str(tmp_path))
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
-                          "--steps", "1", "--warmup", "1", "--oracle-bytes", "2e7"],
+                          "--steps", "1", "--warmup", "1", "--ref-bytes", "2e7"],
                          capture_output=True, text=True, env=env, timeout=600)
     assert out.returncode == 0, out.stderr
     lines = [ln for ln in out.stdout.splitlines() if ln.strip()]
