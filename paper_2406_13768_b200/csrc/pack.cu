@@ -379,6 +379,39 @@ __device__ __forceinline__ uint32_t lanes_combine(uint32_t c, const uint32_t (&k
   return c;  // valid in every lane
 }
 
+// Product by a COMPILE-TIME constant x^(8*kBytes) (reflected): the 32 values
+// K*x^i are immediates, so the product is 32 predicated XORs of constants —
+// no registers held, no table lookups. Used to join two independent chains
+// of a lane (words 0..15 and 16..31: R = R0 * x^(8*64) ^ R1), which halves
+// the dependent-lookup latency of a page.
+constexpr uint32_t ce_gf_mul(uint32_t a, uint32_t b) {
+  uint32_t p = 0;
+  for (uint32_t m = 1u << 31; m; m >>= 1) {
+    if (a & m) p ^= b;
+    b = (b & 1) ? (b >> 1) ^ kPolyRefl : b >> 1;
+  }
+  return p;
+}
+constexpr uint32_t ce_x8n(uint64_t n) {  // x^(8n) mod P
+  uint32_t r = 1u << 31, sq = 1u << 23;  // x^0; x^8
+  for (; n; n >>= 1) {
+    if (n & 1) r = ce_gf_mul(r, sq);
+    sq = ce_gf_mul(sq, sq);
+  }
+  return r;
+}
+template <uint32_t K>
+__device__ __forceinline__ uint32_t gf_mul_const(uint32_t a) {
+  uint32_t p = 0, k = K;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    p ^= (0u - ((a >> (31 - i)) & 1u)) & k;
+    k = (k >> 1) ^ ((k & 1) ? kPolyRefl : 0u);  // folded to immediates (K is constexpr)
+  }
+  return p;
+}
+constexpr uint32_t kX64 = ce_x8n(64);  // x^(8*64): joins a lane's two 64-B chains
+
 // Raw CRC of one 4 KiB page held by a warp, lane l owning bytes
 // [128 l, 128 l + 128) as v[0..7]: one slicing-by-4 chain of 32 words per
 // lane through per-lane (bank-private) copies of the 4 tables (entry e of
@@ -389,16 +422,20 @@ __device__ __forceinline__ uint32_t page_crc_warp(const uint4 (&v)[8], const uin
   const uint32_t* r1 = rep + 256 * 32 + lane;
   const uint32_t* r2 = rep + 2 * 256 * 32 + lane;
   const uint32_t* r3 = rep + 3 * 256 * 32 + lane;
-  uint32_t c = 0;
+  uint32_t c0 = 0, c1 = 0;  // words 0..15 and 16..31: two independent chains
 #pragma unroll
-  for (int q = 0; q < 32; ++q) {
-    const uint4& vv = v[q >> 2];
-    const uint32_t w = (q & 3) == 0 ? vv.x : (q & 3) == 1 ? vv.y : (q & 3) == 2 ? vv.z : vv.w;
-    const uint32_t x = c ^ w;
-    c = r3[(x & 255) << 5] ^ r2[((x >> 8) & 255) << 5] ^ r1[((x >> 16) & 255) << 5] ^
-        r0[(x >> 24) << 5];
+  for (int q = 0; q < 16; ++q) {
+    const uint4& va = v[q >> 2];
+    const uint4& vb = v[4 + (q >> 2)];
+    const uint32_t wa = (q & 3) == 0 ? va.x : (q & 3) == 1 ? va.y : (q & 3) == 2 ? va.z : va.w;
+    const uint32_t wb = (q & 3) == 0 ? vb.x : (q & 3) == 1 ? vb.y : (q & 3) == 2 ? vb.z : vb.w;
+    const uint32_t xa = c0 ^ wa, xb = c1 ^ wb;
+    c0 = r3[(xa & 255) << 5] ^ r2[((xa >> 8) & 255) << 5] ^ r1[((xa >> 16) & 255) << 5] ^
+         r0[(xa >> 24) << 5];
+    c1 = r3[(xb & 255) << 5] ^ r2[((xb >> 8) & 255) << 5] ^ r1[((xb >> 16) & 255) << 5] ^
+         r0[(xb >> 24) << 5];
   }
-  return lanes_combine(c, kv);
+  return lanes_combine(gf_mul_const<kX64>(c0) ^ c1, kv);
 }
 
 __global__ void __launch_bounds__(kCrcThreads, 1)
@@ -499,16 +536,20 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
       v[u] = *reinterpret_cast<const uint4*>(row + ((u ^ (lane & 7)) << 4));
     __syncwarp();
     if (lane == 0) issue(k + 1);  // every lane has its copy of this page
-    // one chain of 32 words per lane; 16 warps per SM supply the parallelism
-    uint32_t c = 0;
+    // two independent chains per lane (words 0..15, 16..31), joined by a
+    // compile-time constant product
+    uint32_t c0 = 0, c1 = 0;
 #pragma unroll
-    for (int q = 0; q < 32; ++q) {
-      const uint4& vv = v[q >> 2];
-      const uint32_t wd = (q & 3) == 0 ? vv.x : (q & 3) == 1 ? vv.y : (q & 3) == 2 ? vv.z : vv.w;
-      const uint32_t x = c ^ wd;
-      c = lk(x, 0, 3) ^ lk(x, 1, 2) ^ lk(x, 2, 1) ^ lk(x, 3, 0);
+    for (int q = 0; q < 16; ++q) {
+      const uint4& va = v[q >> 2];
+      const uint4& vb = v[4 + (q >> 2)];
+      const uint32_t wa = (q & 3) == 0 ? va.x : (q & 3) == 1 ? va.y : (q & 3) == 2 ? va.z : va.w;
+      const uint32_t wb = (q & 3) == 0 ? vb.x : (q & 3) == 1 ? vb.y : (q & 3) == 2 ? vb.z : vb.w;
+      const uint32_t xa = c0 ^ wa, xb = c1 ^ wb;
+      c0 = lk(xa, 0, 3) ^ lk(xa, 1, 2) ^ lk(xa, 2, 1) ^ lk(xa, 3, 0);
+      c1 = lk(xb, 0, 3) ^ lk(xb, 1, 2) ^ lk(xb, 2, 1) ^ lk(xb, 3, 0);
     }
-    const uint32_t cl = lanes_combine(c, kv);
+    const uint32_t cl = lanes_combine(gf_mul_const<kX64>(c0) ^ c1, kv);
     if (lane == 0) out[pg] = cl;
   }
 }
@@ -722,17 +763,20 @@ __global__ void __launch_bounds__(kBcThreads, 1)
             for (int u = 0; u < 8; ++u) v[u] = w[u];
           }
         }
-        uint32_t c = 0;
-#pragma unroll
-        for (int q = 0; q < 32; ++q) {
-          const uint4& vv = v[q >> 2];
-          const uint32_t wd = (q & 3) == 0 ? vv.x : (q & 3) == 1 ? vv.y : (q & 3) == 2 ? vv.z : vv.w;
-          const uint32_t x = c ^ wd;
-          c = lk(x, 0, 3) ^ lk(x, 1, 2) ^ lk(x, 2, 1) ^ lk(x, 3, 0);
-        }
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&empty[s]));  // the page is in registers
-        c = lanes_combine(c, kv);
+        uint32_t c0 = 0, c1 = 0;  // two independent chains per lane (ILP)
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const uint4& va = v[q >> 2];
+          const uint4& vb = v[4 + (q >> 2)];
+          const uint32_t wa = (q & 3) == 0 ? va.x : (q & 3) == 1 ? va.y : (q & 3) == 2 ? va.z : va.w;
+          const uint32_t wb = (q & 3) == 0 ? vb.x : (q & 3) == 1 ? vb.y : (q & 3) == 2 ? vb.z : vb.w;
+          const uint32_t xa = c0 ^ wa, xb = c1 ^ wb;
+          c0 = lk(xa, 0, 3) ^ lk(xa, 1, 2) ^ lk(xa, 2, 1) ^ lk(xa, 3, 0);
+          c1 = lk(xb, 0, 3) ^ lk(xb, 1, 2) ^ lk(xb, 2, 1) ^ lk(xb, 3, 0);
+        }
+        const uint32_t c = lanes_combine(gf_mul_const<kX64>(c0) ^ c1, kv);
         if (lane == 0) page_crc[pg] = c;
       } else {
         __syncwarp();

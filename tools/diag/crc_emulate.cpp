@@ -23,8 +23,13 @@ int main() {
       uint32_t crc = 0;
       for (int lane = 0; lane < 32; ++lane) {
         const uint32_t* w = (const uint32_t*)(buf.data() + (size_t)pg * 4096 + lane * 128);
-        uint32_t c = 0;
-        for (int q = 0; q < 32; ++q) { uint32_t x = c ^ w[q]; c = t3[x & 255] ^ t2[(x >> 8) & 255] ^ t1[(x >> 16) & 255] ^ t0[x >> 24]; }
+        // two chains (words 0..15, 16..31) joined by x^(8*64), as the kernels do
+        uint32_t c0 = 0, c1 = 0;
+        for (int q = 0; q < 16; ++q) {
+          uint32_t x = c0 ^ w[q]; c0 = t3[x & 255] ^ t2[(x >> 8) & 255] ^ t1[(x >> 16) & 255] ^ t0[x >> 24];
+          x = c1 ^ w[16 + q]; c1 = t3[x & 255] ^ t2[(x >> 8) & 255] ^ t1[(x >> 16) & 255] ^ t0[x >> 24];
+        }
+        const uint32_t c = gf_mul(c0, gf_x8n(64)) ^ c1;
         uint32_t kv[32];
         kv[0] = T[kTabLaneK + lane];
         for (int i = 1; i < 32; ++i) kv[i] = (kv[i - 1] >> 1) ^ ((kv[i - 1] & 1) ? 0xEDB88320u : 0u);
