@@ -28,6 +28,8 @@
 #include <atomic>
 #include <cerrno>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "fp_internal.h"
@@ -554,6 +556,101 @@ __global__ void __launch_bounds__(kCtWarps * 32, 1)
   }
 }
 
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+// fp_crc_pages_col: a LANE owns a whole page, so no lane combine at all (the
+// combine products were ~45 % of fp_crc_pages_tma's ALU work). The slab is a
+// 2-D tensor map of pages (rows of 4096 B); one TMA box = the k-th 128-B
+// column of 32 consecutive pages (4 KiB, 128-B swizzle, so lane r reading
+// its row's 16-B chunk c at c ^ (r & 7) is conflict-free). Each of the 16
+// warps walks groups of 32 pages column by column, copies the box to
+// registers, issues the next box into its stage and advances 32 pages' CRC
+// chains by 32 words each; after 32 columns lane r holds page r's raw CRC.
+constexpr int kColWarps = 16;
+constexpr size_t kColSmem = kCtTabBytes + 256 + 1024 + (size_t)kColWarps * 4096;
+
+__global__ void __launch_bounds__(kColWarps * 32, 1)
+    fp_crc_pages_col(const __grid_constant__ CUtensorMap tmap, uint32_t n_pages,
+                     const uint32_t* __restrict__ tabs, uint32_t* __restrict__ out) {
+  extern __shared__ __align__(16) uint8_t cc_raw[];
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(cc_raw + kCtTabBytes);
+  uint8_t* stages = reinterpret_cast<uint8_t*>(
+      ((uintptr_t)(cc_raw + kCtTabBytes + 256) + 1023) & ~(uintptr_t)1023);
+  for (int i = threadIdx.x; i < 4 * 256 * 32; i += blockDim.x) {
+    const int k = i >> 13, e = (i >> 5) & 255, l = i & 31;
+    *reinterpret_cast<uint32_t*>(cc_raw + (k >> 1) * 65536 + e * 256 + (k & 1) * 128 + l * 4) =
+        tabs[kTabS4 + k * 256 + e];
+  }
+  if (threadIdx.x < kColWarps) mbar_init(&mbar[threadIdx.x], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t lane4 = (uint32_t)lane * 4;
+  const uint32_t n_groups = (n_pages + 31) / 32;
+  const uint32_t gw = blockIdx.x * kColWarps + (uint32_t)w, nw = gridDim.x * kColWarps;
+  uint8_t* stage = stages + (size_t)w * 4096;
+  const uint32_t bar = smem_u32(&mbar[w]);
+  // box number b = (group index i of this warp) * 32 + column k
+  auto issue = [&](uint32_t b) {
+    const uint32_t g = gw + (b >> 5) * nw;
+    if (g >= n_groups) return;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_arrive_tx(bar, 4096);
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(stage)),
+        "l"(reinterpret_cast<uint64_t>(&tmap)), "r"((b & 31) * 128), "r"(g * 32), "r"(bar)
+        : "memory");
+  };
+  auto lk = [&](uint32_t x, const int b, const int t) -> uint32_t {
+    const uint32_t r = __byte_perm(x, lane4, 4u | ((uint32_t)b << 4) | (5u << 8) | (5u << 12));
+    return *reinterpret_cast<const uint32_t*>(cc_raw + r + ((t >> 1) * 65536 + (t & 1) * 128));
+  };
+  if (lane == 0) issue(0);
+  uint32_t c = 0;
+  for (uint32_t b = 0;; ++b) {
+    const uint32_t g = gw + (b >> 5) * nw;
+    if (g >= n_groups) break;
+    mbar_wait(bar, b & 1);
+    const uint8_t* row = stage + lane * 128;
+    uint4 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      v[u] = *reinterpret_cast<const uint4*>(row + ((u ^ (lane & 7)) << 4));
+    __syncwarp();
+    if (lane == 0) issue(b + 1);  // every lane has its 128 B of this column
+    if ((b & 31) == 0) c = 0;     // a new group of 32 pages starts
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const uint4& vv = v[q >> 2];
+      const uint32_t wd = (q & 3) == 0 ? vv.x : (q & 3) == 1 ? vv.y : (q & 3) == 2 ? vv.z : vv.w;
+      const uint32_t x = c ^ wd;
+      c = lk(x, 0, 3) ^ lk(x, 1, 2) ^ lk(x, 2, 1) ^ lk(x, 3, 0);
+    }
+    if ((b & 31) == 31 && g * 32 + (uint32_t)lane < n_pages) out[g * 32 + lane] = c;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // fp_pack_bulk_crc: the TMA-engine pack and the page CRCs in ONE pass (SURVEY
 // f4 "per-shard checksum fused into the pack kernel"). Work unit: one 32 KiB
@@ -580,28 +677,6 @@ constexpr int kBcLsuWarps = 2;
 constexpr int kBcCrcWarps = kTile / 4096;  // 8: one page each
 constexpr int kBcThreads = 32 * (1 + kBcLsuWarps + kBcCrcWarps);
 constexpr size_t kBcSmem = kCtTabBytes + (size_t)kBcStages * kTile + 128;
-
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-               : "memory");
-}
 
 // generic-proxy copy of `len` bytes into shared memory (src == nullptr: zeros)
 __device__ __forceinline__ void copy_to_smem(uint8_t* dst, const uint8_t* __restrict__ src,
@@ -951,6 +1026,11 @@ __global__ void fp_wait_flag(const uint32_t* __restrict__ flag, uint32_t value, 
   }
 }
 
+bool env_flag(const char* k) {
+  const char* v = getenv(k);
+  return v && *v && strcmp(v, "0") != 0;
+}
+
 int sm_count(int device) {
   int d = device;
   if (d < 0 && cudaGetDevice(&d) != cudaSuccess) return 148;
@@ -1006,7 +1086,8 @@ int flag_wait_launch(const uint32_t* d_flag, uint32_t value, uint64_t max_ns,
 // 2-D tensor map of d_buf as rows of 128 B, box = one 4 KiB page (32 rows),
 // 128-B swizzle. false if the driver entry point is unavailable or FP_NO_TMA=1
 // (then the LSU kernel fp_crc_pages runs: 1.6x slower)
-static bool encode_page_map(CUtensorMap* m, const uint8_t* d_buf, uint64_t bytes) {
+static bool encode_page_map(CUtensorMap* m, const uint8_t* d_buf, uint64_t bytes,
+                            bool columns) {
   using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -1023,8 +1104,10 @@ static bool encode_page_map(CUtensorMap* m, const uint8_t* d_buf, uint64_t bytes
       fn = reinterpret_cast<Encode>(p);
   });
   if (!fn || ((uintptr_t)d_buf & 15) || bytes / 128 > (1ull << 32)) return false;
-  const cuuint64_t dims[2] = {128, bytes / 128};
-  const cuuint64_t strides[1] = {128};
+  // rows: 128-B lines (box = one page) or whole pages (box = a 128-B column
+  // of 32 pages)
+  const cuuint64_t dims[2] = {columns ? 4096u : 128u, columns ? bytes / 4096 : bytes / 128};
+  const cuuint64_t strides[1] = {columns ? 4096u : 128u};
   const cuuint32_t box[2] = {128, 32};
   const cuuint32_t es[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(d_buf), dims, strides, box,
@@ -1039,7 +1122,13 @@ int crc_pages_launch(const uint8_t* d_buf, uint64_t bytes, const uint32_t* d_tab
   cudaStream_t st = (cudaStream_t)stream;
   const uint32_t n_pages = (uint32_t)(bytes / 4096);
   CUtensorMap tmap;
-  if (encode_page_map(&tmap, d_buf, bytes)) {
+  static const bool rows = env_flag("FP_CRC_ROWS");  // ablation: lane = 128-B row of a page
+  if (!rows && encode_page_map(&tmap, d_buf, bytes, true)) {
+    if (!smem_opt_in<5>(fp_crc_pages_col, kColSmem)) return FP_ECUDA;
+    const int grid = (int)std::min<uint32_t>((n_pages + 32 * kColWarps - 1) / (32 * kColWarps),
+                                             (uint32_t)sm_count(-1));
+    fp_crc_pages_col<<<grid, kColWarps * 32, kColSmem, st>>>(tmap, n_pages, d_tabs, d_page_crc);
+  } else if (encode_page_map(&tmap, d_buf, bytes, false)) {
     if (!smem_opt_in<2>(fp_crc_pages_tma, kCtSmem)) return FP_ECUDA;
     const int grid = (int)std::min<uint32_t>((n_pages + kCtWarps - 1) / kCtWarps,
                                              (uint32_t)sm_count(-1));

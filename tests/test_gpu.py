@@ -518,10 +518,13 @@ def test_crc_fused_kernel_parity(tmp_path, monkeypatch, slot, pack_bytes):
     _check_rank_files(str(tmp_path), lay, 1)
 
 
-def test_crc_pages_lsu_fallback_parity(tmp_path, monkeypatch):
-    """FP_NO_TMA=1: the LSU page-CRC kernel (used when no tensor map can be
-    encoded) gives the same CRC-32 as the default TMA kernel and zlib. Runs in
-    a child process (the tensor-map entry point is resolved once per process)."""
+@pytest.mark.parametrize("env", ["FP_NO_TMA", "FP_CRC_ROWS"])
+def test_crc_pages_variant_parity(tmp_path, env):
+    """The other page-CRC kernels give the same CRC-32 as the default
+    (fp_crc_pages_col, a lane per page) and zlib: FP_NO_TMA=1, the LSU kernel
+    used when no tensor map can be encoded; FP_CRC_ROWS=1, the TMA kernel with
+    a lane per 128-B row and a register lane combine. Child processes (both
+    switches are read once per process)."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -533,7 +536,7 @@ def test_crc_pages_lsu_fallback_parity(tmp_path, monkeypatch):
             "ck=fp.Checkpointer(torch.device('cuda',0), slot_bytes=1<<20, pack_bytes=3<<20);"
             "s=ck.save(entries(st), d); ck.close(); assert s['crc_valid'];"
             "_check_rank_files(d, lay, 1); print('ok')")
-    env = dict(os.environ, FP_ROOT=root, PYTHONPATH=root, FP_NO_TMA="1")
+    env = dict(os.environ, FP_ROOT=root, PYTHONPATH=root, **{env: "1"})
     r = subprocess.run([sys.executable, "-c", code, str(tmp_path)], capture_output=True, text=True,
                        env=env, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-3000:]
