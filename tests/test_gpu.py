@@ -518,12 +518,12 @@ def test_crc_fused_kernel_parity(tmp_path, monkeypatch, slot, pack_bytes):
     _check_rank_files(str(tmp_path), lay, 1)
 
 
-@pytest.mark.parametrize("env", ["FP_NO_TMA", "FP_CRC_ROWS"])
+@pytest.mark.parametrize("env", ["FP_NO_TMA", "FP_CRC_COL"])
 def test_crc_pages_variant_parity(tmp_path, env):
     """The other page-CRC kernels give the same CRC-32 as the default
-    (fp_crc_pages_col, a lane per page) and zlib: FP_NO_TMA=1, the LSU kernel
-    used when no tensor map can be encoded; FP_CRC_ROWS=1, the TMA kernel with
-    a lane per 128-B row and a register lane combine. Child processes (both
+    (fp_crc_pages_tma, a lane per 128-B row of a page) and zlib: FP_NO_TMA=1,
+    the LSU kernel used when no tensor map can be encoded; FP_CRC_COL=1, the
+    TMA kernel with a lane per page (no lane combine). Child processes (both
     switches are read once per process)."""
     import subprocess
     import sys
