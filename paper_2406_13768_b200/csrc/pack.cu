@@ -587,7 +587,6 @@ __device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
 // registers, issues the next box into its stage and advances 32 pages' CRC
 // chains by 32 words each; after 32 columns lane r holds page r's raw CRC.
 constexpr int kColWarps = 16;
-constexpr uint32_t kColPf = 6;  // L2 prefetch distance, in boxes
 constexpr size_t kColSmem = kCtTabBytes + 256 + 1024 + (size_t)kColWarps * 4096;
 
 __global__ void __launch_bounds__(kColWarps * 32, 1)
@@ -611,18 +610,7 @@ __global__ void __launch_bounds__(kColWarps * 32, 1)
   const uint32_t gw = blockIdx.x * kColWarps + (uint32_t)w, nw = gridDim.x * kColWarps;
   uint8_t* stage = stages + (size_t)w * 4096;
   const uint32_t bar = smem_u32(&mbar[w]);
-  // box number b = (group index i of this warp) * 32 + column k. One box per
-  // warp sits in shared memory; the boxes kColPf ahead are prefetched into L2
-  // (no shared memory), so the box TMA finds its bytes in L2 instead of
-  // paying the DRAM latency with only 4 KiB in flight per warp.
-  auto prefetch = [&](uint32_t b) {
-    const uint32_t g = gw + (b >> 5) * nw;
-    if (g >= n_groups) return;
-    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
-                     reinterpret_cast<uint64_t>(&tmap)),
-                 "r"((b & 31) * 128), "r"(g * 32)
-                 : "memory");
-  };
+  // box number b = (group index i of this warp) * 32 + column k
   auto issue = [&](uint32_t b) {
     const uint32_t g = gw + (b >> 5) * nw;
     if (g >= n_groups) return;
@@ -633,16 +621,12 @@ __global__ void __launch_bounds__(kColWarps * 32, 1)
         " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(stage)),
         "l"(reinterpret_cast<uint64_t>(&tmap)), "r"((b & 31) * 128), "r"(g * 32), "r"(bar)
         : "memory");
-    prefetch(b + kColPf);
   };
   auto lk = [&](uint32_t x, const int b, const int t) -> uint32_t {
     const uint32_t r = __byte_perm(x, lane4, 4u | ((uint32_t)b << 4) | (5u << 8) | (5u << 12));
     return *reinterpret_cast<const uint32_t*>(cc_raw + r + ((t >> 1) * 65536 + (t & 1) * 128));
   };
-  if (lane == 0) {
-    for (uint32_t b = 1; b < kColPf; ++b) prefetch(b);
-    issue(0);
-  }
+  if (lane == 0) issue(0);
   uint32_t c = 0;
   for (uint32_t b = 0;; ++b) {
     const uint32_t g = gw + (b >> 5) * nw;
@@ -689,7 +673,6 @@ __global__ void __launch_bounds__(kColWarps * 32, 1)
 // longer re-reads it (the separate fp_crc_pages_tma pass: +1 B per byte).
 // ---------------------------------------------------------------------------
 constexpr int kBcStages = 3;
-constexpr uint32_t kBcPf = 3;  // L2 prefetch distance beyond the stages, in tiles
 constexpr int kBcLsuWarps = 2;
 constexpr int kBcCrcWarps = kTile / 4096;  // 8: one page each
 constexpr int kBcThreads = 32 * (1 + kBcLsuWarps + kBcCrcWarps);
@@ -777,23 +760,7 @@ __global__ void __launch_bounds__(kBcThreads, 1)
         }
       }
     };
-    // L2 prefetch of the items of tile i (bulk bodies), issued kBcPf tiles
-    // ahead of their G2S: the stages hold only 3 tiles, so without it the G2S
-    // of a refilled stage pays the full DRAM latency
-    auto prefetch = [&](uint32_t i) {
-      if (i >= nt) return;
-      const uint32_t t = tile_of(i);
-      for (uint32_t b = tile_lo[t]; b < tile_lo[t + 1]; b += 32) {
-        Item it = {0, 0, 0};
-        if (b + lane < tile_lo[t + 1]) it = items[b + lane];
-        if (b + lane < tile_lo[t + 1] && bulk_ok(it))
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(it.src),
-                       "r"(it.len & ~15u)
-                       : "memory");
-      }
-    };
     const uint32_t ahead = nt < (uint32_t)kBcStages ? nt : (uint32_t)kBcStages;
-    for (uint32_t i = kBcStages; i < kBcStages + kBcPf; ++i) prefetch(i);
     for (uint32_t i = 0; i < ahead; ++i) fill(i);
     for (uint32_t i = 0; i < nt; ++i) {
       const uint32_t s = i % kBcStages, t = tile_of(i), tl = tile_len(t);
@@ -816,7 +783,6 @@ __global__ void __launch_bounds__(kBcThreads, 1)
         mbar_wait(smem_u32(&empty[s]), (i / kBcStages) & 1);
         if (lane == 0) mbar_arrive(smem_u32(&freeb[s]));
         fill(i + kBcStages);
-        prefetch(i + kBcStages + kBcPf);
       }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
