@@ -489,7 +489,8 @@ def synthetic_overhead(a, ck, ents, state, dev, rank, world, path_of, image_gb, 
                                                   if x["eq1_hidden"]], default=None),
             "iters": a.overhead_iters, "warmup": a.overhead_warmup,
             "base_iters": a.overhead_base_iters, "pack_ctas": a.overlap_ctas,
-            "pack": a.overlap_pack, "sweep": out, "workload": CFG}
+            "pack": a.overlap_pack, "io_engine": a.overlap_io_engine or a.io_engine,
+            "sweep": out, "workload": CFG}
 
 
 def our_arm(a):
@@ -719,6 +720,8 @@ def our_arm(a):
             ovcfg = dict(cfg)
             ovcfg["pack_ctas"] = a.overlap_ctas
             ovcfg["pack"] = a.overlap_pack
+            if a.overlap_io_engine:
+                ovcfg["io_engine"] = a.overlap_io_engine
             with fp.Checkpointer(dev, **ovcfg) as cko:
                 overhead = synthetic_overhead(a, cko, ents, state, dev, rank, world, path_of,
                                               image_bytes / 1e9, gbs)
@@ -894,6 +897,9 @@ def main():
                     help="iterations without checkpointing per T_FB (deterministic GEMM loop)")
     ap.add_argument("--overlap-ctas", type=int, default=16)
     ap.add_argument("--overlap-pack", default="v4", choices=["v4", "bulk"])
+    ap.add_argument("--overlap-io-engine", default=None, choices=["uring", "null"],
+                    help="ablation: null = storage that completes at once (the GPU-side "
+                         "interference floor of the overlapped checkpoint)")
     ap.add_argument("--t-fb", type=float, default=0.0,
                     help="headline synthetic fwd+bwd seconds (0: FLOP-derived)")
     ap.add_argument("--t-fb-sweep", default="0.5,1,2,4",
