@@ -222,8 +222,9 @@ def numa_node_of(bdf):
 
 
 def nvme_mounts():
-    """Writable file systems on NVMe block devices: [(mountpoint, device,
-    sysfs PCI path of the controller)], from /proc/mounts."""
+    """Writable file systems on NVMe block devices or on md RAID over NVMe:
+    [(mountpoint, device, sysfs PCI path of the controller, "" for RAID)],
+    from /proc/mounts."""
     out, seen = [], set()
     try:
         lines = open("/proc/mounts").read().splitlines()
@@ -231,12 +232,22 @@ def nvme_mounts():
         return out
     for ln in lines:
         f = ln.split()
-        if len(f) < 4 or not f[0].startswith("/dev/nvme") or "rw" not in f[3].split(","):
+        if len(f) < 4 or "rw" not in f[3].split(","):
             continue
         dev = os.path.basename(f[0])
-        base = dev.split("p")[0] if "p" in dev[4:] else dev     # nvme0n1p2 -> nvme0n1
-        pci = os.path.realpath(f"/sys/block/{base}/device/device") \
-            if os.path.exists(f"/sys/block/{base}") else ""
+        if f[0].startswith("/dev/nvme"):
+            base = dev.split("p")[0] if "p" in dev[4:] else dev     # nvme0n1p2 -> nvme0n1
+            pci = os.path.realpath(f"/sys/block/{base}/device/device") \
+                if os.path.exists(f"/sys/block/{base}") else ""
+        elif f[0].startswith("/dev/md"):
+            # software RAID over NVMe (a DGX's /raid): no single PCIe home
+            slaves = os.listdir(f"/sys/block/{dev}/slaves") \
+                if os.path.isdir(f"/sys/block/{dev}/slaves") else []
+            if not any(x.startswith("nvme") for x in slaves):
+                continue
+            pci = ""
+        else:
+            continue
         if f[1] in seen or not os.access(f[1], os.W_OK):
             continue
         seen.add(f[1])
