@@ -892,6 +892,7 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
     rflags_bytes = round_up((uint64_t)k * std::max<uint64_t>(nrep, 1) * 4, 4096);
     if (ok && rank == 0) {  // created (zero-filled) before anyone learns its name
       const std::string nm = "/fpld." + std::to_string(getpid()) + "." + std::to_string(my_seq);
+      shm_unlink(nm.c_str());  // a stale segment of a crashed process with our pid
       const int sfd = shm_open(nm.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
       if (sfd < 0 || ftruncate(sfd, (off_t)rflags_bytes)) ok = 0;
       if (sfd >= 0) close(sfd);
