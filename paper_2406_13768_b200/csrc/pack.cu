@@ -664,19 +664,23 @@ __global__ void __launch_bounds__(kColWarps * 32, 1)
 //     LSU warps; L2 evict-first both ways.
 //   warps 1-2 (LSU): zero fill, misaligned items and <16 B tails straight
 //     into the stage (generic stores + proxy fence), then arrive on FULL.
-//   warps 3-10 (CRC): page p of the tile from the stage — lane l reads its
-//     128-B row with the 16-B chunks rotated by (l & 7) (conflict-free:
-//     a linear TMA row layout puts every lane's row in the same banks) and
-//     puts them back in order with a 3-level register barrel shift — one
-//     slicing-by-4 chain per lane, lanes_combine; arrive on EMPTY.
+//   warps 3.. (CRC): kGroups groups of 8 warps; group g takes the tiles
+//     i = g (mod kGroups) of this CTA, warp p of the group page p of the
+//     tile, from the stage — lane l reads its 128-B row with the 16-B chunks
+//     rotated by (l & 7) (conflict-free: a linear TMA row layout puts every
+//     lane's row in the same banks) and puts them back in order with a
+//     3-level register barrel shift — two slicing-by-4 chains per lane,
+//     lanes_combine; arrive on EMPTY. With one group (8 CRC warps) the page
+//     chains are latency-bound (the kernel ran at 0.79 of HBM); two groups
+//     keep two tiles' CRCs in flight per SM.
 // The slab is written and read once (2 B of HBM per image byte): the CRC no
 // longer re-reads it (the separate fp_crc_pages_tma pass: +1 B per byte).
 // ---------------------------------------------------------------------------
 constexpr int kBcStages = 3;
 constexpr int kBcLsuWarps = 2;
-constexpr int kBcCrcWarps = kTile / 4096;  // 8: one page each
-constexpr int kBcThreads = 32 * (1 + kBcLsuWarps + kBcCrcWarps);
-constexpr size_t kBcSmem = kCtTabBytes + (size_t)kBcStages * kTile + 128;
+constexpr int kBcCrcWarps = kTile / 4096;  // 8 per group: one page each
+constexpr int bc_threads(int groups) { return 32 * (1 + kBcLsuWarps + groups * kBcCrcWarps); }
+constexpr size_t kBcSmem = kCtTabBytes + (size_t)kBcStages * kTile + 128;  // + 13 mbarriers
 
 // generic-proxy copy of `len` bytes into shared memory (src == nullptr: zeros)
 __device__ __forceinline__ void copy_to_smem(uint8_t* dst, const uint8_t* __restrict__ src,
@@ -691,7 +695,8 @@ __device__ __forceinline__ void copy_to_smem(uint8_t* dst, const uint8_t* __rest
   for (uint32_t j = t; j < len; j += nthr) dst[j] = src ? src[j] : 0;
 }
 
-__global__ void __launch_bounds__(kBcThreads, 1)
+template <int kGroups>
+__global__ void __launch_bounds__(bc_threads(kGroups), 1)
     fp_pack_bulk_crc(const Item* __restrict__ items, const uint32_t* __restrict__ tile_lo,
                      uint32_t n_tiles, uint64_t gbytes, uint8_t* __restrict__ slab,
                      const uint32_t* __restrict__ tabs, uint32_t* __restrict__ page_crc) {
@@ -700,6 +705,7 @@ __global__ void __launch_bounds__(kBcThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(stages + (size_t)kBcStages * kTile);
   uint64_t* empty = full + kBcStages;
   uint64_t* freeb = empty + kBcStages;
+  uint64_t* cfull = freeb + kBcStages;  // [group][2]: tile j of a group is ready
   for (int i = threadIdx.x; i < 4 * 256 * 32; i += blockDim.x) {  // paired per-lane tables
     const int k = i >> 13, e = (i >> 5) & 255, l = i & 31;
     *reinterpret_cast<uint32_t*>(bc_raw + (k >> 1) * 65536 + e * 256 + (k & 1) * 128 + l * 4) =
@@ -711,6 +717,7 @@ __global__ void __launch_bounds__(kBcThreads, 1)
       mbar_init(&empty[s], kBcCrcWarps);
       mbar_init(&freeb[s], 1);
     }
+    for (int b = 0; b < 2 * kGroups; ++b) mbar_init(&cfull[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -722,50 +729,95 @@ __global__ void __launch_bounds__(kBcThreads, 1)
     return (uint32_t)(left < kTile ? left : kTile);
   };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // A tile's descriptors ({first item, end} from tile_lo, then one item per
+  // lane when the tile has <= 32 items — one item for most tiles of a
+  // model state) are loaded one stage cycle before they are needed, so the
+  // two dependent global loads are off the refill's critical path.
+  struct TileDesc {
+    uint32_t lo, hi;
+    Item it;  // item lo + lane, if any
+  };
+  auto load_bounds = [&](uint32_t i, TileDesc& d) {
+    d.lo = d.hi = 0;
+    if (i < nt) {
+      const uint32_t t = tile_of(i);
+      d.lo = tile_lo[t];
+      d.hi = tile_lo[t + 1];
+    }
+  };
+  auto load_item = [&](TileDesc& d) {
+    d.it = {0, 0, 0};
+    if (d.lo + lane < d.hi) d.it = items[d.lo + lane];
+  };
   if (warp == 0) {
     const uint64_t pol = evict_first_policy();
-    auto fill = [&](uint32_t i) {  // G2S of tile i's 16-B aligned item bodies
-      const uint32_t t = tile_of(i), s = i % kBcStages;
+    auto g2s = [&](uint8_t* st, const Item& mine, bool ok, uint32_t bar) {
+      uint32_t mask = __ballot_sync(0xffffffffu, ok && bulk_ok(mine));
+      while (mask) {
+        const int j = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const uint64_t src = __shfl_sync(0xffffffffu, mine.src, j);
+        const uint32_t dst = __shfl_sync(0xffffffffu, mine.dst, j);
+        const uint32_t len = __shfl_sync(0xffffffffu, mine.len, j);
+        if (lane == 0)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+              " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(st + (dst % kTile))),
+              "l"(src), "r"(len & ~15u), "r"(bar), "l"(pol)
+              : "memory");
+      }
+    };
+    auto fill = [&](uint32_t i, const TileDesc& d) {  // G2S of tile i's 16-B aligned item bodies
+      const uint32_t s = i % kBcStages;
       uint8_t* st = stages + (size_t)s * kTile;
-      const uint32_t lo = tile_lo[t], hi = tile_lo[t + 1];
+      const uint32_t bar = smem_u32(&full[s]);
+      const bool one = d.hi - d.lo <= 32;
       uint32_t total = 0;
-      for (uint32_t b = lo; b < hi; b += 32) {
-        Item it = {0, 0, 0};
-        if (b + lane < hi) it = items[b + lane];
-        total += (b + lane < hi && bulk_ok(it)) ? (it.len & ~15u) : 0u;
+      if (one) {
+        total = d.lo + lane < d.hi && bulk_ok(d.it) ? (d.it.len & ~15u) : 0u;
+      } else {
+        for (uint32_t b = d.lo; b < d.hi; b += 32) {
+          Item it = {0, 0, 0};
+          if (b + lane < d.hi) it = items[b + lane];
+          total += (b + lane < d.hi && bulk_ok(it)) ? (it.len & ~15u) : 0u;
+        }
       }
 #pragma unroll
       for (int o = 16; o; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
-      const uint32_t bar = smem_u32(&full[s]);
       if (lane == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive_tx(bar, total);
       }
-      for (uint32_t b = lo; b < hi; b += 32) {
-        Item mine = {0, 0, 0};
-        if (b + lane < hi) mine = items[b + lane];
-        uint32_t mask = __ballot_sync(0xffffffffu, b + lane < hi && bulk_ok(mine));
-        while (mask) {
-          const int j = __ffs(mask) - 1;
-          mask &= mask - 1;
-          const uint64_t src = __shfl_sync(0xffffffffu, mine.src, j);
-          const uint32_t dst = __shfl_sync(0xffffffffu, mine.dst, j);
-          const uint32_t len = __shfl_sync(0xffffffffu, mine.len, j);
-          if (lane == 0)
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-                " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(st + (dst % kTile))),
-                "l"(src), "r"(len & ~15u), "r"(bar), "l"(pol)
-                : "memory");
+      if (one) {
+        g2s(st, d.it, d.lo + lane < d.hi, bar);
+      } else {
+        for (uint32_t b = d.lo; b < d.hi; b += 32) {
+          Item mine = {0, 0, 0};
+          if (b + lane < d.hi) mine = items[b + lane];
+          g2s(st, mine, b + lane < d.hi, bar);
         }
       }
     };
     const uint32_t ahead = nt < (uint32_t)kBcStages ? nt : (uint32_t)kBcStages;
-    for (uint32_t i = 0; i < ahead; ++i) fill(i);
+    for (uint32_t i = 0; i < ahead; ++i) {
+      TileDesc d;
+      load_bounds(i, d);
+      load_item(d);
+      fill(i, d);
+    }
+    TileDesc nxt;  // tile i + kBcStages, items in flight
+    load_bounds(kBcStages, nxt);
+    load_item(nxt);
     for (uint32_t i = 0; i < nt; ++i) {
       const uint32_t s = i % kBcStages, t = tile_of(i), tl = tile_len(t);
       uint8_t* st = stages + (size_t)s * kTile;
+      TileDesc nn;  // tile i + kBcStages + 1: bounds in flight
+      load_bounds(i + kBcStages + 1, nn);
       mbar_wait(smem_u32(&full[s]), (i / kBcStages) & 1);
+      // hand tile i to its CRC group (a group must not test full[s] itself:
+      // with kGroups not dividing kBcStages, stage s's previous phase belongs
+      // to another group and a parity test cannot tell it from this one)
+      if (lane == 0) mbar_arrive(smem_u32(&cfull[(i % kGroups) * 2 + ((i / kGroups) & 1)]));
       const uint32_t body = tl & ~15u;
       if (lane == 0 && body) {
         asm volatile(
@@ -776,24 +828,43 @@ __global__ void __launch_bounds__(kBcThreads, 1)
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
       if ((uint32_t)lane < tl - body) slab[(uint64_t)t * kTile + body + lane] = st[body + lane];
+      // EMPTY of tile i is waited for even when the stage is not refilled:
+      // the CRC group's tile-ready slot of tile i + 2 * kGroups must not be
+      // signalled before the group has taken tile i (parity tests)
+      mbar_wait(smem_u32(&empty[s]), (i / kBcStages) & 1);
       if (i + kBcStages < nt) {
         // the stage is refilled once its S2G has read it and the CRC warps let go
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
-        mbar_wait(smem_u32(&empty[s]), (i / kBcStages) & 1);
         if (lane == 0) mbar_arrive(smem_u32(&freeb[s]));
-        fill(i + kBcStages);
+        fill(i + kBcStages, nxt);
       }
+      load_item(nn);
+      nxt = nn;
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   } else if (warp <= kBcLsuWarps) {
     const int t0 = threadIdx.x - 32, nthr = 32 * kBcLsuWarps;
+    TileDesc cur;
+    load_bounds(0, cur);
+    load_item(cur);
     for (uint32_t i = 0; i < nt; ++i) {
-      const uint32_t s = i % kBcStages, t = tile_of(i);
+      const uint32_t s = i % kBcStages;
       uint8_t* st = stages + (size_t)s * kTile;
+      TileDesc nn;
+      load_bounds(i + 1, nn);
       if (i >= (uint32_t)kBcStages) mbar_wait(smem_u32(&freeb[s]), (i / kBcStages - 1) & 1);
-      for (uint32_t k = tile_lo[t]; k < tile_lo[t + 1]; ++k) {
-        const Item it = items[k];
+      const bool one = cur.hi - cur.lo <= 32;
+      for (uint32_t k = cur.lo; k < cur.hi; ++k) {
+        Item it;
+        if (one) {
+          const int j = (int)(k - cur.lo);
+          it.src = __shfl_sync(0xffffffffu, cur.it.src, j);
+          it.dst = __shfl_sync(0xffffffffu, cur.it.dst, j);
+          it.len = __shfl_sync(0xffffffffu, cur.it.len, j);
+        } else {
+          it = items[k];
+        }
         const uint32_t off = it.dst % kTile;
         if (bulk_ok(it)) {
           const uint32_t body = it.len & ~15u;
@@ -806,9 +877,12 @@ __global__ void __launch_bounds__(kBcThreads, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the S2G
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&full[s]));
+      load_item(nn);
+      cur = nn;
     }
   } else {
-    const int p = warp - 1 - kBcLsuWarps;  // page of the tile
+    const int p = (warp - 1 - kBcLsuWarps) % kBcCrcWarps;  // page of the tile
+    const uint32_t grp = (uint32_t)(warp - 1 - kBcLsuWarps) / kBcCrcWarps;
     const uint32_t lane4 = (uint32_t)lane * 4, rot = (uint32_t)lane & 7;
     uint32_t kv[32];
     lane_k_init(tabs[kTabLaneK + lane], kv);
@@ -816,9 +890,13 @@ __global__ void __launch_bounds__(kBcThreads, 1)
       const uint32_t r = __byte_perm(x, lane4, 4u | ((uint32_t)b << 4) | (5u << 8) | (5u << 12));
       return *reinterpret_cast<const uint32_t*>(bc_raw + r + ((tb >> 1) * 65536 + (tb & 1) * 128));
     };
-    for (uint32_t i = 0; i < nt; ++i) {
+    // tile j of this group (i = grp + j * kGroups) is signalled on
+    // cfull[grp][j & 1], phase j / 2: the producer signals tile j + 2 only
+    // after it waited for this group's EMPTY of tile j, so no slot runs two
+    // phases ahead of its parity test
+    for (uint32_t i = grp, j = 0; i < nt; i += kGroups, ++j) {
       const uint32_t s = i % kBcStages, t = tile_of(i);
-      mbar_wait(smem_u32(&full[s]), (i / kBcStages) & 1);
+      mbar_wait(smem_u32(&cfull[grp * 2 + (j & 1)]), (j >> 1) & 1);
       const uint32_t pg = t * (kTile / 4096) + (uint32_t)p;
       const bool live = (uint64_t)pg * 4096 < gbytes;
       if (live) {
@@ -1148,11 +1226,19 @@ int pack_bulk_crc_launch(const Item* d_items, const uint32_t* d_tile_lo, uint32_
                          uint64_t gbytes, uint8_t* d_slab, const uint32_t* d_tabs,
                          uint32_t* d_page_crc, int ctas, void* stream) {
   if (!n_tiles) return 0;
-  if (!smem_opt_in<4>(fp_pack_bulk_crc, kBcSmem)) return FP_ECUDA;
   const int sms = sm_count(-1);
   const int grid = (int)std::min<uint32_t>(n_tiles, (uint32_t)std::min(ctas > 0 ? ctas : sms, sms));
-  fp_pack_bulk_crc<<<grid, kBcThreads, kBcSmem, (cudaStream_t)stream>>>(
-      d_items, d_tile_lo, n_tiles, gbytes, d_slab, d_tabs, d_page_crc);
+  // FP_BC_GROUPS=1: the 8-CRC-warp variant (ablation)
+  static const bool one = getenv("FP_BC_GROUPS") && !strcmp(getenv("FP_BC_GROUPS"), "1");
+  if (one) {
+    if (!smem_opt_in<6>(fp_pack_bulk_crc<1>, kBcSmem)) return FP_ECUDA;
+    fp_pack_bulk_crc<1><<<grid, bc_threads(1), kBcSmem, (cudaStream_t)stream>>>(
+        d_items, d_tile_lo, n_tiles, gbytes, d_slab, d_tabs, d_page_crc);
+  } else {
+    if (!smem_opt_in<4>(fp_pack_bulk_crc<2>, kBcSmem)) return FP_ECUDA;
+    fp_pack_bulk_crc<2><<<grid, bc_threads(2), kBcSmem, (cudaStream_t)stream>>>(
+        d_items, d_tile_lo, n_tiles, gbytes, d_slab, d_tabs, d_page_crc);
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
 }
 

@@ -115,6 +115,29 @@ def test_misaligned_and_degenerate_tensors(tmp_path, pack):
     _check_rank_files(str(tmp_path), lay, 1)
 
 
+@pytest.mark.parametrize("pack", ["v4", "bulk"])
+def test_many_small_tensors_align512(tmp_path, pack):
+    """Alignment 512 (P:475's example) and 700 small ragged tensors: a 32 KiB
+    slab tile then holds up to ~128 items (payloads, their < 16 B tails, zero
+    padding) — the > 32-items-per-tile paths of the pack kernels."""
+    g = torch.Generator(device=DEV).manual_seed(0xFA572406 + 512)
+    ents = []
+    for i in range(700):
+        n = int(torch.randint(1, 700, (1,)).item())
+        dt = (torch.float32, torch.bfloat16, torch.uint8)[i % 3]
+        t = torch.randint(0, 256, (n * torch.tensor([], dtype=dt).element_size(),),
+                          dtype=torch.uint8, device=DEV, generator=g).view(dt)
+        ents.append((f"t{i}", t, "other", -1))
+    from tests._util import otensor, DT
+    lay = fpck.Layout([otensor(n, t, sec, own, dtype=DT[t.dtype]) for n, t, sec, own in ents],
+                      align=512)
+    with fp.Checkpointer(DEV, pack=pack, alignment=512, slot_bytes=64 << 10,
+                         pack_bytes=256 << 10) as ck:
+        s = ck.save(ents, str(tmp_path))
+    assert s["pack_bytes"] == lay.image_bytes
+    _check_rank_files(str(tmp_path), lay, 1)
+
+
 @pytest.mark.parametrize("cfg,k", [("gpt3_small", 4), ("zero_small", 2), ("moe_small", 4),
                                    ("c1_tiny", 3)])
 def test_dp_ranks_on_one_gpu(tmp_path, cfg, k):
