@@ -695,7 +695,7 @@ __device__ __forceinline__ void copy_to_smem(uint8_t* dst, const uint8_t* __rest
   for (uint32_t j = t; j < len; j += nthr) dst[j] = src ? src[j] : 0;
 }
 
-template <int kGroups>
+template <int kGroups, bool kWarpStore>
 __global__ void __launch_bounds__(bc_threads(kGroups), 1)
     fp_pack_bulk_crc(const Item* __restrict__ items, const uint32_t* __restrict__ tile_lo,
                      uint32_t n_tiles, uint64_t gbytes, uint8_t* __restrict__ slab,
@@ -805,21 +805,28 @@ __global__ void __launch_bounds__(bc_threads(kGroups), 1)
       load_item(d);
       fill(i, d);
     }
-    TileDesc nxt;  // tile i + kBcStages, items in flight
+    // The producer runs one tile behind on the drain side: in iteration i it
+    // issues tile i's S2G and hands tile i to its CRC group, THEN reclaims
+    // the stage of tile i - 1 (its S2G read out, its CRC warps done) and
+    // refills it with tile i + 2. Waiting for tile i's own drain before
+    // moving on (the first design) put the producer -> CRC warps -> producer
+    // round trip and the S2G read of every tile in series (ncu: FULL was
+    // never waited on, EMPTY always).
+    TileDesc nxt;  // tile i + kBcStages - 1, items in flight
     load_bounds(kBcStages, nxt);
     load_item(nxt);
     for (uint32_t i = 0; i < nt; ++i) {
       const uint32_t s = i % kBcStages, t = tile_of(i), tl = tile_len(t);
       uint8_t* st = stages + (size_t)s * kTile;
-      TileDesc nn;  // tile i + kBcStages + 1: bounds in flight
-      load_bounds(i + kBcStages + 1, nn);
+      TileDesc nn;  // tile i + kBcStages: bounds in flight
+      if (i) load_bounds(i + kBcStages, nn);
       mbar_wait(smem_u32(&full[s]), (i / kBcStages) & 1);
       // hand tile i to its CRC group (a group must not test full[s] itself:
       // with kGroups not dividing kBcStages, stage s's previous phase belongs
       // to another group and a parity test cannot tell it from this one)
       if (lane == 0) mbar_arrive(smem_u32(&cfull[(i % kGroups) * 2 + ((i / kGroups) & 1)]));
       const uint32_t body = tl & ~15u;
-      if (lane == 0 && body) {
+      if (!kWarpStore && lane == 0 && body) {
         asm volatile(
             "cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
                 slab + (uint64_t)t * kTile),
@@ -827,22 +834,28 @@ __global__ void __launch_bounds__(bc_threads(kGroups), 1)
             : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
-      if ((uint32_t)lane < tl - body) slab[(uint64_t)t * kTile + body + lane] = st[body + lane];
-      // EMPTY of tile i is waited for even when the stage is not refilled:
-      // the CRC group's tile-ready slot of tile i + 2 * kGroups must not be
-      // signalled before the group has taken tile i (parity tests)
-      mbar_wait(smem_u32(&empty[s]), (i / kBcStages) & 1);
-      if (i + kBcStages < nt) {
-        // the stage is refilled once its S2G has read it and the CRC warps let go
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&freeb[s]));
-        fill(i + kBcStages, nxt);
+      if (!kWarpStore && (uint32_t)lane < tl - body)
+        slab[(uint64_t)t * kTile + body + lane] = st[body + lane];
+      if (i) {
+        // EMPTY of tile i - 1 is waited for even when its stage is not
+        // refilled: the CRC group's tile-ready slot of tile i - 1 + 2 *
+        // kGroups must not be signalled before the group has taken tile i - 1
+        const uint32_t p = i - 1, ps = p % kBcStages;
+        mbar_wait(smem_u32(&empty[ps]), (p / kBcStages) & 1);
+        if (p + kBcStages < nt) {
+          // tile i - 1's S2G has read the stage (tile i's may still be reading)
+          if (!kWarpStore && lane == 0)
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(smem_u32(&freeb[ps]));
+          fill(p + kBcStages, nxt);
+        }
+        load_item(nn);
+        nxt = nn;
       }
-      load_item(nn);
-      nxt = nn;
     }
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if (nt) mbar_wait(smem_u32(&empty[(nt - 1) % kBcStages]), ((nt - 1) / kBcStages) & 1);
+    if (!kWarpStore && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   } else if (warp <= kBcLsuWarps) {
     const int t0 = threadIdx.x - 32, nthr = 32 * kBcLsuWarps;
     TileDesc cur;
@@ -900,6 +913,33 @@ __global__ void __launch_bounds__(bc_threads(kGroups), 1)
       const uint32_t pg = t * (kTile / 4096) + (uint32_t)p;
       const bool live = (uint64_t)pg * 4096 < gbytes;
       if (live) {
+        if (kWarpStore) {
+          // the page to the slab from the stage, coalesced (512 B per warp
+          // instruction), before EMPTY: the stage is free as soon as its
+          // readers have it, with no S2G holding it while the write drains
+          const uint8_t* ps = stages + (size_t)s * kTile + (size_t)p * 4096;
+          uint8_t* pd = slab + (uint64_t)t * kTile + (size_t)p * 4096;
+          const uint32_t tl = tile_len(t), plen = tl - p * 4096 < 4096 ? tl - p * 4096 : 4096;
+          if (plen == 4096) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              uint4 x[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                x[u] = *reinterpret_cast<const uint4*>(ps + ((h * 4 + u) * 32 + lane) * 16);
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                st_v4(reinterpret_cast<uint4*>(pd) + (h * 4 + u) * 32 + lane, x[u]);
+            }
+          } else {
+            for (uint32_t q = lane; q * 16 < plen; q += 32) {
+              if (q * 16 + 16 <= plen)
+                st_v4(reinterpret_cast<uint4*>(pd) + q, *reinterpret_cast<const uint4*>(ps + q * 16));
+              else
+                for (uint32_t b = q * 16; b < plen; ++b) pd[b] = ps[b];
+            }
+          }
+        }
         const uint8_t* row = stages + (size_t)s * kTile + (size_t)p * 4096 + lane * 128;
         uint4 v[8];
 #pragma unroll
@@ -1228,17 +1268,24 @@ int pack_bulk_crc_launch(const Item* d_items, const uint32_t* d_tile_lo, uint32_
   if (!n_tiles) return 0;
   const int sms = sm_count(-1);
   const int grid = (int)std::min<uint32_t>(n_tiles, (uint32_t)std::min(ctas > 0 ? ctas : sms, sms));
-  // FP_BC_GROUPS=1: the 8-CRC-warp variant (ablation)
+  // ablations: FP_BC_GROUPS=1 (one group of 8 CRC warps); FP_BC_WARPSTORE=1
+  // (the CRC warps store the pages from the stage instead of one TMA S2G per
+  // tile: 112 vs 98 us per 256 MiB)
   static const bool one = getenv("FP_BC_GROUPS") && !strcmp(getenv("FP_BC_GROUPS"), "1");
-  if (one) {
-    if (!smem_opt_in<6>(fp_pack_bulk_crc<1>, kBcSmem)) return FP_ECUDA;
-    fp_pack_bulk_crc<1><<<grid, bc_threads(1), kBcSmem, (cudaStream_t)stream>>>(
-        d_items, d_tile_lo, n_tiles, gbytes, d_slab, d_tabs, d_page_crc);
-  } else {
-    if (!smem_opt_in<4>(fp_pack_bulk_crc<2>, kBcSmem)) return FP_ECUDA;
-    fp_pack_bulk_crc<2><<<grid, bc_threads(2), kBcSmem, (cudaStream_t)stream>>>(
-        d_items, d_tile_lo, n_tiles, gbytes, d_slab, d_tabs, d_page_crc);
-  }
+  static const bool s2g = !env_flag("FP_BC_WARPSTORE");
+  cudaStream_t st = (cudaStream_t)stream;
+#define FP_BC_LAUNCH(G, W, SLOT)                                                           \
+  do {                                                                                     \
+    if (!smem_opt_in<SLOT>(fp_pack_bulk_crc<G, W>, kBcSmem)) return FP_ECUDA;              \
+    fp_pack_bulk_crc<G, W><<<grid, bc_threads(G), kBcSmem, st>>>(d_items, d_tile_lo, n_tiles, \
+                                                                 gbytes, d_slab, d_tabs,      \
+                                                                 d_page_crc);                \
+  } while (0)
+  if (one && s2g) FP_BC_LAUNCH(1, false, 6);
+  else if (one) FP_BC_LAUNCH(1, true, 7);
+  else if (s2g) FP_BC_LAUNCH(2, false, 8);
+  else FP_BC_LAUNCH(2, true, 4);
+#undef FP_BC_LAUNCH
   return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
 }
 

@@ -1,7 +1,7 @@
 """Random-schedule model of the mbarrier protocol of fp_pack_bulk_crc
-(pack.cu): producer warp (TMA G2S fill, FULL wait, per-group tile hand-off,
-EMPTY wait, FREE), two LSU warps, kGroups groups of CRC warps. mbarrier
-semantics as PTX defines them: a phase completes when its pending arrivals
+(pack.cu): producer warp (TMA G2S fill, FULL wait, hand-off of tile i to
+its CRC group, then EMPTY wait + FREE + refill for tile i - 1), two LSU
+warps, kGroups groups of CRC warps. mbarrier semantics as PTX defines them: a phase completes when its pending arrivals
 and transaction bytes reach zero; try_wait.parity(P) succeeds iff the current
 phase's parity differs from P. The model checks that every schedule finishes
 (no deadlock) and that a CRC warp only ever reads the tile it was handed.
@@ -61,15 +61,23 @@ def run(nt, groups, warps, seed, old=False):
                 yield
             cfull[(i % groups) * 2 + ((i // groups) & 1)].arrive()
             yield
-            if not old:
-                while not empty[s].test((i // STAGES) & 1):
-                    yield
-            if i + STAGES < nt:
-                if old:
+            if old:             # first design: drain tile i, refill its stage
+                if i + STAGES < nt:
                     while not empty[s].test((i // STAGES) & 1):
                         yield
-                freeb[s].arrive()
-                fill(i + STAGES)
+                    freeb[s].arrive()
+                    fill(i + STAGES)
+                    yield
+            elif i:             # drain tile i - 1 behind tile i's hand-off
+                p = i - 1
+                while not empty[p % STAGES].test((p // STAGES) & 1):
+                    yield
+                if p + STAGES < nt:
+                    freeb[p % STAGES].arrive()
+                    fill(p + STAGES)
+                    yield
+        if not old and nt:
+            while not empty[(nt - 1) % STAGES].test(((nt - 1) // STAGES) & 1):
                 yield
 
     def lsu():
