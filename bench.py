@@ -884,7 +884,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--pack", default="v4", choices=["v4", "bulk", "host", "ce"])
+    ap.add_argument("--pack", default="bulk", choices=["v4", "bulk", "host", "ce"])
     ap.add_argument("--pack-mib", type=int, default=256)
     ap.add_argument("--prio", default="high", choices=["high", "low"])
     ap.add_argument("--writer-stride", type=int, default=1,
@@ -907,7 +907,7 @@ def main():
     ap.add_argument("--overhead-base-iters", type=int, default=3,
                     help="iterations without checkpointing per T_FB (deterministic GEMM loop)")
     ap.add_argument("--overlap-ctas", type=int, default=16)
-    ap.add_argument("--overlap-pack", default="v4", choices=["v4", "bulk"])
+    ap.add_argument("--overlap-pack", default="bulk", choices=["v4", "bulk"])
     ap.add_argument("--overlap-io-engine", default=None, choices=["uring", "null"],
                     help="ablation: null = storage that completes at once (the GPU-side "
                          "interference floor of the overlapped checkpoint)")

@@ -110,9 +110,13 @@ enum fp_io_engine { FP_IO_URING = 0,    /* io_uring, O_DIRECT, registered bufs *
                                            a slab pack (v4/bulk); loads and host
                                            state use io_uring.                   */ };
 enum fp_pack_impl { FP_PACK_V4 = 0,     /* LSU 16-B vector gather -> device slab,
-                                           then copy engine -> pinned ring       */
-                    FP_PACK_BULK = 1,   /* cp.async.bulk (TMA engine) via smem
-                                           -> device slab, then copy engine      */
+                                           then copy engine -> pinned ring; the
+                                           page CRCs by a second kernel over
+                                           the slab                              */
+                    FP_PACK_BULK = 1,   /* default: cp.async.bulk (TMA engine)
+                                           via smem -> device slab, the page
+                                           CRCs computed from the smem stages in
+                                           the same kernel; then copy engine     */
                     FP_PACK_HOST = 2,   /* fused: the v4 kernel stores straight
                                            into the mapped pinned ring slot
                                            (zero-copy D2H over PCIe, no slab)    */
@@ -144,7 +148,7 @@ typedef struct fp_config {
   uint32_t sqe_bytes;    /* bytes per write request; default 1 MiB               */
   uint32_t alignment;    /* power of two >= 512; default 4096           */
   uint32_t io_engine;    /* enum fp_io_engine; default FP_IO_URING              */
-  uint32_t pack_impl;    /* enum fp_pack_impl; default FP_PACK_V4               */
+  uint32_t pack_impl;    /* enum fp_pack_impl; default FP_PACK_BULK             */
   uint32_t pack_ctas;    /* 0 = whole GPU (burst); else CTA cap (background)    */
   uint32_t flags;        /* FP_CFG_*                                             */
   const char *dirs;      /* nullable: comma-separated roots; rank r's shard goes

@@ -737,11 +737,12 @@ int fp_config_default(fp_config* cfg) {
                    : !strcmp(e, "gds")      ? FP_IO_GDS
                                              : FP_IO_URING;
   const char* pk = getenv("FP_PACK");
-  cfg->pack_impl = !pk                   ? FP_PACK_V4
+  cfg->pack_impl = !pk                   ? FP_PACK_BULK
+                   : !strcmp(pk, "v4")   ? FP_PACK_V4
                    : !strcmp(pk, "bulk") ? FP_PACK_BULK
                    : !strcmp(pk, "host") ? FP_PACK_HOST
                    : !strcmp(pk, "ce")   ? FP_PACK_CE
-                                         : FP_PACK_V4;
+                                         : FP_PACK_BULK;
   cfg->dirs = getenv("FP_CKPT_DIRS");
   return 0;
 }

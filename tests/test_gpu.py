@@ -121,9 +121,9 @@ def test_many_small_tensors_align512(tmp_path, pack):
     slab tile then holds up to ~128 items (payloads, their < 16 B tails, zero
     padding) — the > 32-items-per-tile paths of the pack kernels."""
     g = torch.Generator(device=DEV).manual_seed(0xFA572406 + 512)
+    sizes = torch.randint(1, 700, (700,), generator=torch.Generator().manual_seed(512)).tolist()
     ents = []
-    for i in range(700):
-        n = int(torch.randint(1, 700, (1,)).item())
+    for i, n in enumerate(sizes):
         dt = (torch.float32, torch.bfloat16, torch.uint8)[i % 3]
         t = torch.randint(0, 256, (n * torch.tensor([], dtype=dt).element_size(),),
                           dtype=torch.uint8, device=DEV, generator=g).view(dt)
@@ -194,7 +194,7 @@ def test_producer_stream_fence(tmp_path):
 
 
 def test_c1_bench_launch_config(tmp_path):
-    """The configuration bench.py times (64 MiB slots x 4, v4, 1 MiB SQEs)."""
+    """The configuration bench.py times (64 MiB slots x 4, bulk pack + CRC, 1 MiB SQEs)."""
     st = _state("c1_tiny")
     lay = oracle_layout([st], 1)
     with fp.Checkpointer(DEV) as ck:
