@@ -211,6 +211,9 @@ typedef struct fp_load_stats {
                                writer's partition from its device buffer)      */
   int32_t  status;          /* return code of that load                           */
   double   t_exchange_wait; /* s the host waited for peers' chunks (exchange 2)    */
+  double   t_setup;         /* s from the call to the first chunk (manifest,
+                               plan, buffers, exchange setup)                    */
+  double   t_read_wait;     /* s the host waited for its own-shard reads          */
 } fp_load_stats;
 
 typedef struct fp_ctx fp_ctx;

@@ -1083,6 +1083,7 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
   });
   const double spin_s = (double)env_u64("FP_PEER_TIMEOUT_S", 600);
   bool peer_failed = false;
+  c->ld.t_setup = now_s() - t_call;
   uint64_t launches = 0;
   for (uint64_t j = 0; run && j < total_chunks; ++j) {  // every rank runs every exchange
     const bool is_rep = j < nrep;
@@ -1122,7 +1123,9 @@ int fp_ckpt_load_parallel(fp_ctx* c, const fp_tensor* t, size_t n, const char* p
           host_crc(slot);
       }
     } else {
+      const double t_r = now_s();
       int rr = status ? 0 : ra.wait(j);
+      c->ld.t_read_wait += now_s() - t_r;
       if (rr && !status) status = rr;  // keep exchanging so the peers are not left waiting
       if (check_crc && mylen && !gpu_crc && !status) host_crc(slot);
     }

@@ -104,7 +104,8 @@ class fp_stats(C.Structure):
 class fp_load_stats(C.Structure):
     _fields_ = [("bytes_read", C.c_uint64), ("kernel_launches", C.c_uint64),
                 ("t_total", C.c_double), ("exchange", C.c_int32), ("status", C.c_int32),
-                ("t_exchange_wait", C.c_double)]
+                ("t_exchange_wait", C.c_double), ("t_setup", C.c_double),
+                ("t_read_wait", C.c_double)]
 
 
 EXCHANGES = {0: "none", 1: "allgather_bytes", 2: "peer"}
