@@ -220,7 +220,7 @@ typedef struct fp_ctx fp_ctx;
 
 /* Fill *cfg with the defaults above (env overrides: FP_RING_SLOTS,
  * FP_SLOT_BYTES, FP_SQE_BYTES, FP_QD, FP_IO_ENGINE=uring|pwrite|buffered|null|gds,
- * FP_PACK=v4|bulk|host|ce, FP_PACK_PRIO=low, FP_PACK_CTAS, FP_ALIGN, FP_PACK_BYTES,
+ * FP_PACK=bulk|v4|host|ce, FP_PACK_PRIO=low, FP_PACK_CTAS, FP_ALIGN, FP_PACK_BYTES,
  * FP_WRITER_STRIDE, FP_CKPT_DIRS, FP_NO_CRC). Returns 0.
  * Read at run time (not part of fp_config): FP_NO_TMA=1 (LSU page-CRC kernel
  * instead of the TMA-staged one), FP_CRC_FUSED=1 (page CRCs inside the pack

@@ -36,6 +36,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-Wall", "-I", INCLUDE, "-I", CSRC]
+    common += os.environ.get("FP_NVCC_FLAGS", "").split()  # experiments (e.g. -DFP_BC_SKIP_CRC)
 
     def compile_one(src):
         obj = os.path.join(BUILD, src + ".o")

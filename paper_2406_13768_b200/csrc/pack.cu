@@ -958,6 +958,9 @@ __global__ void __launch_bounds__(bc_threads(kGroups), 1)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&empty[s]));  // the page is in registers
+#ifdef FP_BC_SKIP_CRC  // experiment: the pipeline without the CRC arithmetic
+        if (lane == 0) page_crc[pg] = v[0].x ^ v[7].w;
+#else
         uint32_t c0 = 0, c1 = 0;  // two independent chains per lane (ILP)
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
@@ -971,6 +974,7 @@ __global__ void __launch_bounds__(bc_threads(kGroups), 1)
         }
         const uint32_t c = lanes_combine(gf_mul_const<kX64>(c0) ^ c1, kv);
         if (lane == 0) page_crc[pg] = c;
+#endif
       } else {
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&empty[s]));

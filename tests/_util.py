@@ -137,13 +137,23 @@ class MirrorComm:
     """The collectives of ONE rank of a k-rank job, answered locally: every
     rank reports this rank's own facts. Exact for the BASELINE configs C3/C4
     (identical replicated lists; rank-local partitions of identical sizes and
-    name lengths), so one GPU can write rank r's true shard of a DP=8 job."""
+    name lengths), so one GPU can write rank r's true shard of a DP=8 job.
+    region_bytes: every rank's local-region size as the ORACLE lays it out —
+    substituted into the plan's 4-u64 fact all-gather (region bytes, local
+    count, replicated digest, replicated bytes; runtime.cpp ensure_plan) when
+    the ranks' local regions differ (C5: expert names of other ranks have
+    other lengths, so their region headers differ)."""
 
-    def __init__(self, rank, k):
+    def __init__(self, rank, k, region_bytes=None):
         self.rank, self.world = rank, k
+        self.region_bytes = region_bytes
 
     def allgather(self, vals):
-        return list(vals) * self.world
+        vals = list(vals)
+        if self.region_bytes is not None and len(vals) == 4:
+            assert vals[0] == self.region_bytes[self.rank], "library and oracle disagree"
+            return [x for q in range(self.world) for x in [self.region_bytes[q]] + vals[1:]]
+        return vals * self.world
 
     def allreduce_min(self, v):
         return v

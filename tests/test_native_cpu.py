@@ -612,3 +612,38 @@ def test_byte_balance_matches_oracle_and_loads(tmp_path, cfg, k, stride, engine)
     finally:
         for c in cks:
             c.close()
+
+
+
+@pytest.mark.parametrize("rank", [0, 5])
+def test_one_rank_of_k_with_mirror_comm_matches_oracle(tmp_path, rank):
+    """The harness of the full-size one-rank-of-8 GPU tests (C3/C4/C5 on one
+    GPU): a single rank whose collectives MirrorComm answers, given every
+    rank's local-region size as the oracle lays it out. Here, as in C5 (whose
+    other ranks' expert names have other lengths), the ranks' local-region
+    headers differ, so mirroring this rank's facts alone would shift the
+    region table of the global header."""
+    from tests._util import MirrorComm, otensor
+    k = 8
+    g = torch.Generator().manual_seed(77)
+    rep = [(f"rep{i}", torch.randint(0, 256, (5000 + 4096 * i,), dtype=torch.uint8, generator=g))
+           for i in range(3)]
+
+    def local_names(r):          # rank r's 40 local tensors, names 10 + 90*r bytes long
+        return [f"r{r}.{'e' * (90 * r)}.t{i:04d}" for i in range(40)]
+    own = [(n, torch.randint(0, 256, (3000 + i,), dtype=torch.uint8, generator=g))
+           for i, n in enumerate(local_names(rank))]
+    ents = [(n, t, "other", -1) for n, t in rep] + [(n, t, "exp_avg", rank) for n, t in own]
+
+    def ghost(r):
+        return [fpck.OTensor(n, "u8", "exp_avg", r, (3000 + i,), bytes(3000 + i))
+                for i, n in enumerate(local_names(r))]
+    lay = fpck.Layout([otensor(n, t, "other", -1, dtype="u8") for n, t in rep],
+                      [[otensor(n, t, "exp_avg", rank, dtype="u8") for n, t in own] if r == rank
+                       else ghost(r) for r in range(k)], k=k)
+    assert len({b for _, b in lay.regions}) > 1   # the case the region sizes are needed for
+    with fp.Checkpointer(None, comm=MirrorComm(rank, k, [b for _, b in lay.regions]),
+                         slot_bytes=1 << 20) as ck:
+        s = ck.save(ents, str(tmp_path))
+    assert s["image_bytes"] == lay.image_bytes
+    assert file_sha(tmp_path / fpck.shard_name(rank, k)) == fpck.shard_sha256(lay, rank)

@@ -23,6 +23,7 @@ ap.add_argument("--pack", default="v4")
 ap.add_argument("--dir", default="/dev/shm/fp_ab")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--tag", default="")
+ap.add_argument("--no-crc", action="store_true", help="pack only (bulk: fp_pack_bulk)")
 a = ap.parse_args()
 peak = 6538.3
 try:
@@ -36,7 +37,7 @@ st = make_state(config_specs(a.cfg), dev)
 ents = [(x.name, t, x.section, x.owner) for x, t in st]
 torch.cuda.synchronize()
 rows = []
-with fp.Checkpointer(dev, pack=a.pack, no_fsync=True) as ck:
+with fp.Checkpointer(dev, pack=a.pack, no_fsync=True, no_crc=a.no_crc) as ck:
     for i in range(a.reps + 1):
         s = ck.save(ents, a.dir)
         if i:
