@@ -232,7 +232,6 @@ def _one_rank_of_8_full_size(tmp_path, cfg, rank, need_bytes, tmpfs_ok=False):
     (MirrorComm answers its collectives exactly, see tests/_util.py), in the
     bench launch configuration; the whole shard's sha256 against the oracle
     streaming the same tensors."""
-    from tests._util import MirrorComm
     free = os.statvfs(str(tmp_path))
     if free.f_bavail * free.f_frsize < need_bytes * 1.2:
         shm = os.statvfs("/dev/shm") if os.path.isdir("/dev/shm") else None
@@ -242,13 +241,27 @@ def _one_rank_of_8_full_size(tmp_path, cfg, rank, need_bytes, tmpfs_ok=False):
         # back to buffered writes there; the bytes are what is checked)
         import tempfile
         tmp_path = tempfile.mkdtemp(prefix="fp_full_", dir="/dev/shm")
+    try:
+        _one_rank_body(tmp_path, cfg, rank, need_bytes)
+    finally:                 # pytest keeps tmp dirs: never leave a shard behind
+        import shutil
+        for f in os.listdir(str(tmp_path)):
+            if f.endswith(".fpck"):
+                os.remove(os.path.join(str(tmp_path), f))
+        if str(tmp_path).startswith("/dev/shm/"):
+            shutil.rmtree(str(tmp_path), ignore_errors=True)
+        torch.cuda.empty_cache()
+
+
+def _one_rank_body(tmp_path, cfg, rank, need_bytes):
+    from tests._util import MirrorComm
     torch.cuda.empty_cache()
     k = 8
     st = _state(cfg, rank, k)
     mine = [otensor(s, t, lazy=True) for s, t in st]
     if any(s.owner >= 0 for s, _ in st):
         # rank-local partitions: the other ranks' regions only fix offsets
-        # (same sizes and name lengths on every rank); their bytes are never read
+        # (their sizes come from the oracle's layout); their bytes are never read
         def ghost(r):
             return [fpck.OTensor(s.name, s.dtype, s.section, r, s.shape, lambda off, n: bytes(n))
                     for s in config_specs(cfg, r, k) if s.owner >= 0]
@@ -272,12 +285,6 @@ def _one_rank_of_8_full_size(tmp_path, cfg, rank, need_bytes, tmpfs_ok=False):
         c = zlib.crc32(b, c)
     assert s["shard_crc32"] == c
     assert file_sha(path) == h.hexdigest()
-    os.remove(path)          # pytest keeps tmp dirs: do not leave the shard on the disk
-    if str(tmp_path).startswith("/dev/shm/"):
-        import shutil
-        shutil.rmtree(str(tmp_path), ignore_errors=True)
-    del st
-    torch.cuda.empty_cache()
 
 
 @pytest.mark.slow
