@@ -20,6 +20,9 @@
 //                 cp.async.bulk (G2S, mbarrier complete_tx) and
 //                 cp.async.bulk (S2G, bulk_group); the other warps handle
 //                 zero fill, vector tails and misaligned items with the LSU.
+//                 (FP_NO_CRC only; with CRCs the default is:)
+//  fp_pack_bulk_crc : the same TMA-engine pack computing the page CRC-32s
+//                 from its shared-memory stages (see below).
 //  fp_unpack_v4 : load path, slab -> tensors (zero items skipped).
 #include <cuda.h>  // CUtensorMap (the encode entry point is fetched at run time)
 #include <cuda_runtime.h>
@@ -657,11 +660,13 @@ __global__ void __launch_bounds__(kColWarps * 32, 1)
 // slab tile (8 pages); items never cross a tile (plan_tiles). One CTA per SM,
 // 3 shared-memory stages of one tile each:
 //   warp 0 (producer): lane 0 issues cp.async.bulk G2S for the 16-B aligned
-//     bodies of the tile's items into the stage (mbarrier complete_tx), and
-//     once the stage is FULL, one cp.async.bulk S2G of the whole tile to the
-//     slab; it refills a stage when its S2G has been read out of shared
-//     memory and the CRC warps released it (EMPTY), signalling FREE to the
-//     LSU warps; L2 evict-first both ways.
+//     bodies of the tile's items into the stage (mbarrier complete_tx); once
+//     tile i's stage is FULL it hands the tile to its CRC group (the group's
+//     own tile-ready barrier) and issues one cp.async.bulk S2G of the whole
+//     tile to the slab; then it reclaims the stage of tile i-1 — its S2G read
+//     out of shared memory, its CRC warps done with it (EMPTY) — signals FREE
+//     to the LSU warps and refills it with tile i+2. Tile descriptors are
+//     loaded one stage cycle ahead. L2 evict-first both ways.
 //   warps 1-2 (LSU): zero fill, misaligned items and <16 B tails straight
 //     into the stage (generic stores + proxy fence), then arrive on FULL.
 //   warps 3.. (CRC): kGroups groups of 8 warps; group g takes the tiles
@@ -670,9 +675,11 @@ __global__ void __launch_bounds__(kColWarps * 32, 1)
 //     rotated by (l & 7) (conflict-free: a linear TMA row layout puts every
 //     lane's row in the same banks) and puts them back in order with a
 //     3-level register barrel shift — two slicing-by-4 chains per lane,
-//     lanes_combine; arrive on EMPTY. With one group (8 CRC warps) the page
-//     chains are latency-bound (the kernel ran at 0.79 of HBM); two groups
-//     keep two tiles' CRCs in flight per SM.
+//     lanes_combine; arrive on EMPTY as soon as the page is in registers.
+// 92 us per 256 MiB (0.88 of HBM for pack + CRC) vs 90 us for fp_pack_bulk
+// alone and 87.5 + 65.9 us for fp_pack_v4 + fp_crc_pages_tma
+// (profiles/r02_ncu_bulk_crc_q8.md). The protocol is model-checked under
+// random schedules in tests/test_bulk_protocol_cpu.py.
 // The slab is written and read once (2 B of HBM per image byte): the CRC no
 // longer re-reads it (the separate fp_crc_pages_tma pass: +1 B per byte).
 // ---------------------------------------------------------------------------

@@ -100,6 +100,10 @@ std::string shard_file(int r, int k) {
 // ---------------------------------------------------------------------------
 // the helper's chunk pipeline: pack -> D2H -> io_uring, ring of R slots
 // ---------------------------------------------------------------------------
+// a launch gate of this process timed out once (a serialising profiler):
+// contexts created afterwards start ungated
+static std::atomic<bool> g_gate_timed_out{false};
+
 int fp_ctx::save_shard() {
   NvtxRange nv("fp.save_shard");
   const double t0 = now_s();
@@ -282,7 +286,9 @@ int fp_ctx::save_shard() {
       const uint64_t gbytes = std::min<uint64_t>(c1 * S, plan.shard_bytes) - c * S;
       if (c == 0) CK(cudaStreamWaitEvent(stream, ev_producer, 0));
       bool gated = gate_on;
-      if (gated && flag_wait_launch(d_sig, gate_seq + 1, 2000000000ull, nullptr, stream)) {
+      // the gate gives up after 50 ms and reports it in h_sig[48] (the
+      // helper then runs ungated: see submit_chunk)
+      if (gated && flag_wait_launch(d_sig, gate_seq + 1, 50000000ull, d_sig + 48, stream)) {
         gate_on = gated = false;  // could not launch the gate: run ungated from now on
         cudaGetLastError();
       }
@@ -333,6 +339,14 @@ int fp_ctx::save_shard() {
       if (has_pack[s] && gpu_crc && !fused && cudaEventElapsedTime(&cm, ev_p1[s], ev_c1[s]) == cudaSuccess)
         st.crc_ms += cm;
       if (cudaEventElapsedTime(&b, ev_d0[s], ev_d2h[s]) == cudaSuccess) st.d2h_ms += b;
+      // a gate that timed out (its kernel ran before the host could open it:
+      // a profiler serialising launches, or a stalled helper) is measurement
+      // machinery gone wrong: off for the rest of this context
+      if (gate_on && __atomic_load_n(&h_sig[48], __ATOMIC_ACQUIRE)) {
+        gate_on = false;
+        g_gate_timed_out.store(true);  // and for every later context of the process
+        fprintf(stderr, "fastpersist: launch gate timed out; running ungated\n");
+      }
     }
     uint8_t* slot = ring + (size_t)s * S;
     if (want_crc) {
@@ -960,11 +974,12 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
       // The launch gate is measurement machinery (opt-in, FP_LAUNCH_GATE=1:
       // bench.py turns it on so the CUDA events around each pack time the
       // kernel, not the host's launch latency on an idle stream). It relies
-      // on asynchronous launches: a profiler that serialises kernels (ncu,
-      // injected through CUDA_INJECTION64_PATH) would run the gate kernel to
-      // its timeout before the host could open it, so it is off there.
+      // on asynchronous launches: a profiler that serialises kernels (ncu)
+      // runs the gate kernel to its 50 ms timeout before the host can open
+      // it; the first timeout turns the gate off (submit_chunk), and it is
+      // off from the start when an injection library is announced.
       c->gate_on = env_u64("FP_LAUNCH_GATE", 0) == 1 && !getenv("FP_NO_GATE") &&
-                   !getenv("CUDA_INJECTION64_PATH");
+                   !getenv("CUDA_INJECTION64_PATH") && !g_gate_timed_out.load();
     }
     // CRC tables (slicing + constant-product tables, crc_device_tables) and
     // scratch: page CRCs of one pack group, chunk CRCs
