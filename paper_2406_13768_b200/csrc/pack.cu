@@ -676,7 +676,7 @@ __global__ void __launch_bounds__(kColWarps * 32, 1)
 //     lane's row in the same banks) and puts them back in order with a
 //     3-level register barrel shift — two slicing-by-4 chains per lane,
 //     lanes_combine; arrive on EMPTY as soon as the page is in registers.
-// 92 us per 256 MiB (0.88 of HBM for pack + CRC) vs 90 us for fp_pack_bulk
+// 91 us per 256 MiB (0.90 of HBM for pack + CRC) vs 90 us for fp_pack_bulk
 // alone and 87.5 + 65.9 us for fp_pack_v4 + fp_crc_pages_tma
 // (profiles/r02_ncu_bulk_crc_q8.md). The protocol is model-checked under
 // random schedules in tests/test_bulk_protocol_cpu.py.
@@ -713,11 +713,6 @@ __global__ void __launch_bounds__(bc_threads(kGroups), 1)
   uint64_t* empty = full + kBcStages;
   uint64_t* freeb = empty + kBcStages;
   uint64_t* cfull = freeb + kBcStages;  // [group][2]: tile j of a group is ready
-  for (int i = threadIdx.x; i < 4 * 256 * 32; i += blockDim.x) {  // paired per-lane tables
-    const int k = i >> 13, e = (i >> 5) & 255, l = i & 31;
-    *reinterpret_cast<uint32_t*>(bc_raw + (k >> 1) * 65536 + e * 256 + (k & 1) * 128 + l * 4) =
-        tabs[kTabS4 + k * 256 + e];
-  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < kBcStages; ++s) {
       mbar_init(&full[s], 1 + kBcLsuWarps);
@@ -901,6 +896,21 @@ __global__ void __launch_bounds__(bc_threads(kGroups), 1)
       cur = nn;
     }
   } else {
+    // the CRC warps alone fill the paired per-lane tables (the producer's
+    // first loads are in flight meanwhile), then meet at named barrier 1:
+    // 128 KiB as 16-B chunks, consecutive lanes -> consecutive chunks
+    // (conflict-free); chunk c holds entry e of table k for 8 lanes, with
+    // (k >> 1) = c / 4096, e = (c / 16) % 256, (k & 1) = (c / 8) % 2
+    {
+      const int t = threadIdx.x - 32 * (1 + kBcLsuWarps), nthr = 32 * kGroups * kBcCrcWarps;
+#pragma unroll 4
+      for (int c = t; c < (int)(kCtTabBytes / 16); c += nthr) {
+        const int k = ((c >> 12) << 1) | ((c >> 3) & 1), e = (c >> 4) & 255;
+        const uint32_t v = tabs[kTabS4 + k * 256 + e];
+        *reinterpret_cast<uint4*>(bc_raw + (size_t)c * 16) = make_uint4(v, v, v, v);
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(32 * kGroups * kBcCrcWarps) : "memory");
+    }
     const int p = (warp - 1 - kBcLsuWarps) % kBcCrcWarps;  // page of the tile
     const uint32_t grp = (uint32_t)(warp - 1 - kBcLsuWarps) / kBcCrcWarps;
     const uint32_t lane4 = (uint32_t)lane * 4, rot = (uint32_t)lane & 7;
