@@ -27,6 +27,7 @@
 #include <deque>
 #include <mutex>
 #include <thread>
+#include <unistd.h>
 
 #include "ctx.h"
 
@@ -77,11 +78,23 @@ void load_api() {
   FP_SYM(Write, "cuFileWrite");
   FP_SYM(Read, "cuFileRead");
 #undef FP_SYM
-  // cuFileDriverOpen can block indefinitely on a host without nvidia-fs (seen
-  // on the gpurun B200 boxes, compatibility mode forced or not): it runs on
-  // a detached thread and is abandoned after FP_GDS_OPEN_TIMEOUT seconds
-  // (default 20), which makes FP_IO_GDS unavailable (-ENOSYS) instead of
-  // hanging the caller.
+  // Diagnosed on the gpurun B200 boxes (tools/diag/gds_hang_probe.sh,
+  // rip_sample.c): libcufile's RDMA setup reads /proc/modules (looking for
+  // nvidia_peermem) in a `while (!eof) getline` loop; a sandboxed procfs
+  // without /proc/modules makes the open fail, the stream never reaches EOF
+  // and cuFileDriverOpen spins forever. Fail fast there. (With the open
+  // redirected to an empty file — an LD_PRELOAD shim, diagnosis only —
+  // the driver opens in compatibility mode, and cuFileHandleRegister then
+  // fails (5030) because those boxes have no udev database for the volume
+  // holding the file.)
+  if (access("/proc/modules", R_OK) != 0 && !getenv("FP_GDS_SKIP_PRECHECK")) {
+    fprintf(stderr, "fastpersist: /proc/modules is not readable: libcufile's driver open "
+                    "would spin forever; FP_IO_GDS unavailable\n");
+    return;
+  }
+  // Any other hang: cuFileDriverOpen runs on a detached thread and is
+  // abandoned after FP_GDS_OPEN_TIMEOUT seconds (default 20), which makes
+  // FP_IO_GDS unavailable (-ENOSYS) instead of hanging the caller.
   GDS_DBG("cuFileDriverOpen");
   struct OpenState {
     std::mutex mu;
