@@ -116,6 +116,22 @@ def test_misaligned_and_degenerate_tensors(tmp_path, pack):
 
 
 @pytest.mark.parametrize("pack", ["v4", "bulk"])
+@pytest.mark.parametrize("ctas", [1, 3, 16])
+def test_background_pack_few_ctas(tmp_path, pack, ctas):
+    """Overlap mode's CTA cap (pack_ctas, §4.3): with 1-16 CTAs each CTA walks
+    hundreds of tiles of a 64 MiB pack group — the fused kernel's stage /
+    tile hand-off protocol over long sequences (odd tile counts per CTA, both
+    CRC groups) — and the shard and its CRC still match the oracle."""
+    st = _state("gpt3_small")
+    lay = oracle_layout([st], 1)
+    with fp.Checkpointer(DEV, pack=pack, pack_ctas=ctas, slot_bytes=16 << 20,
+                         pack_bytes=64 << 20) as ck:
+        s = ck.save(entries(st), str(tmp_path))
+    assert s["pack_launches"] > 0
+    _check_rank_files(str(tmp_path), lay, 1)
+
+
+@pytest.mark.parametrize("pack", ["v4", "bulk"])
 def test_many_small_tensors_align512(tmp_path, pack):
     """Alignment 512 (P:475's example) and 700 small ragged tensors: a 32 KiB
     slab tile then holds up to ~128 items (payloads, their < 16 B tails, zero
