@@ -209,6 +209,43 @@ def test_producer_stream_fence(tmp_path):
     _check_rank_files(str(tmp_path), lay, 1)
 
 
+@pytest.mark.parametrize("pack", ["bulk", "v4"])
+def test_overlapped_loop_each_checkpoint_is_its_iterations_state(tmp_path, pack):
+    """§4.3 pipelining over several iterations (SURVEY §8(c) pin 8):
+    fwd/bwd (GEMMs + the backward rewriting the grads, which the adam14
+    checkpoint excludes) -> wait() -> optimizer (master/m/v/param updated on
+    the training stream) -> begin(gen n) with that stream as producer.
+    Checkpoint n must equal the oracle of the state right after optimizer n
+    — not before it, and not touched by optimizer n+1 queued while the
+    checkpoint is still being written."""
+    st = _state("gpt3_small")
+    ck_ents = [(s, t) for s, t in st if s.section != "grad"]
+    grads = [t for s, t in st if s.section == "grad"]
+    upd = [t for s, t in ck_ents if t.is_floating_point()]
+    s = torch.cuda.Stream(DEV)
+    a = torch.randn(2048, 2048, device=DEV)
+    snaps = []
+    with fp.Checkpointer(DEV, pack=pack, slot_bytes=4 << 20, ring_slots=3,
+                         pack_bytes=8 << 20, pack_ctas=16) as ck:
+        for n in range(3):
+            with torch.cuda.stream(s):
+                for _ in range(6):                    # forward / backward
+                    a = a @ a
+                    a = a / a.norm()
+                for g in grads:                       # the backward writes the grads
+                    g.add_(1.0)
+            ck.wait()                                 # fence before the optimizer (P:515)
+            with torch.cuda.stream(s):                # optimizer n
+                for t in upd:
+                    t.mul_(0.5).add_(float(n + 1))
+                snaps.append([(sp, t.clone()) for sp, t in ck_ents])
+            ck.begin(entries(ck_ents), str(tmp_path / f"gen{n}"), stream=s)
+        ck.wait()
+    torch.cuda.synchronize()
+    for n, snap in enumerate(snaps):
+        _check_rank_files(str(tmp_path / f"gen{n}"), oracle_layout([snap], 1), 1)
+
+
 def test_c1_bench_launch_config(tmp_path):
     """The configuration bench.py times (64 MiB slots x 4, bulk pack + CRC, 1 MiB SQEs)."""
     st = _state("c1_tiny")
