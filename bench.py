@@ -489,7 +489,11 @@ def synthetic_overhead(a, ck, ents, state, dev, rank, world, path_of, image_gb, 
         out.append({"t_fb_s": round(n_gemm * t_gemm, 3), "flop_derived": t_fb == round(t_flop, 3),
                     "iter_s_no_ckpt": round(mb, 4), "iter_s_ckpt": round(mc, 4),
                     "overhead_pct": round(100 * (mc / mb - 1), 2),
-                    "eq1_hidden": crossover is not None and n_gemm * t_gemm >= crossover})
+                    "eq1_hidden": crossover is not None and n_gemm * t_gemm >= crossover,
+                    # Eq. 1: the optimizer of iteration i+1 waits
+                    # max(0, S_C/B - (T_F + T_B)) for checkpoint i
+                    "eq1_predicted_pct": None if crossover is None else
+                    round(100 * max(0.0, crossover - n_gemm * t_gemm) / mb, 2)})
     head = next(x for x in out if x["flop_derived"])
     return {"overhead_pct": head["overhead_pct"], "t_fb_s": head["t_fb_s"],
             "iter_s_no_ckpt": head["iter_s_no_ckpt"], "iter_s_ckpt": head["iter_s_ckpt"],
