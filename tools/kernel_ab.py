@@ -24,6 +24,7 @@ ap.add_argument("--dir", default="/dev/shm/fp_ab")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--tag", default="")
 ap.add_argument("--no-crc", action="store_true", help="pack only (bulk: fp_pack_bulk)")
+ap.add_argument("--pack-mib", type=int, default=256, help="bytes per pack launch (MiB)")
 a = ap.parse_args()
 peak = 6538.3
 try:
@@ -37,7 +38,8 @@ st = make_state(config_specs(a.cfg), dev)
 ents = [(x.name, t, x.section, x.owner) for x, t in st]
 torch.cuda.synchronize()
 rows = []
-with fp.Checkpointer(dev, pack=a.pack, no_fsync=True, no_crc=a.no_crc) as ck:
+with fp.Checkpointer(dev, pack=a.pack, no_fsync=True, no_crc=a.no_crc,
+                     pack_bytes=a.pack_mib << 20) as ck:
     for i in range(a.reps + 1):
         s = ck.save(ents, a.dir)
         if i:
@@ -48,6 +50,7 @@ b = sum(s["pack_bytes"] for s in rows)
 pms = sum(s["pack_ms"] for s in rows)
 cms = sum(s.get("crc_ms", 0.0) for s in rows)
 out = {"tag": a.tag or a.pack, "pack": a.pack, "env_groups": os.environ.get("FP_BC_GROUPS"),
+       "pack_mib": a.pack_mib,
        "launches": n, "pack_us": round(1e3 * pms / n, 2), "crc_us": round(1e3 * cms / n, 2),
        "pack_frac": round(2 * b / (pms / 1e3) / 1e9 / peak, 4),
        "total_us": round(1e3 * (pms + cms) / n, 2),
