@@ -787,11 +787,10 @@ def our_arm(a):
 
     if rank == 0:
         hbm = float(peaks["hbm_gbs"])
-        # FP_CRC_FUSED=1 (ablation) runs the fused pack + page-CRC kernel
-        fused = a.pack == "v4" and bool(os.environ.get("FP_CRC_FUSED")) \
-            and not os.environ.get("FP_NO_CRC")
-        kname = {"v4": "fp_pack_crc" if fused else "fp_pack_v4",
-                 "bulk": "fp_pack_bulk" if os.environ.get("FP_NO_CRC") else "fp_pack_bulk_crc",
+        nocrc = bool(os.environ.get("FP_NO_CRC"))
+        kname = {"v4": "fp_pack_v4",
+                 "bulk": "fp_pack_bulk" if nocrc else "fp_pack_bulk_crc",
+                 "lsu": "fp_pack_v4" if nocrc else "fp_pack_lsu_crc",
                  "host": "fp_pack_v4 (to mapped host)"}.get(a.pack)
         traffic = a.traffic
         try:   # ncu-measured DRAM bytes per launch of this launch shape (profiles/)
@@ -892,7 +891,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--pack", default="bulk", choices=["v4", "bulk", "host", "ce"])
+    ap.add_argument("--pack", default="bulk", choices=["v4", "bulk", "lsu", "host", "ce"])
     ap.add_argument("--pack-mib", type=int, default=256)
     ap.add_argument("--prio", default="high", choices=["high", "low"])
     ap.add_argument("--writer-stride", type=int, default=1,
@@ -915,7 +914,7 @@ def main():
     ap.add_argument("--overhead-base-iters", type=int, default=3,
                     help="iterations without checkpointing per T_FB (deterministic GEMM loop)")
     ap.add_argument("--overlap-ctas", type=int, default=16)
-    ap.add_argument("--overlap-pack", default="bulk", choices=["v4", "bulk"])
+    ap.add_argument("--overlap-pack", default="bulk", choices=["v4", "bulk", "lsu"])
     ap.add_argument("--overlap-io-engine", default=None, choices=["uring", "null"],
                     help="ablation: null = storage that completes at once (the GPU-side "
                          "interference floor of the overlapped checkpoint)")

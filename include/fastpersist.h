@@ -120,9 +120,14 @@ enum fp_pack_impl { FP_PACK_V4 = 0,     /* LSU 16-B vector gather -> device slab
                     FP_PACK_HOST = 2,   /* fused: the v4 kernel stores straight
                                            into the mapped pinned ring slot
                                            (zero-copy D2H over PCIe, no slab)    */
-                    FP_PACK_CE = 3      /* ablation, no kernel: one copy-engine
+                    FP_PACK_CE = 3,     /* ablation, no kernel: one copy-engine
                                            cudaMemcpyAsync per contiguous run of
-                                           a chunk, tensors -> pinned ring       */ };
+                                           a chunk, tensors -> pinned ring       */
+                    FP_PACK_LSU = 4     /* LSU 16-B vector gather -> device slab,
+                                           the page CRCs computed from the
+                                           registers the data passes through (one
+                                           kernel, no smem staging); then copy
+                                           engine                                */ };
 
 #define FP_CFG_NO_FSYNC 1u     /* skip fdatasync (benchmark ablation only)       */
 #define FP_CFG_NO_CRC   4u     /* skip the per-shard CRC-32          */
@@ -220,11 +225,10 @@ typedef struct fp_ctx fp_ctx;
 
 /* Fill *cfg with the defaults above (env overrides: FP_RING_SLOTS,
  * FP_SLOT_BYTES, FP_SQE_BYTES, FP_QD, FP_IO_ENGINE=uring|pwrite|buffered|null|gds,
- * FP_PACK=bulk|v4|host|ce, FP_PACK_PRIO=low, FP_PACK_CTAS, FP_ALIGN, FP_PACK_BYTES,
+ * FP_PACK=bulk|lsu|v4|host|ce, FP_PACK_PRIO=low, FP_PACK_CTAS, FP_ALIGN, FP_PACK_BYTES,
  * FP_WRITER_STRIDE, FP_CKPT_DIRS, FP_NO_CRC). Returns 0.
  * Read at run time (not part of fp_config): FP_NO_TMA=1 (LSU page-CRC kernel
- * instead of the TMA-staged one), FP_CRC_FUSED=1 (page CRCs inside the pack
- * kernel, ablation), FP_LAUNCH_GATE=1 (measurement: queue each pack group
+ * instead of the TMA-staged one), FP_LAUNCH_GATE=1 (measurement: queue each pack group
  * behind a one-warp gate the helper opens after enqueueing, so CUDA events
  * time the kernel alone; off by default and under a profiler), FP_NUMA=0 (do
  * not place the ring / helper on the GPU's NUMA node), FP_GDS_OPEN_TIMEOUT

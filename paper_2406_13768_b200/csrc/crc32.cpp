@@ -107,6 +107,13 @@ std::vector<uint32_t> crc_device_tables() {
   std::vector<uint32_t> t(kTabWords, 0);
   for (int k = 0; k < 4; ++k) memcpy(&t[kTabS4 + 256 * k], tab[k], 256 * 4);
   for (uint32_t l = 0; l < 32; ++l) t[kTabLaneK + l] = gf_x8n(128ull * (31 - l));
+  const uint32_t x512 = gf_x8n(512);
+  for (uint32_t j = 0; j < 8; ++j)
+    for (uint32_t n = 0; n < 16; ++n) {
+      t[kTabNibX + j * 16 + n] = gf_mul(x512, n << (4 * j));
+      for (uint32_t l = 0; l < 32; ++l)
+        t[kTabNibK + l * 128 + j * 16 + n] = gf_mul(gf_x8n(16ull * (31 - l)), n << (4 * j));
+    }
   return t;
 }
 

@@ -186,16 +186,22 @@ int crc_pages_launch(const uint8_t* d_buf, uint64_t bytes, const uint32_t* d_tab
 int pack_bulk_crc_launch(const Item* d_items, const uint32_t* d_tile_lo, uint32_t n_tiles,
                          uint64_t gbytes, uint8_t* d_slab, const uint32_t* d_tabs,
                          uint32_t* d_page_crc, int ctas, void* stream);
-// fused pack + page CRCs (fp_pack_crc, ablation): items of n_tiles 32 KiB slab
-// tiles (tile t = items [d_tile_lo[t], d_tile_lo[t+1]), none crossing a tile
-// boundary) -> d_slab, raw CRC of each of the first n_pages pages -> d_page_crc
-int pack_crc_launch(const Item* d_items, const uint32_t* d_tile_lo, uint32_t n_tiles,
-                    uint8_t* d_slab, uint32_t n_pages, const uint32_t* d_tabs,
-                    uint32_t* d_page_crc, int ctas, void* stream);
+// LSU pack + page CRCs from the registers it copies through (fp_pack_lsu_crc,
+// FP_PACK_LSU, ablation): tiles as below, gbytes = slab bytes of the group; the raw CRC
+// of every whole page -> d_page_crc (a ragged last page gets 0: the host CRCs
+// ragged chunks itself)
+int pack_lsu_crc_launch(const Item* d_items, const uint32_t* d_tile_lo, uint64_t gbytes,
+                        uint8_t* d_slab, const uint32_t* d_tabs, uint32_t* d_page_crc, int ctas,
+                        void* stream);
 // device CRC table blob layout (uint32 offsets)
 constexpr uint32_t kTabS4 = 0;
 constexpr uint32_t kTabLaneK = 4 * 256;  // 32 lane-combine constants x^(8*128*(31-l))
-constexpr uint32_t kTabWords = kTabLaneK + 32;
+// fp_pack_lsu_crc: products by a constant as 8 nibble lookups, entry
+// [j * 16 + n] = K * (n << 4j) (reflected): K = x^(8*512) (the stride between
+// a lane's 16-B chunks), and per lane l K_l = x^(8*16*(31-l))
+constexpr uint32_t kTabNibX = kTabLaneK + 32;
+constexpr uint32_t kTabNibK = kTabNibX + 128;  // [l * 128 + j * 16 + n]
+constexpr uint32_t kTabWords = kTabNibK + 32 * 128;
 
 // ---------------------------------------------------------------------------
 // CRC-32 helpers (crc32.cpp)

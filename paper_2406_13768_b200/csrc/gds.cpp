@@ -303,18 +303,17 @@ int fp_ctx::save_shard_gds(int fd) {
     if (g == 0) CK(cudaStreamWaitEvent(stream, ev_producer, 0));
     CK(cudaEventRecord(gds_ev[3 * h], stream));
     const bool bulk_crc = gpu_crc && cfg.pack_impl == FP_PACK_BULK && !group_tile_off.empty();
-    const bool fused = bulk_crc || (gpu_crc && cfg.pack_impl == FP_PACK_V4 &&
-                                    getenv("FP_CRC_FUSED") && !group_tile_off.empty());
+    const bool lsu_crc = gpu_crc && cfg.pack_impl == FP_PACK_LSU && !group_tile_off.empty();
+    const bool fused = bulk_crc || lsu_crc;
     int rr = bulk_crc ? pack_bulk_crc_launch(d_items + item_lo[c0], d_tiles + group_tile_off[g],
                                              (uint32_t)((gbytes + kTile - 1) / kTile), gbytes,
                                              slab, d_crc_tabs, d_page_crc, pack_ctas, stream)
-             : fused ? pack_crc_launch(d_items + item_lo[c0], d_tiles + group_tile_off[g],
-                                     (uint32_t)((gbytes + kTile - 1) / kTile), slab,
-                                     (uint32_t)(round_up(gbytes, 4096) / 4096), d_crc_tabs,
-                                     d_page_crc, (int)cfg.pack_ctas, stream)
-                   : pack_launch(cfg.pack_impl == FP_PACK_BULK ? FP_PACK_BULK : FP_PACK_V4,
-                                 d_items + item_lo[c0], item_lo[c1] - item_lo[c0], slab,
-                                 pack_ctas, stream);
+             : lsu_crc ? pack_lsu_crc_launch(d_items + item_lo[c0], d_tiles + group_tile_off[g],
+                                             gbytes, slab, d_crc_tabs, d_page_crc, pack_ctas,
+                                             stream)
+             : pack_launch(cfg.pack_impl == FP_PACK_BULK ? FP_PACK_BULK : FP_PACK_V4,
+                           d_items + item_lo[c0], item_lo[c1] - item_lo[c0], slab, pack_ctas,
+                           stream);
     if (rr) return rr;
     CK(cudaEventRecord(gds_ev[3 * h + 1], stream));
     st.kernel_launches += 1;

@@ -1001,144 +1001,180 @@ __global__ void __launch_bounds__(bc_threads(kGroups), 1)
 }
 
 // ---------------------------------------------------------------------------
-// fp_pack_crc: the pack and the page CRCs in ONE pass over the data (the
-// separate fp_crc_pages re-reads the whole slab from HBM). Work unit: one
-// 32 KiB tile of the slab (8 pages); items never cross a tile boundary and
-// tile_lo[t] is the first item of tile t. Warp-specialised CTA of 512
-// threads, one per SM (the per-lane CRC tables take 148 KiB of shared memory):
-//   warps 0-7  (producers): gather the tile's items src -> slab exactly as
-//              fp_pack_v4 does, and store the same bytes into a shared-memory
-//              staging tile (double buffered, 16-B chunks XOR-swizzled so both
-//              the producers' coalesced stores and the consumers' per-lane
-//              128-B reads are free of bank conflicts);
-//   warps 8-15 (consumers): CRC of page w of the staged tile from shared
-//              memory, as fp_crc_pages computes it from global memory.
-// Hand-off through named barriers: FULL[b] (producers arrive, consumers sync)
-// and EMPTY[b] (consumers arrive, producers sync before refilling b).
+// fp_pack_lsu_crc (FP_PACK_LSU, ablation): the LSU pack of fp_pack_v4
+// computing the page CRC-32s from the registers it copies through — no
+// shared-memory staging, no bulk-copy engine, no hand-off between warps. One
+// warp per 4 KiB slab page (pages dealt round robin over all warps of the
+// grid): lane l loads the 16-B chunks 32u + l, u = 0..7 (eight coalesced
+// 512-B loads in flight), stores them to the slab with the same pattern, then
+//   c_u = raw CRC of chunk 32u + l     (4-word slicing-by-4 chains from 0,
+//                                       eight independent chains per lane)
+//   s_l = sum_u c_u * x^(8*512*(7-u))  (Horner, product by x^(8*512) as 8
+//                                       nibble lookups)
+//   page = XOR_l s_l * x^(8*16*(31-l)) (8 nibble lookups into lane l's own
+//                                       table, then a 5-step XOR shuffle)
+// which is R(page) by the linearity R(A||B) = R(A) x^(8|B|) + R(B): chunk q
+// is followed by 4096 - 16q - 16 = 512(7-u) + 16(31-l) bytes. All tables are
+// per-lane (bank-private) copies in shared memory: 128 KiB slicing tables in
+// fp_crc_pages_tma's paired layout + 2 x 16 KiB nibble tables. Pages that no
+// single co-aligned item covers (header/padding seams, odd storage offsets,
+// byte-granular shard starts, a group's ragged last page) are gathered by the
+// warp with copy_bytes and read back from the slab for their CRC. The scheme
+// is emulated against the plain CRC on the host (tools/diag/crc_emulate.cpp).
+// Measured (profiles/r02_lsu_crc_ablation.md): 103.5 us per 256 MiB (0.79 of
+// HBM) vs 90 us for fp_pack_bulk_crc — the table lookups share the L1/LSU
+// data pipe with the pack's own loads and stores, and a warp busy with its
+// CRC has no loads in flight; software pipelining the next page's loads
+// through a shared-memory transpose (16 warps, 118 registers) was slower
+// still (123.5 us: the CRC chains became latency-bound). The TMA pack keeps
+// the copy off the LSU, which is why it is the default.
 // ---------------------------------------------------------------------------
-constexpr int kPcThreads = 512;
-constexpr int kPcProducers = 256;
-constexpr size_t kPcTabWords = kCrcTabWords;
-constexpr size_t kPcSmem = kPcTabWords * 4 + 2 * (size_t)kTile;  // 192 KiB
+constexpr int kLcWarps = 24;  // 80 registers, no spills (32 warps spill at 64)
+constexpr size_t kLcNibBytes = 8 * 16 * 32 * 4;  // 16 KiB: [j * 16 + n][lane]
+constexpr size_t kLcSmem = kCtTabBytes + 2 * kLcNibBytes;
 
-__device__ __forceinline__ uint32_t stage_off(uint32_t off) {  // swizzled byte offset
-  const uint32_t c = off >> 4;
-  return ((c ^ ((c >> 3) & 7)) << 4) | (off & 15);
-}
-__device__ __forceinline__ void bar_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void bar_arrive(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-// copy_bytes + the same bytes into the staging tile at `soff` (tile offset)
-__device__ __forceinline__ void copy_stage(uint8_t* __restrict__ dst,
-                                           const uint8_t* __restrict__ src, uint32_t len,
-                                           uint8_t* __restrict__ stage, uint32_t soff, int t,
-                                           int nthr) {
-  const uint32_t phase = (uint32_t)((uintptr_t)dst & 15);
-  const bool coaligned = !src || (((uintptr_t)src & 15) == phase) ;
-  if (!coaligned || ((soff ^ phase) & 15)) {
-    for (uint32_t i = t; i < len; i += nthr) {
-      const uint8_t b = src[i];
-      dst[i] = b;
-      stage[stage_off(soff + i)] = b;
-    }
-    return;
-  }
-  uint32_t head = (16 - phase) & 15;
-  if (head > len) head = len;
-  if ((uint32_t)t < head) {
-    const uint8_t b = src ? src[t] : 0;
-    dst[t] = b;
-    stage[stage_off(soff + t)] = b;
-  }
-  const uint32_t n16 = (len - head) >> 4;
-  uint4* d16 = reinterpret_cast<uint4*>(dst + head);
-  const uint32_t s0 = soff + head;  // 16-B aligned
-  if (src) {
-    const uint4* s16 = reinterpret_cast<const uint4*>(src + head);
-    for (uint32_t base = 0; base < n16; base += (uint32_t)nthr * kV4Unroll) {
-      uint4 v[kV4Unroll];
+// a * K as XOR_j NT[j][(a >> 4j) & 15]; `t` = the table base + lane * 4
+// (entry e of lane l at byte e * 128 + l * 4)
+__device__ __forceinline__ uint32_t nib_mul(uint32_t a, const uint8_t* t) {
+  uint32_t r = 0;
 #pragma unroll
-      for (int u = 0; u < kV4Unroll; ++u) {
-        const uint32_t j = base + (uint32_t)u * nthr + t;
-        if (j < n16) v[u] = ld_stream(s16 + j);
-      }
-#pragma unroll
-      for (int u = 0; u < kV4Unroll; ++u) {
-        const uint32_t j = base + (uint32_t)u * nthr + t;
-        if (j < n16) {
-          st_v4(d16 + j, v[u]);
-          *reinterpret_cast<uint4*>(stage + stage_off(s0 + 16 * j)) = v[u];
-        }
-      }
-    }
-  } else {
-    const uint4 z = make_uint4(0, 0, 0, 0);
-    for (uint32_t j = t; j < n16; j += nthr) {
-      st_v4(d16 + j, z);
-      *reinterpret_cast<uint4*>(stage + stage_off(s0 + 16 * j)) = z;
-    }
+  for (int j = 0; j < 8; ++j) {
+    const uint32_t idx = (j == 0 ? (a << 7) : j == 1 ? (a << 3) : (a >> (4 * j - 7))) & 0x780u;
+    r ^= *reinterpret_cast<const uint32_t*>(t + j * 2048 + idx);
   }
-  const uint32_t done = head + (n16 << 4);
-  const uint32_t tail = len - done;
-  if ((uint32_t)t < tail) {
-    const uint8_t b = src ? src[done + t] : 0;
-    dst[done + t] = b;
-    stage[stage_off(soff + done + t)] = b;
-  }
+  return r;
 }
 
-__global__ void __launch_bounds__(kPcThreads, 1)
-    fp_pack_crc(const Item* __restrict__ items, const uint32_t* __restrict__ tile_lo,
-                uint32_t n_tiles, uint8_t* __restrict__ slab, uint32_t n_pages,
-                const uint32_t* __restrict__ tabs, uint32_t* __restrict__ page_crc) {
-  extern __shared__ __align__(16) uint32_t pc_smem[];
-  uint32_t* rep = pc_smem;                    // [4][256][32] per-lane copies
-  uint8_t* stage0 = reinterpret_cast<uint8_t*>(pc_smem + kPcTabWords);
-  for (int i = threadIdx.x; i < 4 * 256 * 32; i += blockDim.x) rep[i] = tabs[kTabS4 + (i >> 5)];
-  __syncthreads();
+__global__ void __launch_bounds__(kLcWarps * 32, 1)
+    fp_pack_lsu_crc(const Item* __restrict__ items, const uint32_t* __restrict__ tile_lo,
+                    uint64_t gbytes, uint8_t* __restrict__ slab,
+                    const uint32_t* __restrict__ tabs, uint32_t* __restrict__ page_crc) {
+  extern __shared__ __align__(128) uint8_t lc_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp < kPcProducers / 32) {
-    const int t = threadIdx.x;
-    uint32_t k = 0;
-    for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
-      const int b = (int)(k & 1);
-      if (k >= 2) bar_sync(3 + b, kPcThreads);  // EMPTY[b]
-      uint8_t* stage = stage0 + (size_t)b * kTile;
-      const uint32_t base = tile * kTile;
-      for (uint32_t i = tile_lo[tile]; i < tile_lo[tile + 1]; ++i) {
-        const Item it = items[i];
-        copy_stage(slab + it.dst, reinterpret_cast<const uint8_t*>(it.src), it.len, stage,
-                   it.dst - base, t, kPcProducers);
-      }
-      bar_arrive(1 + b, kPcThreads);  // FULL[b]
+  const uint32_t n_pages = (uint32_t)((gbytes + 4095) / 4096);
+  const uint32_t W = gridDim.x * kLcWarps;
+  // page descriptors: {first item, end} of the page's tile and one item per
+  // lane; the next page's are loaded while this page's data is in flight
+  struct Desc {
+    uint32_t lo, hi;
+    Item it;
+  };
+  auto load_bounds = [&](uint32_t pg, Desc& d) {
+    d.lo = d.hi = 0;
+    if (pg < n_pages) {
+      const uint32_t t = pg / (kTile / 4096);
+      d.lo = tile_lo[t];
+      d.hi = tile_lo[t + 1];
     }
-    // consume the consumers' last EMPTY arrivals (barrier state must balance)
-    for (uint32_t j = (k >= 2 ? k - 2 : 0); j < k; ++j) bar_sync(3 + (int)(j & 1), kPcThreads);
-  } else {
-    const int w = warp - kPcProducers / 32;  // page of the tile
-    uint32_t kv[32];
-    lane_k_init(tabs[kTabLaneK + lane], kv);
-    uint32_t k = 0;
-    for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
-      const int b = (int)(k & 1);
-      bar_sync(1 + b, kPcThreads);  // FULL[b]
-      const uint8_t* stage = stage0 + (size_t)b * kTile;
-      const uint32_t pg = tile * (kTile / 4096) + (uint32_t)w;
-      uint4 v[8];
+  };
+  auto load_item = [&](Desc& d) {
+    d.it = {0, 0, 0};
+    if (d.lo + lane < d.hi) d.it = items[d.lo + lane];
+  };
+  Desc cur;
+  load_bounds(blockIdx.x * kLcWarps + warp, cur);
+  load_item(cur);
+  // the tables (the descriptor loads above are in flight meanwhile):
+  // slicing tables as in fp_pack_bulk_crc, nibble tables [e][lane]
+  for (int c = threadIdx.x; c < (int)(kCtTabBytes / 16); c += blockDim.x) {
+    const int k = ((c >> 12) << 1) | ((c >> 3) & 1), e = (c >> 4) & 255;
+    const uint32_t v = tabs[kTabS4 + k * 256 + e];
+    *reinterpret_cast<uint4*>(lc_raw + (size_t)c * 16) = make_uint4(v, v, v, v);
+  }
+  for (int c = threadIdx.x; c < (int)(kLcNibBytes / 16); c += blockDim.x) {
+    const int e = c >> 3, l0 = (c & 7) * 4;
+    const uint32_t x = tabs[kTabNibX + e];
+    *reinterpret_cast<uint4*>(lc_raw + kCtTabBytes + (size_t)c * 16) = make_uint4(x, x, x, x);
+    const uint32_t* k = tabs + kTabNibK + e;
+    *reinterpret_cast<uint4*>(lc_raw + kCtTabBytes + kLcNibBytes + (size_t)c * 16) =
+        make_uint4(k[l0 * 128], k[(l0 + 1) * 128], k[(l0 + 2) * 128], k[(l0 + 3) * 128]);
+  }
+  __syncthreads();
+  const uint32_t lane4 = (uint32_t)lane * 4;
+  const uint8_t* tx = lc_raw + kCtTabBytes + lane4;
+  const uint8_t* tk = tx + kLcNibBytes;
+  auto lk = [&](uint32_t x, const int b, const int tb) -> uint32_t {
+    const uint32_t r = __byte_perm(x, lane4, 4u | ((uint32_t)b << 4) | (5u << 8) | (5u << 12));
+    return *reinterpret_cast<const uint32_t*>(lc_raw + r + ((tb >> 1) * 65536 + (tb & 1) * 128));
+  };
+  for (uint32_t pg = blockIdx.x * kLcWarps + warp; pg < n_pages; pg += W) {
+    const uint32_t p0 = pg * 4096u;  // slab offset (a pack group is < 4 GiB)
+    const uint64_t left = gbytes - p0;
+    const uint32_t plen = left < 4096 ? (uint32_t)left : 4096u;
+    // the item covering the whole page with a source co-aligned to the slab
+    // (or a zero item): the common case, one item per 32 KiB tile
+    Item f = {0, 0, 0};
+    bool fast = false;
+    for (uint32_t b = cur.lo; b < cur.hi; b += 32) {
+      const Item it = b == cur.lo ? cur.it : (b + lane < cur.hi ? items[b + lane] : Item{0, 0, 0});
+      const bool ok = plen == 4096 && b + lane < cur.hi && it.dst <= p0 &&
+                      it.dst + it.len >= p0 + 4096 && (!it.src || !((it.src - it.dst) & 15));
+      const uint32_t m = __ballot_sync(0xffffffffu, ok);
+      if (m) {
+        const int j = __ffs(m) - 1;
+        f.src = __shfl_sync(0xffffffffu, it.src, j);
+        f.dst = __shfl_sync(0xffffffffu, it.dst, j);
+        fast = true;
+        break;
+      }
+    }
+    Desc nxt;
+    load_bounds(pg + W, nxt);
+    uint4 v[8];
+    uint4* d = reinterpret_cast<uint4*>(slab + p0);
+    if (fast) {
+      if (f.src) {
+        const uint4* s = reinterpret_cast<const uint4*>(f.src + (p0 - f.dst));
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
-        v[u] = *reinterpret_cast<const uint4*>(
-            stage + stage_off((uint32_t)w * 4096 + (uint32_t)lane * 128 + 16 * u));
-      bar_arrive(3 + b, kPcThreads);  // EMPTY[b]: the page is in registers
-      if (pg < n_pages) {
-        const uint32_t c = page_crc_warp(v, rep, kv, lane);
-        if (lane == 0) page_crc[pg] = c;
+        for (int u = 0; u < 8; ++u) v[u] = ld_stream(s + u * 32 + lane);
+      } else {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = make_uint4(0, 0, 0, 0);
+      }
+      load_item(nxt);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) st_v4(d + u * 32 + lane, v[u]);
+    } else {
+      // every item of the tile that meets the page, clipped to it
+      for (uint32_t k = cur.lo; k < cur.hi; ++k) {
+        const Item it = items[k];
+        const uint32_t a = it.dst > p0 ? it.dst : p0;
+        const uint32_t e = it.dst + it.len < p0 + plen ? it.dst + it.len : p0 + plen;
+        if (a < e)
+          copy_bytes(slab + a, it.src ? reinterpret_cast<const uint8_t*>(it.src) + (a - it.dst) : nullptr,
+                     e - a, lane, 32);
+      }
+      load_item(nxt);
+      __syncwarp();  // the warp's slab stores are visible to its loads below
+      if (plen == 4096) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = ld_coherent(d + u * 32 + lane);
       }
     }
+    cur = nxt;
+    if (plen < 4096) {  // a ragged last page: the host CRCs ragged chunks itself
+      if (lane == 0) page_crc[pg] = 0;
+      continue;
+    }
+    uint32_t cu[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      uint32_t x = v[u].x;
+      uint32_t c = lk(x, 0, 3) ^ lk(x, 1, 2) ^ lk(x, 2, 1) ^ lk(x, 3, 0);
+      x = c ^ v[u].y;
+      c = lk(x, 0, 3) ^ lk(x, 1, 2) ^ lk(x, 2, 1) ^ lk(x, 3, 0);
+      x = c ^ v[u].z;
+      c = lk(x, 0, 3) ^ lk(x, 1, 2) ^ lk(x, 2, 1) ^ lk(x, 3, 0);
+      x = c ^ v[u].w;
+      cu[u] = lk(x, 0, 3) ^ lk(x, 1, 2) ^ lk(x, 2, 1) ^ lk(x, 3, 0);
+    }
+    uint32_t s = cu[0];
+#pragma unroll
+    for (int u = 1; u < 8; ++u) s = nib_mul(s, tx) ^ cu[u];
+    s = nib_mul(s, tk);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s ^= __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) page_crc[pg] = s;
   }
 }
 
@@ -1199,7 +1235,7 @@ static bool smem_opt_in(K kernel, size_t bytes) {
 
 int pack_default_ctas(int impl, int device) {
   const int sms = sm_count(device);
-  return impl == FP_PACK_BULK ? sms : sms * 4;
+  return impl == FP_PACK_BULK || impl == FP_PACK_LSU ? sms : sms * 4;
 }
 
 int pack_launch(int impl, const Item* d_items, uint32_t n_items, uint8_t* d_slab, int ctas,
@@ -1310,16 +1346,17 @@ int pack_bulk_crc_launch(const Item* d_items, const uint32_t* d_tile_lo, uint32_
   return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
 }
 
-int pack_crc_launch(const Item* d_items, const uint32_t* d_tile_lo, uint32_t n_tiles,
-                    uint8_t* d_slab, uint32_t n_pages, const uint32_t* d_tabs,
-                    uint32_t* d_page_crc, int ctas, void* stream) {
-  if (!n_tiles) return 0;
-  if (!smem_opt_in<3>(fp_pack_crc, kPcSmem)) return FP_ECUDA;
+int pack_lsu_crc_launch(const Item* d_items, const uint32_t* d_tile_lo, uint64_t gbytes,
+                        uint8_t* d_slab, const uint32_t* d_tabs, uint32_t* d_page_crc, int ctas,
+                        void* stream) {
+  if (!gbytes) return 0;
+  if (!smem_opt_in<9>(fp_pack_lsu_crc, kLcSmem)) return FP_ECUDA;
   const int sms = sm_count(-1);
-  const int grid = (int)std::min<uint32_t>(n_tiles, (uint32_t)std::min(ctas > 0 ? ctas : sms, sms));
-  fp_pack_crc<<<grid, kPcThreads, kPcSmem, (cudaStream_t)stream>>>(d_items, d_tile_lo, n_tiles,
-                                                                  d_slab, n_pages, d_tabs,
-                                                                  d_page_crc);
+  const uint64_t n_pages = (gbytes + 4095) / 4096;
+  const int grid = (int)std::min<uint64_t>((n_pages + kLcWarps - 1) / kLcWarps,
+                                           (uint64_t)std::min(ctas > 0 ? ctas : sms, sms));
+  fp_pack_lsu_crc<<<grid, kLcWarps * 32, kLcSmem, (cudaStream_t)stream>>>(d_items, d_tile_lo, gbytes,
+                                                                         d_slab, d_tabs, d_page_crc);
   return cudaGetLastError() == cudaSuccess ? 0 : FP_ECUDA;
 }
 

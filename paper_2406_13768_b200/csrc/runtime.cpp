@@ -227,11 +227,11 @@ int fp_ctx::save_shard() {
   xcrc.reset(plan.extents);
   // FP_PACK_V4: fp_pack_v4, then fp_crc_pages_tma over the slab;
   // FP_PACK_BULK: fp_pack_bulk_crc computes the page CRCs from its shared-
-  // memory stages (one pass); FP_CRC_FUSED=1 with v4: fp_pack_crc (LSU
-  // fused ablation)
+  // memory stages (one pass); FP_PACK_LSU: fp_pack_lsu_crc computes them
+  // from the registers its LSU pack copies through (one pass, ablation)
   const bool bulk_crc = gpu_crc && cfg.pack_impl == FP_PACK_BULK && !group_tile_off.empty();
-  const bool fused = bulk_crc || (gpu_crc && cfg.pack_impl == FP_PACK_V4 &&
-                                  getenv("FP_CRC_FUSED") && !group_tile_off.empty());
+  const bool lsu_crc = gpu_crc && cfg.pack_impl == FP_PACK_LSU && !group_tile_off.empty();
+  const bool fused = bulk_crc || lsu_crc;
   auto stage = [&](uint64_t c) -> int {
     const uint32_t s = (uint32_t)(c % R);
     const uint64_t len = std::min<uint64_t>(S, plan.shard_bytes - c * S);
@@ -300,11 +300,9 @@ int fp_ctx::save_shard() {
         r = pack_bulk_crc_launch(d_items + item_lo[c], d_tiles + group_tile_off[c / G],
                                  (uint32_t)((gbytes + kTile - 1) / kTile), gbytes, d_slab,
                                  d_crc_tabs, d_page_crc, pack_ctas, stream);
-      else if (!r && fused)  // pack + page CRCs in one pass over the data
-        r = pack_crc_launch(d_items + item_lo[c], d_tiles + group_tile_off[c / G],
-                            (uint32_t)((gbytes + kTile - 1) / kTile), d_slab,
-                            (uint32_t)(round_up(gbytes, 4096) / 4096), d_crc_tabs, d_page_crc,
-                            (int)cfg.pack_ctas, stream);
+      else if (!r && lsu_crc)  // LSU pack + page CRCs from its registers, one pass
+        r = pack_lsu_crc_launch(d_items + item_lo[c], d_tiles + group_tile_off[c / G], gbytes,
+                                d_slab, d_crc_tabs, d_page_crc, pack_ctas, stream);
       else if (!r)
         r = pack_launch(cfg.pack_impl, d_items + item_lo[c], item_lo[c1] - item_lo[c], d_slab,
                         pack_ctas, stream);
@@ -754,6 +752,7 @@ int fp_config_default(fp_config* cfg) {
   cfg->pack_impl = !pk                   ? FP_PACK_BULK
                    : !strcmp(pk, "v4")   ? FP_PACK_V4
                    : !strcmp(pk, "bulk") ? FP_PACK_BULK
+                   : !strcmp(pk, "lsu")  ? FP_PACK_LSU
                    : !strcmp(pk, "host") ? FP_PACK_HOST
                    : !strcmp(pk, "ce")   ? FP_PACK_CE
                                          : FP_PACK_BULK;
@@ -768,7 +767,7 @@ static int check_cfg(const fp_config& c) {
   if (!c.slot_bytes || c.slot_bytes % A || c.slot_bytes > (1ull << 31)) return -EINVAL;
   if (!c.sqe_bytes || c.sqe_bytes % A || c.sqe_bytes > (1u << 30)) return -EINVAL;
   if (c.sqe_bytes / 512 >= (1u << 24)) return -EINVAL;
-  if (c.io_engine > FP_IO_GDS || c.pack_impl > FP_PACK_CE) return -EINVAL;
+  if (c.io_engine > FP_IO_GDS || c.pack_impl > FP_PACK_LSU) return -EINVAL;
   if (c.io_engine == FP_IO_GDS && (c.pack_impl == FP_PACK_HOST || c.pack_impl == FP_PACK_CE))
     return -EINVAL;  // GDS writes from the device slab: a slab-producing pack is needed
   if (c.pack_bytes > (2ull << 30)) return -EINVAL;
@@ -996,9 +995,7 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
         return fail(FP_ECUDA);
     }
     c->pack_ctas = cfg.pack_ctas ? (int)cfg.pack_ctas
-                                 : pack_default_ctas(cfg.pack_impl == FP_PACK_BULK ? FP_PACK_BULK
-                                                                                   : FP_PACK_V4,
-                                                     cuda_device);
+                                 : pack_default_ctas((int)cfg.pack_impl, cuda_device);
   }
   c->th = std::thread([c] {
     bind_thread_to_node(c->numa_node);

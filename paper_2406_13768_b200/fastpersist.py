@@ -33,7 +33,7 @@ FP_CFG_PRIO_LOW = 2
 FP_CFG_NO_CRC = 4
 FP_CFG_BALANCE_BYTES = 8
 IO_ENGINES = {"uring": 0, "pwrite": 1, "buffered": 2, "null": 3, "gds": 4}
-PACK_IMPLS = {"v4": 0, "bulk": 1, "host": 2, "ce": 3}
+PACK_IMPLS = {"v4": 0, "bulk": 1, "host": 2, "ce": 3, "lsu": 4}
 SECTIONS = {"param": 0, "grad": 1, "master": 2, "exp_avg": 3, "exp_avg_sq": 4, "other": 5}
 DTYPES = {torch.float32: 1, torch.bfloat16: 2, torch.float16: 3, torch.float64: 4,
           torch.int64: 5, torch.int32: 6, torch.uint8: 7}

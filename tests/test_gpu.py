@@ -41,7 +41,7 @@ def _check_rank_files(tmp, lay, k, crc=True):
             assert man["shards"][r]["crc32"] == fpck.shard_crc32(lay, r), r
 
 
-@pytest.mark.parametrize("pack", ["v4", "bulk", "host", "ce"])
+@pytest.mark.parametrize("pack", ["v4", "bulk", "lsu", "host", "ce"])
 @pytest.mark.parametrize("slot_bytes", [4096, 1 << 20, 3 << 20, 64 << 20])
 def test_c1_tiny_parity(tmp_path, pack, slot_bytes):
     st = _state("c1_tiny")
@@ -57,7 +57,7 @@ def test_c1_tiny_parity(tmp_path, pack, slot_bytes):
     _check_rank_files(str(tmp_path), lay, 1)
 
 
-@pytest.mark.parametrize("pack", ["v4", "bulk"])
+@pytest.mark.parametrize("pack", ["v4", "bulk", "lsu"])
 @pytest.mark.parametrize("slot_bytes,pack_bytes,slots", [(1 << 20, 3 << 20, 2), (4096, 5 * 4096, 3),
                                                          (8 << 20, 64 << 20, 4),
                                                          (2 << 20, 2 << 20, 1)])
@@ -84,7 +84,7 @@ def test_stream_priority_parity(tmp_path, prio):
     _check_rank_files(str(tmp_path), lay, 1)
 
 
-@pytest.mark.parametrize("pack", ["v4", "bulk", "host", "ce"])
+@pytest.mark.parametrize("pack", ["v4", "bulk", "lsu", "host", "ce"])
 @pytest.mark.parametrize("cfg", ["gpt3_small", "gpt3_odd", "zero_small", "moe_small"])
 def test_structured_states_parity(tmp_path, cfg, pack):
     st = _state(cfg)
@@ -94,7 +94,7 @@ def test_structured_states_parity(tmp_path, cfg, pack):
     _check_rank_files(str(tmp_path), lay, 1)
 
 
-@pytest.mark.parametrize("pack", ["v4", "bulk", "host", "ce"])
+@pytest.mark.parametrize("pack", ["v4", "bulk", "lsu", "host", "ce"])
 def test_misaligned_and_degenerate_tensors(tmp_path, pack):
     """Odd storage offsets (byte path), empty tensors, scalars, 1-byte tails."""
     base = torch.randint(0, 256, (1 << 20,), dtype=torch.uint8, device=DEV)
@@ -115,7 +115,7 @@ def test_misaligned_and_degenerate_tensors(tmp_path, pack):
     _check_rank_files(str(tmp_path), lay, 1)
 
 
-@pytest.mark.parametrize("pack", ["v4", "bulk"])
+@pytest.mark.parametrize("pack", ["v4", "bulk", "lsu"])
 @pytest.mark.parametrize("ctas", [1, 3, 16])
 def test_background_pack_few_ctas(tmp_path, pack, ctas):
     """Overlap mode's CTA cap (pack_ctas, §4.3): with 1-16 CTAs each CTA walks
@@ -131,7 +131,7 @@ def test_background_pack_few_ctas(tmp_path, pack, ctas):
     _check_rank_files(str(tmp_path), lay, 1)
 
 
-@pytest.mark.parametrize("pack", ["v4", "bulk"])
+@pytest.mark.parametrize("pack", ["v4", "bulk", "lsu"])
 def test_many_small_tensors_align512(tmp_path, pack):
     """Alignment 512 (P:475's example) and 700 small ragged tensors: a 32 KiB
     slab tile then holds up to ~128 items (payloads, their < 16 B tails, zero
@@ -209,7 +209,7 @@ def test_producer_stream_fence(tmp_path):
     _check_rank_files(str(tmp_path), lay, 1)
 
 
-@pytest.mark.parametrize("pack", ["bulk", "v4"])
+@pytest.mark.parametrize("pack", ["bulk", "v4", "lsu"])
 def test_overlapped_loop_each_checkpoint_is_its_iterations_state(tmp_path, pack):
     """§4.3 pipelining over several iterations (SURVEY §8(c) pin 8):
     fwd/bwd (GEMMs + the backward rewriting the grads, which the adam14
@@ -513,7 +513,7 @@ def test_writer_stride_device(tmp_path, cfg, k, stride):
             c.close()
 
 
-@pytest.mark.parametrize("pack", ["v4", "bulk"])
+@pytest.mark.parametrize("pack", ["v4", "bulk", "lsu"])
 @pytest.mark.parametrize("cfg,k,exchange", [("c1_tiny", 7, "peer"), ("gpt3_odd", 3, "nccl"),
                                             ("moe_small", 4, "peer"), ("gpt3_odd", 1, "peer")])
 def test_byte_balance_device(tmp_path, monkeypatch, cfg, k, exchange, pack):
@@ -613,14 +613,13 @@ def test_gds_engine_parity(tmp_path, cfg, slot, pack_bytes, pack):
 
 
 @pytest.mark.parametrize("slot,pack_bytes", [(1 << 20, 3 << 20), (4096, 8192), (64 << 20, 256 << 20)])
-def test_crc_fused_kernel_parity(tmp_path, monkeypatch, slot, pack_bytes):
-    """FP_CRC_FUSED=1 (ablation): page CRCs computed inside the pack
-    (fp_pack_crc) instead of fp_crc_pages_tma over the slab; same shard bytes,
-    same CRC-32."""
-    monkeypatch.setenv("FP_CRC_FUSED", "1")
+def test_crc_lsu_kernel_parity(tmp_path, slot, pack_bytes):
+    """pack="lsu" (ablation): page CRCs computed from the registers of the
+    LSU pack (fp_pack_lsu_crc: per-chunk chains, Horner over the lane's
+    chunks, nibble-table products) — same shard bytes, same CRC-32."""
     st = _state("gpt3_odd")
     lay = oracle_layout([st], 1)
-    with fp.Checkpointer(DEV, slot_bytes=slot, pack_bytes=pack_bytes) as ck:
+    with fp.Checkpointer(DEV, pack="lsu", slot_bytes=slot, pack_bytes=pack_bytes) as ck:
         s = ck.save(entries(st), str(tmp_path))
     assert s["crc_valid"]
     _check_rank_files(str(tmp_path), lay, 1)

@@ -1,5 +1,5 @@
 // Host emulation of the device CRC-32 scheme (pack.cu: page_crc_warp as used
-// by fp_crc_pages / fp_crc_pages_tma / fp_pack_crc) and the host fold of page
+// by fp_crc_pages / fp_crc_pages_tma / fp_pack_bulk_crc, and fp_pack_lsu_crc) and the host fold of page
 // CRCs per extent (ExtentCrc): the same table blob (crc_device_tables), the
 // same per-lane chain and register lane combine, compared with the plain slicing CRC
 // (crc_raw_update) on random pages, for several page and extent counts. Built and run by
@@ -39,6 +39,30 @@ int main() {
       }
       pc[pg] = crc;
       if (pc[pg] != crc_raw_update(0, buf.data() + (size_t)pg * 4096, 4096)) { printf("page mismatch\n"); return 1; }
+      // pack.cu fp_pack_lsu_crc: lane l holds the 16-B chunks 32u + l
+      // (u = 0..7, the coalesced load pattern); a chain per chunk from 0, the
+      // chunks joined by Horner with x^(8*512) and the lane's term times
+      // x^(8*16*(31-l)), both products as 8 nibble lookups (kTabNibX/kTabNibK)
+      auto nib = [&](uint32_t a, const uint32_t* nt) {
+        uint32_t r = 0;
+        for (int j = 0; j < 8; ++j) r ^= nt[j * 16 + ((a >> (4 * j)) & 15)];
+        return r;
+      };
+      uint32_t crc2 = 0;
+      for (int lane = 0; lane < 32; ++lane) {
+        uint32_t s = 0;
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t* w = (const uint32_t*)(buf.data() + (size_t)pg * 4096 + (32 * u + lane) * 16);
+          uint32_t c = 0;
+          for (int q = 0; q < 4; ++q) {
+            const uint32_t x = c ^ w[q];
+            c = t3[x & 255] ^ t2[(x >> 8) & 255] ^ t1[(x >> 16) & 255] ^ t0[x >> 24];
+          }
+          s = (u ? nib(s, &T[kTabNibX]) : 0u) ^ c;
+        }
+        crc2 ^= nib(s, &T[kTabNibK + lane * 128]);
+      }
+      if (crc2 != crc) { printf("lsu page mismatch\n"); return 1; }
     }
     // host fold (ExtentCrc): the pages split into extents at page boundaries
     // (every ppc pages), some runs added as pages and some as bytes; each
