@@ -360,6 +360,52 @@ int fp_io_bench(const char *dir, uint64_t bytes, const fp_config *cfg, int tag,
 int fp_io_bench_read(const char *dir, uint64_t bytes, const fp_config *cfg, int tag,
                      double *gbps);
 
+/* ---------------------------------------------------------------------------
+ * Byte-stream writer: the paper's torch.save integration (§5.1 P:532-533:
+ * "implementing FastPersist in a compatible object that we pass to
+ * torch.save() ... with no change to other operations (e.g., tensor
+ * serialization)") on the NVMe path of §4.1: the stream's bytes go through
+ * an IO buffer of ring_slots x slot_bytes page-aligned host memory (P:467-473:
+ * ring_slots = 1 is the paper's single-buffer mode, >= 2 double buffering —
+ * slot i+1 fills while slot i is being written) and every full slot is
+ * written with O_DIRECT at its file offset (cfg->io_engine, sqe_bytes per
+ * request, io_depth in flight). At close the last slot's aligned prefix goes
+ * the same way and the < alignment suffix through a buffered descriptor of
+ * the same file ("the suffix using traditional I/O libraries, into
+ * the same checkpoint file"), then both are fdatasync'd. The file is
+ * byte-for-byte what a plain write() of the same stream gives.
+ * ------------------------------------------------------------------------- */
+typedef struct fp_stream fp_stream;
+typedef struct {
+  uint64_t bytes;         /* stream length = file size                         */
+  uint64_t direct_bytes;  /* written by the engine (O_DIRECT unless fallback)  */
+  uint64_t suffix_bytes;  /* written by the buffered descriptor (< alignment)  */
+  double t_total;         /* open -> close return, s                           */
+  double t_fill;          /* copying into the IO buffer (memcpy or D2H), s     */
+  double t_io_wait;       /* waiting for a slot's writes to complete, s        */
+  double t_fsync;         /* final fdatasync, s                                */
+  uint32_t fallback;      /* 1: the file system refused O_DIRECT (buffered)    */
+  uint32_t requests;      /* engine write requests                             */
+} fp_stream_stats;
+
+/* Create / truncate `path` and allocate the IO buffer (ring_slots x
+ * slot_bytes; cfg NULL = defaults). cuda_device >= 0 also registers the
+ * buffer with CUDA for fp_stream_write_device (page-locked); -1 = host
+ * bytes only. Errors: -EINVAL (bad cfg), -ENOMEM, -errno of open, FP_ECUDA. */
+int fp_stream_open(const fp_config *cfg, int cuda_device, const char *path, fp_stream **out);
+/* Append n host bytes (copied into the IO buffer; returns once they are
+ * copied — full slots are written asynchronously). -EIO / -errno of a failed
+ * earlier write (the stream is then failed; close still frees it).          */
+int fp_stream_write(fp_stream *s, const void *buf, uint64_t n);
+/* Append n bytes of device memory: copy-engine D2H straight into the
+ * page-locked IO buffer on `stream` (cudaStream_t), slot by slot (GPU
+ * -> page-locked CPU memory -> NVMe). Needs cuda_device >= 0 at open.
+ * Synchronous with respect to the copies. -EINVAL without a device.        */
+int fp_stream_write_device(fp_stream *s, const void *dev_ptr, uint64_t n, void *stream);
+/* Flush (aligned prefix O_DIRECT, suffix buffered), fdatasync, close, free.
+ * Always frees s. Returns 0 or the first error; *st (nullable) filled.      */
+int fp_stream_close(fp_stream *s, fp_stream_stats *st);
+
 #ifdef __cplusplus
 }
 #endif

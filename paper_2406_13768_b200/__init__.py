@@ -4,5 +4,5 @@ Native library (csrc/, C-ABI in include/fastpersist.h) + this thin ctypes
 binding. See DESIGN.md.
 """
 from .fastpersist import (  # noqa: F401
-    Checkpointer, Entry, FastPersistError, io_bench, lib, LIB_PATH, EXPORTS,
+    Checkpointer, Entry, FastPersistError, io_bench, lib, LIB_PATH, EXPORTS, StreamWriter, save,
 )

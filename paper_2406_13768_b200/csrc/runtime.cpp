@@ -32,6 +32,7 @@
 #include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
+#include <deque>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -1287,6 +1288,253 @@ int fp_io_bench(const char* dir, uint64_t bytes, const fp_config* cfg, int tag, 
 int fp_io_bench_read(const char* dir, uint64_t bytes, const fp_config* cfg, int tag,
                      double* gbps) {
   return io_bench(dir, bytes, cfg, tag, true, gbps);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// fp_stream: a sequential byte stream written through the IO buffer with
+// O_DIRECT (the paper's torch.save integration, §5.1; single /
+// double buffering P:467-473; prefix / suffix P:477). See fastpersist.h.
+// ---------------------------------------------------------------------------
+struct fp_stream {
+  struct Req {
+    uint32_t slot, len;
+    uint64_t off;  // file offset; the buffer is ring + slot * slot_bytes + (off - base)
+    uint64_t base;
+  };
+  fp_config cfg{};
+  IoEngine* io = nullptr;
+  uint8_t* ring = nullptr;
+  size_t ring_bytes = 0;
+  bool registered = false;  // cudaHostRegister'd (write_device)
+  int fd = -1;
+  std::string path;
+  uint32_t cur = 0;          // slot being filled
+  uint64_t fill = 0;         // bytes in it
+  uint64_t slot_off = 0;     // file offset of its first byte
+  uint32_t inflight = 0;     // engine requests in flight
+  std::deque<Req> pending;   // requests of handed-off slots not yet queued
+  std::vector<uint32_t> busy;  // requests per slot, pending or in flight
+  int status = 0;
+  double t0 = 0;
+  fp_stream_stats st{};
+};
+
+namespace {
+
+constexpr uint64_t kStreamPiece = 4ull << 20;
+
+// queue pending requests up to the engine's depth (io_depth in flight)
+void stream_pump(fp_stream* s) {
+  bool any = false;
+  while (!s->pending.empty() && s->inflight < s->io->capacity() && !s->status) {
+    const fp_stream::Req& q = s->pending.front();
+    uint8_t* buf = s->ring + (size_t)q.slot * s->cfg.slot_bytes + (q.off - q.base);
+    if (s->io->queue(true, s->fd, buf, q.len, q.off, (int)q.slot, ((uint64_t)q.slot << 32) | q.len))
+      break;  // submission queue full: after the next reap
+    ++s->inflight;
+    s->st.direct_bytes += q.len;
+    ++s->st.requests;
+    s->pending.pop_front();
+    any = true;
+  }
+  if (any) s->io->submit();
+}
+
+// reap at least `min_wait` completions (requests carry (slot << 32) | len),
+// then top the engine up again
+int stream_reap(fp_stream* s, int min_wait) {
+  IoDone done[64];
+  const double tw = now_s();
+  const int k = s->io->reap(done, 64, min_wait);
+  s->st.t_io_wait += now_s() - tw;
+  if (k < 0) return s->status = s->status ? s->status : k;
+  for (int i = 0; i < k; ++i) {
+    --s->busy[done[i].user >> 32];
+    --s->inflight;
+    if (done[i].res != (int32_t)(uint32_t)done[i].user && !s->status)
+      s->status = done[i].res < 0 ? done[i].res : -EIO;
+  }
+  stream_pump(s);
+  return s->status;
+}
+
+// hand [0, len) of slot `slot` (file offset `off`; len a multiple of the
+// alignment) to the engine as sqe_bytes requests; returns without waiting
+int stream_submit(fp_stream* s, uint32_t slot, uint64_t len, uint64_t off) {
+  for (uint64_t o = 0; o < len; o += s->cfg.sqe_bytes) {
+    const uint32_t n = (uint32_t)std::min<uint64_t>(s->cfg.sqe_bytes, len - o);
+    s->pending.push_back({slot, n, off + o, off});
+    ++s->busy[slot];
+  }
+  stream_pump(s);
+  return s->status;
+}
+
+int stream_wait_slot(fp_stream* s, uint32_t slot) {
+  while (s->busy[slot] && !s->status) {
+    if (!s->inflight) stream_pump(s);
+    if (stream_reap(s, 1)) break;
+  }
+  return s->status;
+}
+
+// the current slot is full: hand it to the engine, move to the next one
+// (waiting for its previous writes: with one slot this is the paper's
+// single-buffer mode, with two the next slot fills while this one is written)
+int stream_advance(fp_stream* s) {
+  if (stream_submit(s, s->cur, s->fill, s->slot_off)) return s->status;
+  s->slot_off += s->fill;
+  s->fill = 0;
+  s->cur = (s->cur + 1) % s->cfg.ring_slots;
+  return stream_wait_slot(s, s->cur);
+}
+
+}  // namespace
+
+extern "C" {
+
+int fp_stream_open(const fp_config* cfg_in, int cuda_device, const char* path, fp_stream** out) {
+  if (!path || !out) return -EINVAL;
+  *out = nullptr;
+  fp_config cfg;
+  if (cfg_in)
+    cfg = *cfg_in;
+  else
+    fp_config_default(&cfg);
+  int r = check_cfg(cfg);
+  if (r) return r;
+  if (cfg.io_engine == FP_IO_GDS) cfg.io_engine = FP_IO_URING;  // host buffer: the ring engine
+  fp_stream* s = new fp_stream();
+  s->t0 = now_s();
+  s->cfg = cfg;
+  s->path = path;
+  s->ring_bytes = (size_t)cfg.ring_slots * cfg.slot_bytes;
+  s->ring = alloc_ring(s->ring_bytes, -1);
+  if (!s->ring) {
+    delete s;
+    return -ENOMEM;
+  }
+  s->busy.assign(cfg.ring_slots, 0);
+  auto fail = [&](int e) {
+    if (s->fd >= 0) close(s->fd);
+    if (s->registered) cudaHostUnregister(s->ring);
+    munmap(s->ring, s->ring_bytes);
+    delete s->io;
+    delete s;
+    return e;
+  };
+  if (cuda_device >= 0) {
+    if (cudaSetDevice(cuda_device) != cudaSuccess ||
+        cudaHostRegister(s->ring, s->ring_bytes, cudaHostRegisterDefault) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(FP_ECUDA);
+    }
+    s->registered = true;
+  }
+  const bool direct = cfg.io_engine != FP_IO_BUFFERED;
+  s->fd = open(path, O_WRONLY | O_CREAT | O_TRUNC | (direct ? O_DIRECT : 0), 0644);
+  if (s->fd < 0 && direct && errno == EINVAL) {  // no O_DIRECT on this file system
+    s->fd = open(path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
+    s->st.fallback = 1;
+  }
+  if (s->fd < 0) return fail(-errno);
+  int kind = 0;
+  s->io = open_engine(cfg, &kind);
+  s->io->register_buffers(s->ring, cfg.slot_bytes, cfg.ring_slots);
+  *out = s;
+  return 0;
+}
+
+int fp_stream_write(fp_stream* s, const void* buf, uint64_t n) {
+  if (!s || (!buf && n)) return -EINVAL;
+  const uint8_t* p = (const uint8_t*)buf;
+  while (n && !s->status) {
+    // at most 4 MiB per copy, then the completions that arrived meanwhile
+    // are reaped and the engine topped up (a long copy must not drain it)
+    const uint64_t m = std::min<uint64_t>({n, s->cfg.slot_bytes - s->fill, kStreamPiece});
+    const double tc = now_s();
+    memcpy(s->ring + (size_t)s->cur * s->cfg.slot_bytes + s->fill, p, m);
+    s->st.t_fill += now_s() - tc;
+    if (s->inflight) stream_reap(s, 0);
+    s->fill += m;
+    s->st.bytes += m;
+    p += m;
+    n -= m;
+    if (s->fill == s->cfg.slot_bytes) stream_advance(s);
+  }
+  return s->status;
+}
+
+int fp_stream_write_device(fp_stream* s, const void* dev_ptr, uint64_t n, void* stream) {
+  if (!s || (!dev_ptr && n)) return -EINVAL;
+  if (!s->registered) return -EINVAL;
+  const uint8_t* p = (const uint8_t*)dev_ptr;
+  cudaStream_t cs = (cudaStream_t)stream;
+  while (n && !s->status) {
+    const uint64_t m = std::min<uint64_t>({n, s->cfg.slot_bytes - s->fill, 4 * kStreamPiece});
+    const double tc = now_s();
+    if (cudaMemcpyAsync(s->ring + (size_t)s->cur * s->cfg.slot_bytes + s->fill, p, m,
+                        cudaMemcpyDeviceToHost, cs) != cudaSuccess ||
+        cudaStreamSynchronize(cs) != cudaSuccess) {
+      cudaGetLastError();
+      s->status = FP_ECUDA;
+      break;
+    }
+    s->st.t_fill += now_s() - tc;
+    if (s->inflight) stream_reap(s, 0);
+    s->fill += m;
+    s->st.bytes += m;
+    p += m;
+    n -= m;
+    if (s->fill == s->cfg.slot_bytes) stream_advance(s);
+  }
+  return s->status;
+}
+
+int fp_stream_close(fp_stream* s, fp_stream_stats* st) {
+  if (!s) return -EINVAL;
+  const uint64_t A = s->cfg.alignment;
+  const uint64_t pre = s->fill / A * A, suf = s->fill - pre;
+  if (!s->status && pre) stream_submit(s, s->cur, pre, s->slot_off);
+  for (uint32_t i = 0; i < s->cfg.ring_slots; ++i) stream_wait_slot(s, i);
+  if (!s->status && suf) {
+    // the < alignment suffix through a buffered descriptor of the same file
+    int bfd = open(s->path.c_str(), O_WRONLY);
+    if (bfd < 0) {
+      s->status = -errno;
+    } else {
+      const uint8_t* p = s->ring + (size_t)s->cur * s->cfg.slot_bytes + pre;
+      uint64_t done = 0;
+      while (done < suf) {
+        const ssize_t w = pwrite(bfd, p + done, suf - done, (off_t)(s->slot_off + pre + done));
+        if (w < 0 && errno == EINTR) continue;
+        if (w <= 0) {
+          s->status = w < 0 ? -errno : -EIO;
+          break;
+        }
+        done += (uint64_t)w;
+      }
+      if (!s->status && fdatasync(bfd)) s->status = -errno;
+      close(bfd);
+      s->st.suffix_bytes = suf;
+    }
+  }
+  if (!s->status && !(s->cfg.flags & FP_CFG_NO_FSYNC)) {
+    const double tf = now_s();
+    s->status = s->io->fdatasync(s->fd);
+    s->st.t_fsync = now_s() - tf;
+  }
+  close(s->fd);
+  if (s->registered) cudaHostUnregister(s->ring);
+  munmap(s->ring, s->ring_bytes);
+  delete s->io;
+  s->st.t_total = now_s() - s->t0;
+  if (st) *st = s->st;
+  const int r = s->status;
+  delete s;
+  return r;
 }
 
 }  // extern "C"

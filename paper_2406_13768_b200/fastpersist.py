@@ -17,9 +17,11 @@ PAPER.md §4.3 P:511-515 (begin after optimizer, wait before the next one);
 from __future__ import annotations
 
 import ctypes as C
+import io
 import os
 from collections import namedtuple
 
+import numpy as np
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -112,7 +114,14 @@ EXCHANGES = {0: "none", 1: "allgather_bytes", 2: "peer"}
 
 EXPORTS = ("fp_config_default", "fp_ckpt_init", "fp_ckpt_begin", "fp_ckpt_fence", "fp_ckpt_wait",
            "fp_ckpt_load", "fp_ckpt_load_parallel", "fp_ckpt_load_stats", "fp_ckpt_plan_info",
-           "fp_ckpt_destroy", "fp_strerror", "fp_io_bench", "fp_io_bench_read")
+           "fp_ckpt_destroy", "fp_strerror", "fp_io_bench", "fp_io_bench_read",
+           "fp_stream_open", "fp_stream_write", "fp_stream_write_device", "fp_stream_close")
+
+
+class fp_stream_stats(C.Structure):
+    _fields_ = [("bytes", C.c_uint64), ("direct_bytes", C.c_uint64), ("suffix_bytes", C.c_uint64),
+                ("t_total", C.c_double), ("t_fill", C.c_double), ("t_io_wait", C.c_double),
+                ("t_fsync", C.c_double), ("fallback", C.c_uint32), ("requests", C.c_uint32)]
 
 _lib = None
 
@@ -148,6 +157,11 @@ def lib():
                               C.POINTER(C.c_double)]
     L.fp_io_bench_read.argtypes = [C.c_char_p, C.c_uint64, C.POINTER(fp_config), C.c_int,
                                    C.POINTER(C.c_double)]
+    L.fp_stream_open.argtypes = [C.POINTER(fp_config), C.c_int, C.c_char_p,
+                                 C.POINTER(C.c_void_p)]
+    L.fp_stream_write.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64]
+    L.fp_stream_write_device.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]
+    L.fp_stream_close.argtypes = [C.c_void_p, C.POINTER(fp_stream_stats)]
     _lib = L
     return L
 
@@ -469,3 +483,77 @@ def io_bench(directory, nbytes, tag=0, read=False, **cfg):
     _check(fn(os.fsencode(directory), int(nbytes), C.byref(c), int(tag), C.byref(g)),
            "fp_io_bench_read" if read else "fp_io_bench")
     return g.value
+
+
+class StreamWriter(io.RawIOBase):
+    """Write-only file object over fp_stream (the paper's torch.save
+    integration, §5.1): ``torch.save(obj, StreamWriter(path))``
+    serialises as usual and every byte goes through the IO buffer with
+    O_DIRECT. ``io_buffer_bytes`` = slot size, ``double_buffer``
+    = 2 slots (False: the single-buffer mode). ``device`` (CUDA index) enables
+    ``write_tensor``: a device tensor's bytes D2H'd straight into the
+    page-locked buffer. ``close()`` flushes, fsyncs and returns the stats."""
+
+    def __init__(self, path, io_buffer_bytes=None, double_buffer=True, device=None, **cfg):
+        super().__init__()
+        if io_buffer_bytes is not None:
+            cfg["slot_bytes"] = int(io_buffer_bytes)
+        cfg.setdefault("ring_slots", 2 if double_buffer else 1)
+        c = make_config(**cfg)
+        self._dev = None if device is None else torch.device("cuda", torch.device(device).index or 0
+                                                             if not isinstance(device, int) else device)
+        h = C.c_void_p()
+        _check(lib().fp_stream_open(C.byref(c), -1 if self._dev is None else self._dev.index,
+                                    os.fsencode(path), C.byref(h)), "fp_stream_open")
+        self._h = h
+        self.stats = None
+
+    def writable(self):
+        return True
+
+    def write(self, b):
+        if self._h is None:
+            raise ValueError("write to a closed StreamWriter")
+        a = np.frombuffer(b, dtype=np.uint8)  # no copy, read-only buffers too
+        if a.size:
+            _check(lib().fp_stream_write(self._h, a.ctypes.data, a.size), "fp_stream_write")
+        return a.size
+
+    def write_tensor(self, t):
+        """Append the raw bytes of a contiguous device tensor (D2H into the IO
+        buffer on the current stream)."""
+        if self._dev is None or not t.is_cuda or not t.is_contiguous():
+            raise ValueError("write_tensor needs a contiguous CUDA tensor and device= at open")
+        n = t.numel() * t.element_size()
+        st = torch.cuda.current_stream(t.device).cuda_stream
+        _check(lib().fp_stream_write_device(self._h, t.data_ptr(), n, st), "fp_stream_write_device")
+        return n
+
+    def close(self):
+        if self._h is not None:
+            h, self._h = self._h, None
+            s = fp_stream_stats()
+            code = lib().fp_stream_close(h, C.byref(s))
+            self.stats = {k: getattr(s, k) for k, _ in fp_stream_stats._fields_}
+            super().close()
+            _check(code, "fp_stream_close")
+        return self.stats
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - never raise from a finaliser
+            pass
+
+
+def save(obj, path, **kw):
+    """torch.save(obj, path) through StreamWriter; returns the stream stats."""
+    w = StreamWriter(path, **kw)
+    try:
+        torch.save(obj, w)
+    except BaseException:
+        try:
+            w.close()
+        finally:
+            raise
+    return w.close()

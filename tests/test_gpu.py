@@ -680,3 +680,35 @@ def test_bench_json_line_contract(tmp_path):
     assert d["restore"]["value"] > 0, d["restore"]
     for k in ("sm_mhz", "sm_max_mhz", "reasons"):
         assert k in d["clocks"], k
+
+
+@pytest.mark.parametrize("slots", [1, 2])
+@pytest.mark.parametrize("nbytes", [1, 4095, 4096 * 3, (16 << 20) + 7])
+def test_stream_write_tensor_parity(tmp_path, slots, nbytes):
+    """fp_stream_write_device: a device tensor's bytes D2H'd straight into the
+    page-locked IO buffer and written with O_DIRECT, the unaligned
+    tail through the buffered descriptor: file == tensor bytes."""
+    g = torch.Generator(device=DEV).manual_seed(nbytes + slots)
+    t = torch.randint(0, 256, (nbytes,), dtype=torch.uint8, device=DEV, generator=g)
+    p = str(tmp_path / "t.bin")
+    w = fp.StreamWriter(p, io_buffer_bytes=1 << 20, ring_slots=slots, device=0)
+    w.write_tensor(t[: nbytes // 2])
+    w.write(t[nbytes // 2: nbytes // 2 + 3].cpu().numpy().tobytes())   # host bytes in between
+    w.write_tensor(t[nbytes // 2 + 3:])
+    st = w.close()
+    assert open(p, "rb").read() == t.cpu().numpy().tobytes()
+    assert st["bytes"] == nbytes and st["suffix_bytes"] == nbytes % 4096
+
+
+def test_stream_torch_save_cuda_state(tmp_path):
+    """torch.save of a CUDA state dict through StreamWriter == torch.save into
+    a file object, and torch.load restores it on the GPU."""
+    import io as _io
+    st = {x.name: t for x, t in _state("gpt3_small")}
+    p = str(tmp_path / "s.pt")
+    fp.save(st, p, io_buffer_bytes=8 << 20)
+    ref = _io.BytesIO()
+    torch.save(st, ref)
+    assert file_sha(p) == __import__("hashlib").sha256(ref.getvalue()).hexdigest()
+    back = torch.load(p, map_location=DEV)
+    assert all(torch.equal(back[k], v) for k, v in st.items())
