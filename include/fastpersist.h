@@ -388,10 +388,14 @@ typedef struct {
   uint32_t requests;      /* engine write requests                             */
 } fp_stream_stats;
 
-/* Create / truncate `path` and allocate the IO buffer (ring_slots x
+/* Create or overwrite `path` (an existing file is overwritten in place and
+ * cut to the stream's length at close) and allocate the IO buffer (ring_slots x
  * slot_bytes; cfg NULL = defaults). cuda_device >= 0 also registers the
  * buffer with CUDA for fp_stream_write_device (page-locked); -1 = host
- * bytes only. Errors: -EINVAL (bad cfg), -ENOMEM, -errno of open, FP_ECUDA. */
+ * bytes only. The buffer of a closed stream is kept (two at most) and reused
+ * by the next stream of the same ring shape, as the paper's helper allocates
+ * its page-locked buffer once. Errors: -EINVAL (bad cfg), -ENOMEM,
+ * -errno of open, FP_ECUDA.                                                  */
 int fp_stream_open(const fp_config *cfg, int cuda_device, const char *path, fp_stream **out);
 /* Append n host bytes (copied into the IO buffer; returns once they are
  * copied — full slots are written asynchronously). -EIO / -errno of a failed

@@ -1325,6 +1325,42 @@ namespace {
 
 constexpr uint64_t kStreamPiece = 4ull << 20;
 
+// IO buffers of closed streams, kept for the next stream of the same shape
+// (the paper's helper allocates its page-locked buffer once): two
+// entries at most; a cached buffer stays CUDA-registered if it was.
+struct RingCacheEntry {
+  uint8_t* ring;
+  size_t bytes;
+  bool registered;
+};
+std::mutex g_ring_cache_mu;
+std::vector<RingCacheEntry> g_ring_cache;
+
+uint8_t* ring_cache_take(size_t bytes, bool want_registered, bool* registered) {
+  std::lock_guard<std::mutex> g(g_ring_cache_mu);
+  for (size_t i = 0; i < g_ring_cache.size(); ++i)
+    if (g_ring_cache[i].bytes == bytes && (g_ring_cache[i].registered || !want_registered)) {
+      RingCacheEntry e = g_ring_cache[i];
+      g_ring_cache.erase(g_ring_cache.begin() + (long)i);
+      *registered = e.registered;
+      return e.ring;
+    }
+  return nullptr;
+}
+
+void ring_cache_put(uint8_t* ring, size_t bytes, bool registered) {
+  RingCacheEntry ev{nullptr, 0, false};
+  {
+    std::lock_guard<std::mutex> g(g_ring_cache_mu);
+    g_ring_cache.push_back({ring, bytes, registered});
+    if (g_ring_cache.size() <= 2) return;
+    ev = g_ring_cache.front();
+    g_ring_cache.erase(g_ring_cache.begin());
+  }
+  if (ev.registered) cudaHostUnregister(ev.ring);
+  munmap(ev.ring, ev.bytes);
+}
+
 // queue pending requests up to the engine's depth (io_depth in flight)
 void stream_pump(fp_stream* s) {
   bool any = false;
@@ -1411,7 +1447,8 @@ int fp_stream_open(const fp_config* cfg_in, int cuda_device, const char* path, f
   s->cfg = cfg;
   s->path = path;
   s->ring_bytes = (size_t)cfg.ring_slots * cfg.slot_bytes;
-  s->ring = alloc_ring(s->ring_bytes, -1);
+  s->ring = ring_cache_take(s->ring_bytes, cuda_device >= 0, &s->registered);
+  if (!s->ring) s->ring = alloc_ring(s->ring_bytes, -1);
   if (!s->ring) {
     delete s;
     return -ENOMEM;
@@ -1427,16 +1464,21 @@ int fp_stream_open(const fp_config* cfg_in, int cuda_device, const char* path, f
   };
   if (cuda_device >= 0) {
     if (cudaSetDevice(cuda_device) != cudaSuccess ||
-        cudaHostRegister(s->ring, s->ring_bytes, cudaHostRegisterDefault) != cudaSuccess) {
+        (!s->registered &&
+         cudaHostRegister(s->ring, s->ring_bytes, cudaHostRegisterDefault) != cudaSuccess)) {
       cudaGetLastError();
       return fail(FP_ECUDA);
     }
     s->registered = true;
   }
+  // No O_TRUNC: an existing file is overwritten in place and cut to the
+  // stream's length at close, so its blocks are not freed (and discarded)
+  // only to be allocated again — the same in-place overwrite as a rotated
+  // checkpoint generation
   const bool direct = cfg.io_engine != FP_IO_BUFFERED;
-  s->fd = open(path, O_WRONLY | O_CREAT | O_TRUNC | (direct ? O_DIRECT : 0), 0644);
+  s->fd = open(path, O_WRONLY | O_CREAT | (direct ? O_DIRECT : 0), 0644);
   if (s->fd < 0 && direct && errno == EINVAL) {  // no O_DIRECT on this file system
-    s->fd = open(path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
+    s->fd = open(path, O_WRONLY | O_CREAT, 0644);
     s->st.fallback = 1;
   }
   if (s->fd < 0) return fail(-errno);
@@ -1521,14 +1563,14 @@ int fp_stream_close(fp_stream* s, fp_stream_stats* st) {
       s->st.suffix_bytes = suf;
     }
   }
+  if (!s->status && ftruncate(s->fd, (off_t)s->st.bytes)) s->status = -errno;
   if (!s->status && !(s->cfg.flags & FP_CFG_NO_FSYNC)) {
     const double tf = now_s();
     s->status = s->io->fdatasync(s->fd);
     s->st.t_fsync = now_s() - tf;
   }
   close(s->fd);
-  if (s->registered) cudaHostUnregister(s->ring);
-  munmap(s->ring, s->ring_bytes);
+  ring_cache_put(s->ring, s->ring_bytes, s->registered);
   delete s->io;
   s->st.t_total = now_s() - s->t0;
   if (st) *st = s->st;

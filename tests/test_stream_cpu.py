@@ -95,3 +95,15 @@ def test_buffered_engine_and_no_fsync(tmp_path):
     p = str(tmp_path / "b.pt")
     fp.save(obj, p, io_engine="buffered", no_fsync=True)
     assert open(p, "rb").read() == _torch_save_bytes(obj)
+
+
+def test_overwrite_longer_file_is_cut(tmp_path):
+    """An existing longer file is overwritten in place and cut to the new
+    stream's length (no stale tail)."""
+    p = str(tmp_path / "o.bin")
+    with open(p, "wb") as f:
+        f.write(b"\xab" * 300000)
+    w = fp.StreamWriter(p, io_buffer_bytes=8192)
+    w.write(b"x" * 12345)
+    w.close()
+    assert open(p, "rb").read() == b"x" * 12345

@@ -57,6 +57,10 @@ def torch_save(t):
         os.fsync(f.fileno())
 
 
+roof = fp.io_bench(a.dir, 2 << 30, tag=7)  # same-run O_DIRECT write roofline (64 x 1 MiB)
+print(json.dumps({"kind": "nvme_roofline", "gbs": round(roof, 3),
+                  "how": "fp_io_bench: 2 GiB O_DIRECT io_uring seq overwrite, 64 x 1 MiB"}),
+      flush=True)
 rows = []
 for mb in [int(x) for x in a.sizes_mb.split(",")]:
     n = mb << 20
@@ -70,16 +74,21 @@ for mb in [int(x) for x in a.sizes_mb.split(",")]:
             def fp_save():
                 fp.save(t, path, io_buffer_bytes=bmb << 20, ring_slots=slots)
 
+            last = {}
+
             def fp_raw():
                 w = fp.StreamWriter(path, io_buffer_bytes=bmb << 20, ring_slots=slots, device=0)
                 w.write_tensor(t)
-                w.close()
+                last.update(w.close())
             for kind, fn in (("fp_save", fp_save), ("fp_raw", fp_raw)):
                 r = timed(fn)
                 rows.append({"kind": kind, "tensor_mb": mb, "buffer_mb": bmb,
                              "mode": "double" if slots == 2 else "single",
                              "gbs": round(n / r[0] / 1e9, 3), "s": [round(x, 4) for x in r],
                              "speedup_vs_torch_save": round(base[0] / r[0], 2)})
+                if kind == "fp_raw":
+                    rows[-1]["last_stats_s"] = {k: round(last[k], 4) for k in
+                                                ("t_total", "t_fill", "t_io_wait", "t_fsync")}
                 print(json.dumps(rows[-1]), flush=True)
     del t
     torch.cuda.empty_cache()
@@ -91,5 +100,8 @@ for r in rows:
         best[k] = max(best.get(k, 0), r["speedup_vs_torch_save"])
 print(json.dumps({"summary": "best speedup over torch.save per (kind, tensor MB, mode)",
                   "best": {f"{k[0]}/{k[1]}MB/{k[2]}": v for k, v in sorted(best.items())},
+                  "nvme_roofline_gbs": round(roof, 3),
+                  "best_raw_frac_of_roofline": round(max(r["gbs"] for r in rows
+                                                         if r["kind"] == "fp_raw") / roof, 3),
                   "paper_context": "1.8-3.6x single, 1.8-6.6x double buffer (V100, P:613)"}),
       flush=True)
