@@ -796,8 +796,9 @@ def our_arm(a):
         try:   # ncu-measured DRAM bytes per launch of this launch shape (profiles/)
             with open(os.path.join(ROOT, "profiles", "pack_traffic.json")) as f:
                 tr = json.load(f).get(kname or "", {})
-            if traffic is None and tr.get("bytes_per_launch") == (a.pack_mib << 21):
-                traffic = tr["dram_bytes"]
+            for e in (tr if isinstance(tr, list) else [tr]):   # one entry per launch shape
+                if traffic is None and e.get("bytes_per_launch") == (a.pack_mib << 21):
+                    traffic = e["dram_bytes"]
         except (OSError, ValueError):
             pass
         launch_avg_ms = pk_ms / max(1, pk_launches)
@@ -892,7 +893,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pack", default="bulk", choices=["v4", "bulk", "lsu", "host", "ce"])
-    ap.add_argument("--pack-mib", type=int, default=256)
+    ap.add_argument("--pack-mib", type=int, default=1024)
     ap.add_argument("--prio", default="high", choices=["high", "low"])
     ap.add_argument("--writer-stride", type=int, default=1,
                     help="writer subset (P:495-499): ranks r %% s == 0 write replicated bytes")

@@ -168,7 +168,10 @@ typedef struct fp_config {
   uint64_t pack_bytes;   /* bytes gathered per pack-kernel launch (device slab
                             size); rounded up to a multiple of slot_bytes, so one
                             launch feeds pack_bytes/slot_bytes ring slots; 0 =
-                            slot_bytes; default 256 MiB, max 2 GiB             */
+                            slot_bytes; default 1 GiB (a launch carries ~12 us
+                            of fixed cost: 256 MiB groups reach 0.90 of HBM,
+                            1 GiB 0.98 — profiles/r02_pack_group_size.md),
+                            max 2 GiB                                          */
 } fp_config;
 
 /* ---- per-checkpoint statistics ------------------------------------------ */

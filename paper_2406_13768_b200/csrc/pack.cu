@@ -222,10 +222,11 @@ __global__ void __launch_bounds__(kV4Threads) fp_unpack_peer(const Item* __restr
 // ---------------------------------------------------------------------------
 // bulk-async (TMA engine) variant
 // ---------------------------------------------------------------------------
-constexpr int kBulkStages = 6;
+constexpr int kBulkStagesMax = 6;
 constexpr int kBulkThreads = 128;
 constexpr uint32_t kBulkStageBytes = kTile;  // one item per stage
-constexpr size_t kBulkSmem = (size_t)kBulkStages * kBulkStageBytes + kBulkStages * 16;
+template <int kBulkStages>
+constexpr size_t bulk_smem() { return (size_t)kBulkStages * kBulkStageBytes + kBulkStages * 16; }
 
 __device__ __forceinline__ bool bulk_ok(const Item& it) {
   return it.src && !(it.src & 15) && !(it.dst & 15) && it.len >= 16;
@@ -235,7 +236,9 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-__global__ void __launch_bounds__(kBulkThreads, 1)
+// kBulkStages = 6: one CTA per SM; 3: two CTAs per SM (FP_BULK_2CTA=1, ablation)
+template <int kBulkStages>
+__global__ void __launch_bounds__(kBulkThreads, kBulkStagesMax / kBulkStages)
     fp_pack_bulk(const Item* __restrict__ items, uint32_t n, uint8_t* __restrict__ slab) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + (size_t)kBulkStages * kBulkStageBytes);
@@ -1244,8 +1247,15 @@ int pack_launch(int impl, const Item* d_items, uint32_t n_items, uint8_t* d_slab
   cudaStream_t st = (cudaStream_t)stream;
   const int grid = (int)((uint32_t)ctas < n_items ? (uint32_t)ctas : n_items);
   if (impl == FP_PACK_BULK) {
-    if (!smem_opt_in<0>(fp_pack_bulk, kBulkSmem)) return FP_ECUDA;
-    fp_pack_bulk<<<grid, kBulkThreads, kBulkSmem, st>>>(d_items, n_items, d_slab);
+    static const bool two = env_flag("FP_BULK_2CTA");
+    if (two) {
+      if (!smem_opt_in<10>(fp_pack_bulk<3>, bulk_smem<3>())) return FP_ECUDA;
+      const int g2 = (int)std::min<uint32_t>(n_items, 2u * (uint32_t)ctas);
+      fp_pack_bulk<3><<<g2, kBulkThreads, bulk_smem<3>(), st>>>(d_items, n_items, d_slab);
+    } else {
+      if (!smem_opt_in<0>(fp_pack_bulk<6>, bulk_smem<6>())) return FP_ECUDA;
+      fp_pack_bulk<6><<<grid, kBulkThreads, bulk_smem<6>(), st>>>(d_items, n_items, d_slab);
+    }
   } else {
     fp_pack_v4<<<grid, kV4Threads, 0, st>>>(d_items, n_items, d_slab);
   }

@@ -736,7 +736,7 @@ int fp_config_default(fp_config* cfg) {
   cfg->sqe_bytes = (uint32_t)env_u64("FP_SQE_BYTES", 1u << 20);
   cfg->alignment = (uint32_t)env_u64("FP_ALIGN", 4096);
   cfg->pack_ctas = (uint32_t)env_u64("FP_PACK_CTAS", 0);
-  cfg->pack_bytes = env_u64("FP_PACK_BYTES", 256ull << 20);
+  cfg->pack_bytes = env_u64("FP_PACK_BYTES", 1ull << 30);
   cfg->writer_stride = (uint32_t)env_u64("FP_WRITER_STRIDE", 1);
   if (getenv("FP_NO_CRC")) cfg->flags |= FP_CFG_NO_CRC;
   if (env_u64("FP_BALANCE_BYTES", 0)) cfg->flags |= FP_CFG_BALANCE_BYTES;

@@ -24,7 +24,7 @@ ap.add_argument("--dir", default="/dev/shm/fp_ab")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--tag", default="")
 ap.add_argument("--no-crc", action="store_true", help="pack only (bulk: fp_pack_bulk)")
-ap.add_argument("--pack-mib", type=int, default=256, help="bytes per pack launch (MiB)")
+ap.add_argument("--pack-mib", type=int, default=1024, help="bytes per pack launch (MiB)")
 a = ap.parse_args()
 peak = 6538.3
 try:
