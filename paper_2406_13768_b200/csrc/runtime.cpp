@@ -1463,9 +1463,12 @@ int fp_stream_open(const fp_config* cfg_in, int cuda_device, const char* path, f
     return e;
   };
   if (cuda_device >= 0) {
-    if (cudaSetDevice(cuda_device) != cudaSuccess ||
+    // portable registration: page-locked for every device, and the caller's
+    // current device is left alone
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device >= ndev ||
         (!s->registered &&
-         cudaHostRegister(s->ring, s->ring_bytes, cudaHostRegisterDefault) != cudaSuccess)) {
+         cudaHostRegister(s->ring, s->ring_bytes, cudaHostRegisterPortable) != cudaSuccess)) {
       cudaGetLastError();
       return fail(FP_ECUDA);
     }

@@ -500,8 +500,11 @@ class StreamWriter(io.RawIOBase):
             cfg["slot_bytes"] = int(io_buffer_bytes)
         cfg.setdefault("ring_slots", 2 if double_buffer else 1)
         c = make_config(**cfg)
-        self._dev = None if device is None else torch.device("cuda", torch.device(device).index or 0
-                                                             if not isinstance(device, int) else device)
+        if device is None:
+            self._dev = None
+        else:
+            idx = device if isinstance(device, int) else (torch.device(device).index or 0)
+            self._dev = torch.device("cuda", idx)
         h = C.c_void_p()
         _check(lib().fp_stream_open(C.byref(c), -1 if self._dev is None else self._dev.index,
                                     os.fsencode(path), C.byref(h)), "fp_stream_open")
