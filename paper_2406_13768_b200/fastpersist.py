@@ -549,14 +549,25 @@ class StreamWriter(io.RawIOBase):
             pass
 
 
-def save(obj, path, **kw):
-    """torch.save(obj, path) through StreamWriter; returns the stream stats."""
-    w = StreamWriter(path, **kw)
+def save(obj, path, zip_crc32=True, pinned_d2h=False, **kw):
+    """torch.save(obj, path) through StreamWriter; returns the stream stats.
+
+    zip_crc32 / pinned_d2h are torch.save's own serializer switches
+    (torch.utils.serialization.config.save.compute_crc32 /
+    use_pinned_memory_for_d2h), set for this call only. The defaults give
+    exactly torch.save's bytes; zip_crc32=False skips the zip records' CRC-32
+    (torch.load does not check it; zip tools then report bad CRCs) and
+    pinned_d2h=True stages CUDA storages through pinned memory — the two costs
+    that bound torch.save once the writes are fast."""
+    from torch.utils.serialization import config as tcfg
+    old = (tcfg.save.compute_crc32, tcfg.save.use_pinned_memory_for_d2h)
+    tcfg.save.compute_crc32, tcfg.save.use_pinned_memory_for_d2h = bool(zip_crc32), bool(pinned_d2h)
+    w = None
     try:
+        w = StreamWriter(path, **kw)
         torch.save(obj, w)
-    except BaseException:
-        try:
+        return w.close()
+    finally:
+        tcfg.save.compute_crc32, tcfg.save.use_pinned_memory_for_d2h = old
+        if w is not None:
             w.close()
-        finally:
-            raise
-    return w.close()

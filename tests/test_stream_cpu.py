@@ -107,3 +107,21 @@ def test_overwrite_longer_file_is_cut(tmp_path):
     w.write(b"x" * 12345)
     w.close()
     assert open(p, "rb").read() == b"x" * 12345
+
+
+def test_save_serializer_switches(tmp_path):
+    """zip_crc32=False (torch's own compute_crc32 switch, this call only):
+    the bytes equal torch.save under the same switch, torch.load reads them,
+    and the switch is restored afterwards."""
+    from torch.utils.serialization import config as tcfg
+    obj = _state(11)
+    p = str(tmp_path / "f.pt")
+    fp.save(obj, p, zip_crc32=False)
+    assert tcfg.save.compute_crc32 is True
+    tcfg.save.compute_crc32 = False
+    try:
+        ref = _torch_save_bytes(obj)
+    finally:
+        tcfg.save.compute_crc32 = True
+    assert open(p, "rb").read() == ref
+    assert torch.equal(torch.load(p)["w"], obj["w"])
