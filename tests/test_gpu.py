@@ -625,13 +625,15 @@ def test_crc_lsu_kernel_parity(tmp_path, slot, pack_bytes):
     _check_rank_files(str(tmp_path), lay, 1)
 
 
-@pytest.mark.parametrize("env", ["FP_NO_TMA", "FP_CRC_COL"])
+@pytest.mark.parametrize("env", ["FP_NO_TMA", "FP_CRC_COL", "FP_BULK_2CTA"])
 def test_crc_pages_variant_parity(tmp_path, env):
     """The other page-CRC kernels give the same CRC-32 as the default
     (fp_crc_pages_tma, a lane per 128-B row of a page) and zlib: FP_NO_TMA=1,
     the LSU kernel used when no tensor map can be encoded; FP_CRC_COL=1, the
-    TMA kernel with a lane per page (no lane combine). Child processes (both
-    switches are read once per process)."""
+    TMA kernel with a lane per page (no lane combine); FP_BULK_2CTA=1 (with
+    pack="bulk", no_crc): the bare TMA pack at two CTAs per SM, the shard
+    still == oracle. Child processes (the switches are read once per
+    process)."""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -640,9 +642,10 @@ def test_crc_pages_variant_parity(tmp_path, env):
             "from tests._util import entries, oracle_layout;"
             "from tests.test_gpu import _check_rank_files, _state;"
             "st=_state('gpt3_odd'); lay=oracle_layout([st],1); d=sys.argv[1];"
-            "ck=fp.Checkpointer(torch.device('cuda',0), slot_bytes=1<<20, pack_bytes=3<<20);"
-            "s=ck.save(entries(st), d); ck.close(); assert s['crc_valid'];"
-            "_check_rank_files(d, lay, 1); print('ok')")
+            "nc=os.environ.get('FP_BULK_2CTA')=='1';"
+            "ck=fp.Checkpointer(torch.device('cuda',0), slot_bytes=1<<20, pack_bytes=3<<20, no_crc=nc);"
+            "s=ck.save(entries(st), d); ck.close(); assert nc or s['crc_valid'];"
+            "_check_rank_files(d, lay, 1, crc=not nc); print('ok')")
     env = dict(os.environ, FP_ROOT=root, PYTHONPATH=root, **{env: "1"})
     r = subprocess.run([sys.executable, "-c", code, str(tmp_path)], capture_output=True, text=True,
                        env=env, timeout=300)
