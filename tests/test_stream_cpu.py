@@ -49,14 +49,17 @@ def test_torch_save_through_stream_is_byte_identical(tmp_path, slots, slot_bytes
 @pytest.mark.parametrize("sizes", [[0], [1], [4095], [4096], [4097], [3 * 65536 + 5],
                                    [1] * 5000, [65536, 0, 3, 65533, 70000, 4096 * 17 + 1]])
 @pytest.mark.parametrize("slots", [1, 2])
-def test_raw_writes_concatenate(tmp_path, sizes, slots):
+@pytest.mark.parametrize("engine", ["uring", "pwrite"])
+def test_raw_writes_concatenate(tmp_path, sizes, slots, engine):
     """Writes of any length (empty, 1 byte at a time, slot-crossing, exact
-    slot multiples) -> the file is their concatenation."""
+    slot multiples) -> the file is their concatenation, with either engine
+    (io_uring, or the O_DIRECT pwrite thread pool)."""
     g = torch.Generator().manual_seed(sum(sizes) + slots)
     parts = [torch.randint(0, 256, (n,), dtype=torch.uint8, generator=g).numpy().tobytes()
              for n in sizes]
     p = str(tmp_path / "raw.bin")
-    w = fp.StreamWriter(p, io_buffer_bytes=65536, ring_slots=slots, sqe_bytes=8192)
+    w = fp.StreamWriter(p, io_buffer_bytes=65536, ring_slots=slots, sqe_bytes=8192,
+                        io_depth=4, io_engine=engine)
     for b in parts:
         assert w.write(b) == len(b)
     st = w.close()
