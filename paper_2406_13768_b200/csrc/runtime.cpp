@@ -1544,6 +1544,15 @@ int fp_stream_close(fp_stream* s, fp_stream_stats* st) {
   const uint64_t pre = s->fill / A * A, suf = s->fill - pre;
   if (!s->status && pre) stream_submit(s, s->cur, pre, s->slot_off);
   for (uint32_t i = 0; i < s->cfg.ring_slots; ++i) stream_wait_slot(s, i);
+  // after an error: drop what was never queued and let every request the
+  // engine holds complete before the buffer is reused or freed
+  s->pending.clear();
+  while (s->inflight) {
+    IoDone done[64];
+    const int k = s->io->reap(done, 64, 1);
+    if (k <= 0) break;
+    s->inflight -= (uint32_t)k;
+  }
   if (!s->status && suf) {
     // the < alignment suffix through a buffered descriptor of the same file
     int bfd = open(s->path.c_str(), O_WRONLY);

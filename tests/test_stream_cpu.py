@@ -128,3 +128,24 @@ def test_save_serializer_switches(tmp_path):
         tcfg.save.compute_crc32 = True
     assert open(p, "rb").read() == ref
     assert torch.equal(torch.load(p)["w"], obj["w"])
+
+
+@pytest.mark.skipif(not os.path.exists("/dev/full"), reason="needs /dev/full")
+@pytest.mark.parametrize("engine", ["uring", "pwrite"])
+def test_write_error_surfaces_and_close_drains(engine):
+    """A failing device (/dev/full: every write -ENOSPC) fails the stream on a
+    later write and again at close; close still drains the engine and frees
+    the stream (a new stream of the same shape reuses the buffer cleanly)."""
+    import errno
+    w = fp.StreamWriter("/dev/full", io_buffer_bytes=8192, io_engine=engine)
+    with pytest.raises(FastPersistError) as e:
+        for _ in range(50):
+            w.write(b"x" * 10000)
+    assert e.value.code == -errno.ENOSPC
+    with pytest.raises(FastPersistError):
+        w.close()
+    w2 = fp.StreamWriter("/dev/full", io_buffer_bytes=8192, io_engine=engine)
+    with pytest.raises(FastPersistError):
+        w2.write(b"y" * 100000)
+        w2.close()
+    w2.close()
