@@ -46,7 +46,7 @@ constexpr int kV4Unroll = 8;  // 256 thr x 8 x 16 B = 32 KiB = kTile per pass
 // Streaming accesses (SURVEY §8(a'): the pack must not evict the training
 // stream's L2 working set): loads bypass L1 and, like the stores, carry an
 // L2 evict-first policy — every byte is touched once (the slab is re-read by
-// the copy engine, but a 256 MiB group exceeds the 126 MB L2 anyway).
+// the copy engine, but a 1 GiB group exceeds the 126 MB L2 anyway).
 __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -679,9 +679,11 @@ __global__ void __launch_bounds__(kColWarps * 32, 1)
 //     lane's row in the same banks) and puts them back in order with a
 //     3-level register barrel shift — two slicing-by-4 chains per lane,
 //     lanes_combine; arrive on EMPTY as soon as the page is in registers.
-// 91 us per 256 MiB (0.90 of HBM for pack + CRC) vs 90 us for fp_pack_bulk
-// alone and 87.5 + 65.9 us for fp_pack_v4 + fp_crc_pages_tma
-// (profiles/r02_ncu_bulk_crc_q8.md). The protocol is model-checked under
+// 90 us per 256 MiB (0.90 of HBM for pack + CRC) — the bare packs' own time
+// at that size (fp_pack_bulk 90.1, fp_pack_v4 90.5 us, no CRC) — and 328 us per
+// 1 GiB launch (0.98, the default group size: a launch carries ~12 us of fixed
+// cost); fp_pack_v4 + fp_crc_pages_tma take 87.5 + 65.9 us per 256 MiB
+// (profiles/r02_pack_group_size.md, r02_ncu_bulk_crc_q8.md). The protocol is model-checked under
 // random schedules in tests/test_bulk_protocol_cpu.py.
 // The slab is written and read once (2 B of HBM per image byte): the CRC no
 // longer re-reads it (the separate fp_crc_pages_tma pass: +1 B per byte).

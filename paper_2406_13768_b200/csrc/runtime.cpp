@@ -936,7 +936,7 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
       for (auto& e : c->gds_ev)
         if (cudaEventCreate(&e) != cudaSuccess) return fail(FP_ECUDA);
     }
-    // The pack is short (a 256 MiB group is ~85 us of HBM time) and is what
+    // The pack is short (a 1 GiB group is ~0.33 ms of HBM time) and is what
     // feeds the ring: by default it runs at the GREATEST priority so its CTAs
     // are dispatched in the gaps of a saturating compute stream instead of
     // starving behind it; FP_CFG_PRIO_LOW selects the least priority.
