@@ -67,3 +67,20 @@ def test_shard_dirs_follow_pcie_affinity(monkeypatch):
     assert bench.pick_shard_dirs(2, [None, None], []) is None
     monkeypatch.setenv("FP_CKPT_DIRS", "/x,/y")
     assert bench.pick_shard_dirs(2, [None, None]) == ["/x", "/y"]
+
+
+def test_pack_traffic_covers_the_default_launch_shape():
+    """roofline.traffic comes from profiles/pack_traffic.json for the launch
+    shape bench.py runs by default (--pack bulk --pack-mib 1024): there must be
+    an ncu-measured entry for it, and it must be within [0.9, 1.1] of the
+    algorithmic bytes (2 B per slab byte; far above = wasted re-reads)."""
+    import json
+    import re
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = open(os.path.join(root, "bench.py")).read()
+    mib = int(re.search(r'"--pack-mib", type=int, default=(\d+)', src).group(1))
+    tr = json.load(open(os.path.join(root, "profiles", "pack_traffic.json")))["fp_pack_bulk_crc"]
+    ents = tr if isinstance(tr, list) else [tr]
+    hit = [e for e in ents if e["bytes_per_launch"] == mib << 21]
+    assert hit, f"no ncu traffic entry for {mib} MiB launches"
+    assert 0.9 <= hit[0]["dram_bytes"] / hit[0]["bytes_per_launch"] <= 1.1
