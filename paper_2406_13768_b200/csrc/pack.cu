@@ -37,6 +37,25 @@
 
 #include "fp_internal.h"
 
+// Debug builds (FP_NVCC_FLAGS=-DFP_KERNEL_ASSERTS): device-side checks of the
+// work-item invariants the kernels rely on (items inside their 32 KiB tile and
+// inside the group); a violation prints and traps (the launch then fails).
+#ifdef FP_KERNEL_ASSERTS
+#include <cstdio>
+#define FP_KASSERT(c)                                                               \
+  do {                                                                              \
+    if (!(c)) {                                                                     \
+      printf("FP_KASSERT %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,      \
+             (int)blockIdx.x, (int)threadIdx.x, #c);                                \
+      __trap();                                                                     \
+    }                                                                               \
+  } while (0)
+#else
+#define FP_KASSERT(c) \
+  do {                \
+  } while (0)
+#endif
+
 namespace fp {
 namespace {
 
@@ -775,6 +794,10 @@ __global__ void __launch_bounds__(bc_threads(kGroups), 1)
       }
     };
     auto fill = [&](uint32_t i, const TileDesc& d) {  // G2S of tile i's 16-B aligned item bodies
+      FP_KASSERT(d.lo <= d.hi);
+      FP_KASSERT(d.lo + lane >= d.hi ||
+                 (d.it.dst / kTile == tile_of(i) && d.it.dst % kTile + d.it.len <= kTile &&
+                  (uint64_t)d.it.dst + d.it.len <= gbytes));
       const uint32_t s = i % kBcStages;
       uint8_t* st = stages + (size_t)s * kTile;
       const uint32_t bar = smem_u32(&full[s]);
@@ -886,6 +909,7 @@ __global__ void __launch_bounds__(bc_threads(kGroups), 1)
           it = items[k];
         }
         const uint32_t off = it.dst % kTile;
+        FP_KASSERT(it.dst / kTile == tile_of(i) && off + it.len <= kTile);
         if (bulk_ok(it)) {
           const uint32_t body = it.len & ~15u;
           if ((uint32_t)t0 < it.len - body)
@@ -1143,6 +1167,7 @@ __global__ void __launch_bounds__(kLcWarps * 32, 1)
       // every item of the tile that meets the page, clipped to it
       for (uint32_t k = cur.lo; k < cur.hi; ++k) {
         const Item it = items[k];
+        FP_KASSERT(it.dst / kTile == pg / (kTile / 4096) && it.dst % kTile + it.len <= kTile);
         const uint32_t a = it.dst > p0 ? it.dst : p0;
         const uint32_t e = it.dst + it.len < p0 + plen ? it.dst + it.len : p0 + plen;
         if (a < e)
