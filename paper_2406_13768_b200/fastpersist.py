@@ -567,7 +567,12 @@ def save(obj, path, zip_crc32=True, pinned_d2h=False, **kw):
         w = StreamWriter(path, **kw)
         torch.save(obj, w)
         return w.close()
+    except BaseException:
+        if w is not None:   # free the stream; the original error is what propagates
+            try:
+                w.close()
+            except FastPersistError:
+                pass
+        raise
     finally:
         tcfg.save.compute_crc32, tcfg.save.use_pinned_memory_for_d2h = old
-        if w is not None:
-            w.close()

@@ -152,3 +152,13 @@ def test_write_error_surfaces_and_close_drains(engine):
     with pytest.raises(FastPersistError):
         w2.close()
     assert w2.close()["bytes"] > 0    # closed: the stats of the failed stream
+
+
+def test_save_error_propagates_and_restores_switches(tmp_path):
+    """An object torch.save cannot pickle: torch's own error propagates, the
+    stream is freed and torch's serializer switches are restored."""
+    from torch.utils.serialization import config as tcfg
+    with pytest.raises(Exception) as e:
+        fp.save({"f": lambda x: x}, str(tmp_path / "bad.pt"), zip_crc32=False)
+    assert not isinstance(e.value, FastPersistError)
+    assert tcfg.save.compute_crc32 is True
