@@ -280,6 +280,44 @@ def test_c2_gpt3_1p3b_full_size_parity(tmp_path):
     os.remove(path)          # pytest keeps tmp dirs: do not leave 21 GB on the disk
 
 
+@pytest.mark.slow
+@pytest.mark.timeout(1500)
+def test_c2_gpt3_1p3b_full_size_dp8_thread_ranks(tmp_path):
+    """BASELINE configs[1] at DP=8, full size: 8 DP ranks as threads sharing
+    this GPU (one Checkpointer, helper thread, io_uring and 1 GiB slab each,
+    collectives through ThreadComm) write the 21 GB image split 8 ways in the
+    bench launch configuration; every shard's sha256 == the oracle's shard of
+    the same tensors, and rank 0's manifest lists all 8 with their CRC-32s."""
+    import json
+    free = os.statvfs(str(tmp_path))
+    if free.f_bavail * free.f_frsize < 25e9:
+        pytest.skip("needs ~25 GB free disk")
+    k = 8
+    st = _state("c2_gpt3_1.3b")
+    lay = oracle_layout([st] * k, k, lazy=True)
+    comms = ThreadComm.group(k)
+    cks = [fp.Checkpointer(DEV, comm=comms[r]) for r in range(k)]
+    try:
+        stats = run_threads([lambda r=r: cks[r].save(entries(st), str(tmp_path))
+                             for r in range(k)])
+        assert all(x["image_bytes"] == lay.image_bytes for x in stats)
+        assert sum(x["shard_bytes"] for x in stats) == lay.image_bytes
+        man = json.load(open(os.path.join(str(tmp_path), "manifest.json")))
+        assert len(man["shards"]) == k
+        for r in range(k):
+            path = os.path.join(str(tmp_path), fpck.shard_name(r, k))
+            assert file_sha(path) == fpck.shard_sha256(lay, r), r
+            assert man["shards"][r]["crc32"] == stats[r]["shard_crc32"], r
+            os.remove(path)  # pytest keeps tmp dirs: do not leave 21 GB behind
+    finally:
+        for c in cks:
+            c.close()
+        for f in os.listdir(str(tmp_path)):
+            if f.endswith(".fpck"):
+                os.remove(os.path.join(str(tmp_path), f))
+        torch.cuda.empty_cache()
+
+
 def _one_rank_of_8_full_size(tmp_path, cfg, rank, need_bytes, tmpfs_ok=False):
     """BASELINE configs that need 8 GPUs: rank `rank` of DP=8 on this GPU
     (MirrorComm answers its collectives exactly, see tests/_util.py), in the
