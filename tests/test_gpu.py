@@ -441,6 +441,46 @@ def test_load_parallel_device(tmp_path, monkeypatch, cfg, k, slot, exchange):
             c.close()
 
 
+@pytest.mark.slow
+@pytest.mark.timeout(1500)
+def test_c2_full_size_load_parallel_dp4_thread_ranks(tmp_path):
+    """SURVEY f1 at full size: C2 (21 GB) saved by 4 DP ranks, then restored
+    with the paper's two-step load — each rank reads only its own
+    5.3 GB shard into its device buffer and the partitions are exchanged over
+    peer memory into every rank's own copy of the state — bit-exact on all 4
+    ranks (thread ranks on one GPU: ~130 GB of device memory)."""
+    free_dev = torch.cuda.mem_get_info(DEV)[0]
+    if free_dev < 140e9:
+        pytest.skip("needs ~140 GB of free device memory")
+    free = os.statvfs(str(tmp_path))
+    if free.f_bavail * free.f_frsize < 25e9:
+        pytest.skip("needs ~25 GB free disk")
+    k = 4
+    st = _state("c2_gpt3_1.3b")
+    comms = ThreadComm.group(k)
+    cks = [fp.Checkpointer(DEV, comm=comms[r]) for r in range(k)]
+    try:
+        run_threads([lambda r=r: cks[r].save(entries(st), str(tmp_path)) for r in range(k)])
+        dst = [[(s, torch.zeros_like(t)) for s, t in st] for _ in range(k)]
+        streams = [torch.cuda.Stream(DEV) for _ in range(k)]
+        res = run_threads([lambda r=r: cks[r].load_parallel(entries(dst[r]), str(tmp_path),
+                                                            stream=streams[r]) for r in range(k)])
+        torch.cuda.synchronize()
+        assert [x["exchange"] for x in res] == ["peer"] * k
+        assert all(x["status"] == 0 for x in res)
+        for r in range(k):
+            for (_, a), (_, b) in zip(st, dst[r]):
+                assert torch.equal(a.reshape(-1).view(torch.uint8), b.reshape(-1).view(torch.uint8))
+            dst[r] = None
+    finally:
+        for c in cks:
+            c.close()
+        for f in os.listdir(str(tmp_path)):
+            if f.endswith(".fpck"):
+                os.remove(os.path.join(str(tmp_path), f))
+        torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("exchange", ["peer", "nccl"])
 def test_load_parallel_device_detects_payload_corruption(tmp_path, monkeypatch, exchange):
     """The own-shard CRC-32 (GPU kernels over the H2D'd chunk) is checked
