@@ -793,3 +793,20 @@ def test_stream_torch_save_cuda_state(tmp_path):
     assert file_sha(p) == __import__("hashlib").sha256(ref.getvalue()).hexdigest()
     back = torch.load(p, map_location=DEV)
     assert all(torch.equal(back[k], v) for k, v in st.items())
+
+
+def test_stream_write_tensor_large(tmp_path):
+    """2 GiB + a ragged tail of device bytes through 128 MiB double-buffered
+    IO buffers (many engine requests pending per slot): the file == the
+    tensor's bytes (sha256 on both sides)."""
+    import hashlib
+    n = (2 << 30) + 4093
+    g = torch.Generator(device=DEV).manual_seed(77)
+    t = torch.randint(0, 256, (n,), dtype=torch.uint8, device=DEV, generator=g)
+    p = str(tmp_path / "big.bin")
+    w = fp.StreamWriter(p, io_buffer_bytes=128 << 20, ring_slots=2, device=0)
+    w.write_tensor(t)
+    st = w.close()
+    assert st["bytes"] == n and st["suffix_bytes"] == n % 4096
+    assert file_sha(p) == hashlib.sha256(t.cpu().numpy().tobytes()).hexdigest()
+    os.remove(p)
