@@ -677,12 +677,17 @@ def our_arm(a):
                        "nvme_read_gbs": round(nvme_read, 3),
                        "frac": round(image_bytes / rt / 1e9 / nvme_read, 4),
                        "call": "fp_ckpt_load_parallel (own shard O_DIRECT read-ahead over the "
-                               "pinned ring -> H2D -> all-gather -> unpack kernel, CRC-32 checked)",
+                               "pinned ring -> H2D -> exchange of the partitions (peer memory, "
+                               "or all-gather) -> unpack kernel, CRC-32 checked)",
                        "exchange": rinfo.get("exchange"),
                        # host time blocked on this rank's own-shard reads in the
                        # last call: ~t_total when the storage is the bound
                        "t_read_wait_s": round(rinfo.get("t_read_wait", 0.0), 4),
                        "t_total_s": round(rinfo.get("t_total", 0.0), 4),
+                       # rank 0's wait for the other writers' chunks (N > 1),
+                       # and its setup (buffers, IPC mapping) in the last call
+                       "t_exchange_wait_s": round(rinfo.get("t_exchange_wait", 0.0), 4),
+                       "t_setup_s": round(rinfo.get("t_setup", 0.0), 4),
                        "roofline_how": f"fp_io_bench_read: O_DIRECT io_uring seq read, {a.qd} x "
                                        f"{a.sqe_kib} KiB in flight, best of 2, {world} concurrent "
                                        f"readers x {nv_bytes} B, same dirs, same run"}
