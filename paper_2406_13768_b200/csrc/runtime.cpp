@@ -924,9 +924,20 @@ int fp_ckpt_init(const fp_config* cfg_in, int cuda_device, const fp_comm* comm, 
     c->ring_cuda_registered = true;
     if (cudaHostGetDevicePointer((void**)&c->d_ring, c->ring, 0) != cudaSuccess)
       return fail(FP_ECUDA);
-    // GDS doubles the slab: group g+1 is packed while group g is written
-    const size_t slab_bytes = (size_t)cfg.pack_bytes * (c->gds ? 2 : 1);
-    if (cudaMalloc(&c->d_slab, slab_bytes) != cudaSuccess) return fail(-ENOMEM);
+    // GDS doubles the slab: group g+1 is packed while group g is written.
+    // A device too full for the default 1 GiB group (training state near
+    // the 180 GB) gets a smaller one: halved down to one ring chunk, the
+    // pack group size in use is what c->cfg.pack_bytes reports.
+    size_t slab_bytes = 0;
+    for (;;) {
+      slab_bytes = (size_t)cfg.pack_bytes * (c->gds ? 2 : 1);
+      if (cudaMalloc(&c->d_slab, slab_bytes) == cudaSuccess) break;
+      cudaGetLastError();
+      c->d_slab = nullptr;
+      if (cfg.pack_bytes <= cfg.slot_bytes) return fail(-ENOMEM);
+      cfg.pack_bytes = std::max<uint64_t>(cfg.slot_bytes, round_up(cfg.pack_bytes / 2, cfg.slot_bytes));
+    }
+    c->cfg.pack_bytes = cfg.pack_bytes;
     if (c->gds) {
       c->gds_slab_registered = gds_buf_register(c->d_slab, slab_bytes) == 0;  // best effort
       c->gds_pool = gds_pool_new(std::min<uint32_t>(cfg.io_depth, 16), cuda_device);

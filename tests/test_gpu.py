@@ -810,3 +810,22 @@ def test_stream_write_tensor_large(tmp_path):
     assert st["bytes"] == n and st["suffix_bytes"] == n % 4096
     assert file_sha(p) == hashlib.sha256(t.cpu().numpy().tobytes()).hexdigest()
     os.remove(p)
+
+
+def test_slab_falls_back_to_a_smaller_group_when_memory_is_short(tmp_path):
+    """A device too full for the requested pack group: fp_ckpt_init halves
+    the slab down to what fits (here 2 GiB -> 128 MiB with ~200 MiB free),
+    the checkpoint runs with the smaller groups and is still == oracle."""
+    st = _state("gpt3_small")
+    lay = oracle_layout([st], 1)
+    torch.cuda.empty_cache()
+    free = torch.cuda.mem_get_info(DEV)[0]
+    filler = torch.empty(free - (200 << 20), dtype=torch.uint8, device=DEV)
+    try:
+        with fp.Checkpointer(DEV, slot_bytes=16 << 20, pack_bytes=2 << 30) as ck:
+            s = ck.save(entries(st), str(tmp_path))
+        assert s["pack_launches"] == -(-lay.image_bytes // (128 << 20)) > 1
+        _check_rank_files(str(tmp_path), lay, 1)
+    finally:
+        del filler
+        torch.cuda.empty_cache()
